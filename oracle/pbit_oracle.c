@@ -1,0 +1,202 @@
+/*
+ * oracle/pbit_oracle.c -- TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, single-threaded CPU implementation of Pbit exactly as the paper
+ * (arXiv cs/0511020, /root/reference/PAPER.md, cited "P:<line>") defines it, on
+ * node arrays instead of pointers.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code, header, table or constant with the CUDA path
+ * (paper_cs_0511020_b200/csrc); neither includes nor links the other.
+ *
+ * Representation (reading Q9 in DESIGN.md): a node is an index v in [0, n);
+ * the paper's `L->next` is next[v] (u32) and its NULL (P:8) is 0xFFFFFFFF;
+ * the paper's `L->data` is key[v], an unsigned M-bit integer (M = 8/16/32/64).
+ *
+ * Every function cites the passage it follows.  Pinned by tests/test_oracle.py
+ * against: the worked example (tests/golden/), bits(123,3)=15
+ * (P:179-182), brute force over all link orders for n <= 6 (a stable sort of
+ * the list-order sequence), seeded random lists vs numpy's stable argsort, the
+ * counter identities relinks = n*M/K and merge visits = n,
+ * the depth/live-table bound M/K with the memory formula T,
+ * direction duality and the reverse-stability of odd M/K (Q1).
+ * Nothing here is "parity unpinned".
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORACLE_NULL 0xFFFFFFFFu
+
+enum { ORACLE_OK = 0, ORACLE_ERR_ARG = 1, ORACLE_ERR_LIST = 2, ORACLE_ERR_OOM = 3 };
+
+/* Operation counters (SPEC metrics module).  Filled when non-NULL. */
+typedef struct {
+    uint64_t relinks;        /* +1 per node pushed into tab[] by the split loop   */
+    uint64_t merge_visits;   /* +1 per node walked inside merge, exactly as the listing P:310-320 */
+    uint32_t max_depth;      /* deepest active Pbit call (levels), <= M/K                        */
+    uint32_t max_live_tabs;  /* most root tables tab[Omega] alive at once, <= M/K        */
+    uint64_t bucket_scans;   /* tab slots visited by the loops of listing lines 8-9  */
+} oracle_counters;
+
+typedef struct {
+    const uint8_t *key;      /* node-indexed keys, key_bytes each, little-endian host order   */
+    int key_bytes;
+    uint32_t *next;          /* the list being relinked in place                      */
+    unsigned K;              /* pattern length                                      */
+    uint32_t omega;          /* Omega = 2^K                                            */
+    int descending;          /* 0: ascending loops P:379-380; 1: descending loops P:371-372    */
+    uint32_t *tabs;          /* (M/K) root tables of Omega slots, one per recursion level     */
+    uint32_t depth, live;
+    oracle_counters c;
+} ctx_t;
+
+/* The key of node v as an unsigned integer (the paper's L->data). */
+static uint64_t key_of(const ctx_t *x, uint32_t v) {
+    const uint8_t *p = x->key + (size_t)v * (size_t)x->key_bytes;
+    switch (x->key_bytes) {
+    case 1: return p[0];
+    case 2: { uint16_t k; memcpy(&k, p, 2); return k; }
+    case 4: { uint32_t k; memcpy(&k, p, 4); return k; }
+    default: { uint64_t k; memcpy(&k, p, 8); return k; }
+    }
+}
+
+/* bits(number, M) = (number div 2^M) mod Omega, written in C as
+ * (number >> M) & (Omega - 1). */
+uint64_t oracle_bits(uint64_t number, unsigned M, unsigned K) {
+    uint64_t omega = (uint64_t)1 << K;
+    return (number >> M) & (omega - 1);
+}
+
+/* merge(A, B): splice list B behind the tail of list A; return the head.
+ * Instrumented exactly as P:310-320: count the first node, then each advance. */
+static uint32_t merge(ctx_t *x, uint32_t A, uint32_t B) {
+    if (A == ORACLE_NULL) return B;               /* line 2: if(A==0) return B;     */
+    x->c.merge_visits++;                          /* count++; first node (maybe only) */
+    uint32_t temp = A;                            /* line 3                          */
+    while (x->next[temp] != ORACLE_NULL) {        /* line 4: while(temp->next)       */
+        temp = x->next[temp];
+        x->c.merge_visits++;                      /* count++; n-node of list         */
+    }
+    x->next[temp] = B;                            /* line 5: temp->next = B          */
+    return A;                                     /* line 6                          */
+}
+
+/* Pbit(L, M, P) -- the listing of P:346-361 with the loop direction of P:371-372
+ * (descending) or P:379-380 (ascending).  `level` indexes the root table that the
+ * listing declares as a local (`Node *tab[Omega]={NULL};`). */
+static uint32_t Pbit(ctx_t *x, uint32_t L, unsigned M, uint32_t P, uint32_t level) {
+    if (L != ORACLE_NULL) {                                       /* 2: if(L){          */
+        M -= x->K;                                                /* 3: M-=K;           */
+        uint32_t *tab = x->tabs + (size_t)level * x->omega;       /* 4: tab[Omega]={NULL} */
+        for (uint32_t b = 0; b < x->omega; ++b) tab[b] = ORACLE_NULL;
+        x->depth++; x->live++;
+        if (x->depth > x->c.max_depth) x->c.max_depth = x->depth;
+        if (x->live > x->c.max_live_tabs) x->c.max_live_tabs = x->live;
+
+        /* 5: for(Node *i,**in; i=L; i->next=*in,*in=i){
+         * 6:     in = tab + ((L->data>>M) & (Omega-1));
+         * 7:     L = L->next; }
+         * i.e. a push-front of every node into tab[digit]. */
+        for (uint32_t i; (i = L) != ORACLE_NULL; ) {
+            uint32_t *in = tab + oracle_bits(key_of(x, L), M, x->K); /* line 6 */
+            L = x->next[L];                                          /* line 7 */
+            x->next[i] = *in; *in = i;                               /* for-increment */
+            x->c.relinks++;
+        }
+
+        if (M) {                                                  /* 8 */
+            if (x->descending)
+                for (uint32_t b = 0; b < x->omega; ++b) { x->c.bucket_scans++; P = Pbit(x, tab[b], M, P, level + 1); }
+            else
+                for (int64_t b = (int64_t)x->omega - 1; b >= 0; --b) { x->c.bucket_scans++; P = Pbit(x, tab[b], M, P, level + 1); }
+        } else {                                                  /* 9 */
+            if (x->descending)
+                for (uint32_t b = 0; b < x->omega; ++b) { x->c.bucket_scans++; P = merge(x, tab[b], P); }
+            else
+                for (int64_t b = (int64_t)x->omega - 1; b >= 0; --b) { x->c.bucket_scans++; P = merge(x, tab[b], P); }
+        }
+        x->depth--; x->live--;
+    }
+    return P;                                                     /* 10: return P; */
+}
+
+/* The paper assumes a well-formed list (P:8: the last pointer shows NULL).  The
+ * oracle rejects anything else before mutating (reading Q10): starting at head it
+ * must reach NULL after exactly n nodes, every index < n.  Reaching NULL after
+ * exactly n steps implies the n visited nodes are distinct (a repeat never ends). */
+int oracle_validate_list(const uint32_t *next, uint32_t head, uint64_t n) {
+    if (n == 0) return head == ORACLE_NULL ? ORACLE_OK : ORACLE_ERR_LIST;
+    uint64_t steps = 0;
+    uint32_t v = head;
+    while (v != ORACLE_NULL) {
+        if ((uint64_t)v >= n || steps >= n) return ORACLE_ERR_LIST;
+        ++steps;
+        v = next[v];
+    }
+    return steps == n ? ORACLE_OK : ORACLE_ERR_LIST;
+}
+
+/* Sort the list (head, next[]) of n nodes by its M = key_bits unsigned keys with
+ * pattern length K; the result goes to (*out_head, out_next[]).  out_next may
+ * alias next.  Unsigned entry of the dispatcher P:444-466 (lines 14-15):
+ * size = sizeof(data)<<3, then Pbit_ascending / Pbit_decreasing. */
+int oracle_pbit_sort(const void *keys, int key_bits, const uint32_t *next, uint32_t head,
+                     uint64_t n, unsigned K, int descending,
+                     uint32_t *out_head, uint32_t *out_next, oracle_counters *counters) {
+    if (!out_head || (n && (!keys || !next || !out_next))) return ORACLE_ERR_ARG;
+    if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return ORACLE_ERR_ARG;
+    if (K < 1 || K > 16 || (key_bits % K) != 0) return ORACLE_ERR_ARG;   /* reading Q7 */
+    if (n > 0xFFFFFFFFull) return ORACLE_ERR_ARG;
+    int rc = oracle_validate_list(next, head, n);
+    if (rc) return rc;
+
+    ctx_t x;
+    memset(&x, 0, sizeof x);
+    x.key = (const uint8_t *)keys;
+    x.key_bytes = key_bits / 8;
+    x.K = K;
+    x.omega = 1u << K;
+    x.descending = descending;
+    unsigned levels = (unsigned)key_bits / K;
+    x.tabs = (uint32_t *)malloc((size_t)levels * x.omega * sizeof(uint32_t));
+    if (!x.tabs) return ORACLE_ERR_OOM;
+    if (out_next != next && n) memcpy(out_next, next, (size_t)n * sizeof(uint32_t));
+    x.next = out_next;
+
+    *out_head = Pbit(&x, head, (unsigned)key_bits, ORACLE_NULL, 0);
+
+    free(x.tabs);
+    if (counters) *counters = x.c;
+    return ORACLE_OK;
+}
+
+/* First split only (P:351-353 at the top level, M -= K once): fills tab[Omega] with
+ * the bucket heads and relinks next[] in place.  Exposed so tests can pin the
+ * worked example's first-level groups. */
+int oracle_split_once(const void *keys, int key_bits, uint32_t *next, uint32_t head,
+                      uint64_t n, unsigned K, uint32_t *tab) {
+    if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return ORACLE_ERR_ARG;
+    if (K < 1 || K > 16 || (key_bits % K) != 0) return ORACLE_ERR_ARG;
+    int rc = oracle_validate_list(next, head, n);
+    if (rc) return rc;
+    ctx_t x;
+    memset(&x, 0, sizeof x);
+    x.key = (const uint8_t *)keys; x.key_bytes = key_bits / 8; x.K = K; x.omega = 1u << K;
+    x.next = next;
+    unsigned M = (unsigned)key_bits - K;
+    for (uint32_t b = 0; b < x.omega; ++b) tab[b] = ORACLE_NULL;
+    uint32_t L = head;
+    for (uint32_t i; (i = L) != ORACLE_NULL; ) {
+        uint32_t *in = tab + oracle_bits(key_of(&x, L), M, K);
+        L = next[L];
+        next[i] = *in; *in = i;
+    }
+    return ORACLE_OK;
+}
+
+/* The paper's memory formula T = (Omega*4 + 3*4) * M/K + 2*4 bytes. */
+uint64_t oracle_memory_bound_T(unsigned M, unsigned K) {
+    uint64_t omega = (uint64_t)1 << K;
+    return (omega * 4 + 3 * 4) * (M / K) + 2 * 4;
+}

@@ -1,0 +1,218 @@
+"""Pins of the CPU oracle (oracle/pbit_oracle.c) against what the paper and the
+mathematics fix -- never against the oracle itself.  CPU only."""
+from __future__ import annotations
+
+import itertools
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import workloads
+from tests.listcheck import (NULL, check_sorted_list_properties, expected_by_definition,
+                             expected_by_definition_small, walk)
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "worked_example.txt")
+
+
+def _golden():
+    d = {}
+    for line in open(GOLDEN):
+        line = line.strip()
+        if not line or line.startswith("#"):
+            continue
+        k, v = line.split(None, 1)
+        d[k] = v
+    return d
+
+
+def _chain(keys):
+    n = len(keys)
+    nxt = np.array(list(range(1, n)) + [NULL], np.uint32) if n else np.zeros(0, np.uint32)
+    return nxt, (0 if n else NULL)
+
+
+# ---------------------------------------------------------------- worked example P:84-98
+def test_worked_example_output():
+    g = _golden()
+    keys = np.array([int(x) for x in g["input"].split()], np.uint8)
+    nxt, head = _chain(keys)
+    h, out = oracle.pbit_sort(keys, nxt, head, int(g["key_bits"]), int(g["K"]))
+    seq = walk(out, h)
+    assert [int(keys[v]) for v in seq] == [int(x) for x in g["output"].split()]
+    # stability: the 3 at input position 1 precedes the 3 at input position 6
+    val, pos = g["equal_key_positions"].split(":")
+    assert [v for v in seq if keys[v] == int(val)] == [int(p) for p in pos.split(",")]
+
+
+def test_worked_example_first_level_groups():
+    g = _golden()
+    keys = np.array([int(x) for x in g["input"].split()], np.uint8)
+    nxt, head = _chain(keys)
+    tab, relinked = oracle.split_once(keys, nxt, head, 8, 4)
+    want = {int(b): sorted(int(x) for x in ks.split(",")) for b, ks in
+            (t.split(":") for t in g["level1"].split())}
+    got = {b: sorted(int(keys[v]) for v in walk(relinked, tab[b])) for b in range(16) if tab[b] != NULL}
+    assert got == want
+    # push-front leaves each bucket in reverse input order
+    assert walk(relinked, tab[0]) == [6, 3, 1]
+
+
+def test_bits_paper_example():
+    # 123 / 8 = 15.375 -> 01111011 >> 3 = 00001111 = 15 (mod 16 keeps 15)
+    assert oracle.bits(123, 3, 4) == 15
+    assert oracle.bits(209, 4, 4) == 13 and oracle.bits(214, 4, 4) == 13  # P:91 group {209,214}
+    assert oracle.bits(0xABCDEF12, 28, 4) == 0xA
+    assert oracle.bits(0xFFFFFFFFFFFFFFFF, 56, 8) == 0xFF
+
+
+def test_memory_formula_paper_values():
+    # P:129-131 T(8)=160, T(32)=616; P:981-982 K=8: 4152
+    assert oracle.memory_bound_T(8, 4) == 160
+    assert oracle.memory_bound_T(32, 4) == 616
+    assert oracle.memory_bound_T(32, 8) == 4152
+
+
+# ---------------------------------------------------------------- brute force
+ALPHABETS = {
+    8: [0x00, 0x0F, 0x10, 0xFF, 0x7F, 0x80],
+    16: [0x0000, 0x00FF, 0xFF00, 0xFFFF, 0x0F0F],
+    32: [0, 1, 0x10, 0xFFFFFFFF, 0x80000000, 0x0000FFFF],
+    64: [0, 0xFFFFFFFFFFFFFFFF, 0x8000000000000000, 0x00000000FFFFFFFF, 0x10],
+}
+
+
+@pytest.mark.parametrize("key_bits", [8, 16, 32, 64])
+def test_brute_force_all_link_orders(key_bits):
+    """Every link order of n <= 6 nodes, keys from an adversarial alphabet (extreme
+    digits, duplicates) vs python's stable sorted() of the list-order sequence."""
+    rng = np.random.default_rng(key_bits)
+    alpha = ALPHABETS[key_bits]
+    dt = {8: np.uint8, 16: np.uint16, 32: np.uint32, 64: np.uint64}[key_bits]
+    for n in range(0, 7):
+        keys = np.array([alpha[i] for i in rng.integers(0, len(alpha), n)], dt)
+        perms = list(itertools.permutations(range(n)))
+        if len(perms) > 240:
+            perms = [perms[i] for i in rng.choice(len(perms), 240, replace=False)]
+        for perm in perms:
+            nxt = np.full(n, NULL, np.uint32)
+            for a, b in zip(perm[:-1], perm[1:]):
+                nxt[a] = b
+            head = perm[0] if n else NULL
+            h, out = oracle.pbit_sort(keys, nxt, head, key_bits, 4)
+            eh, eout = expected_by_definition_small(keys, nxt, head)
+            assert h == eh and np.array_equal(out, eout), (n, perm, keys)
+
+
+@pytest.mark.parametrize("key_bits,keys_kind,links", [
+    (8, "uniform", "random"), (16, "uniform", "random"), (32, "uniform", "random"),
+    (32, "zipf", "random"), (64, "uniform", "random"), (64, "runs4096", "random"),
+    (32, "equal", "random"), (32, "max", "identity"), (32, "sorted", "push"),
+    (32, "reverse", "random"), (8, "uniform", "push"), (16, "uniform", "identity"),
+])
+@pytest.mark.parametrize("n", [1, 2, 3, 10, 100, 2048, 4099, 70001])
+def test_seeded_random_lists_vs_stable_argsort(key_bits, keys_kind, links, n):
+    li = workloads.make_list(n, key_bits, seed=n * 7 + key_bits, keys=keys_kind, links=links)
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li)
+    assert oracle.validate_list(nxt, li.head)
+    h, out, cnt = oracle.pbit_sort(keys, nxt, li.head, key_bits, 4, with_counters=True)
+    eh, eout = expected_by_definition(keys, li.order.numpy())
+    assert h == eh and np.array_equal(out, eout)
+    check_sorted_list_properties(keys, li.order.numpy(), h, out)
+    # P:73 / P:328-330: n*M/K relinks and exactly n merge visits
+    assert cnt["relinks"] == n * key_bits // 4
+    assert cnt["merge_visits"] == n
+
+
+# ---------------------------------------------------------------- counter identities
+@pytest.mark.parametrize("key_bits,K", [(8, 4), (32, 4), (32, 8), (64, 4), (32, 16), (16, 2)])
+def test_counter_identities_and_depth(key_bits, K):
+    n = 5000
+    li = workloads.make_list(n, key_bits, seed=5, keys="uniform")
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li)
+    _, _, c = oracle.pbit_sort(keys, nxt, li.head, key_bits, K, with_counters=True)
+    assert c["relinks"] == n * (key_bits // K)          # split term of f(n)
+    assert c["merge_visits"] == n                       # "Always count equal n"
+    assert c["max_depth"] == key_bits // K              # M/K levels
+    assert c["max_live_tabs"] <= key_bits // K          # at most M/K root tables
+    omega = 1 << K
+    assert c["max_live_tabs"] * omega * 4 <= oracle.memory_bound_T(key_bits, K)
+
+
+def test_counters_empty_and_single():
+    _, _, c = oracle.pbit_sort(np.zeros(0, np.uint32), np.zeros(0, np.uint32), NULL, 32, 4, with_counters=True)
+    assert c["relinks"] == 0 and c["merge_visits"] == 0
+    h, out, c = oracle.pbit_sort(np.array([7], np.uint32), np.array([NULL], np.uint32), 0, 32, 4,
+                                 with_counters=True)
+    assert h == 0 and out[0] == NULL and c["relinks"] == 8 and c["merge_visits"] == 1
+
+
+# ---------------------------------------------------------------- direction + parity readings
+def test_descending_duality_distinct_keys():
+    """P:371-374 (loops 0..Omega-1) sort descending; with distinct keys it is the
+    exact reverse of ascending (SPEC direction duality)."""
+    n = 3000
+    li = workloads.make_list(n, 32, seed=9, keys="uniform")
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li)
+    assert len(np.unique(keys)) == n
+    ha, oa = oracle.pbit_sort(keys, nxt, li.head, 32, 4)
+    hd, od = oracle.pbit_sort(keys, nxt, li.head, 32, 4, descending=True)
+    assert walk(od, hd) == walk(oa, ha)[::-1]
+
+
+def test_descending_stable_with_duplicates():
+    n = 4000
+    li = workloads.make_list(n, 16, seed=11, keys="uniform", key_range=50)
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li)
+    hd, od = oracle.pbit_sort(keys, nxt, li.head, 16, 4, descending=True)
+    eh, eo = expected_by_definition(keys, li.order.numpy(), descending=True)
+    assert hd == eh and np.array_equal(od, eo)
+
+
+def test_odd_levels_are_reverse_stable():
+    """Reading Q1: the push-front split reverses equal digits once per level, so the
+    literal listing is stable only when M/K is even.  M=8, K=8 (one level) must
+    reverse the order of equal keys -- documents why the oracle uses K=4."""
+    keys = np.array([5, 5, 1, 5], np.uint8)
+    nxt, head = _chain(keys)
+    h, out = oracle.pbit_sort(keys, nxt, head, 8, 8)
+    assert walk(out, h) == [2, 3, 1, 0]
+    h, out = oracle.pbit_sort(keys, nxt, head, 8, 4)   # M/K = 2: stable
+    assert walk(out, h) == [2, 0, 1, 3]
+
+
+# ---------------------------------------------------------------- invalid lists
+def test_invalid_lists_rejected():
+    keys = np.arange(4, dtype=np.uint32)
+    bad = {
+        "cycle_through_head": (np.array([1, 2, 3, 0], np.uint32), 0),
+        "cycle_off_path": (np.array([1, NULL, 3, 2], np.uint32), 0),
+        "short": (np.array([1, 2, NULL, NULL], np.uint32), 0),
+        "index_ge_n": (np.array([1, 9, 3, NULL], np.uint32), 0),
+        "head_ge_n": (np.array([1, 2, 3, NULL], np.uint32), 4),
+        "empty_head_not_null": (np.zeros(0, np.uint32), 0),
+    }
+    for name, (nxt, head) in bad.items():
+        k = keys[: len(nxt)] if len(nxt) else np.zeros(1, np.uint32)
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.pbit_sort(k, nxt, head, 32, 4)
+        assert e.value.code == 2, name
+
+
+def test_invalid_args_rejected():
+    keys = np.arange(4, dtype=np.uint32)
+    nxt = np.array([1, 2, 3, NULL], np.uint32)
+    for kb, K in [(24, 4), (32, 3), (32, 0), (8, 16)]:
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.pbit_sort(keys, nxt, 0, kb, K)
+        assert e.value.code == 1
+
+
+def test_in_place_alias():
+    """out_next may alias next: the paper relinks in situ."""
+    li = workloads.make_list(1000, 32, seed=3, keys="uniform", key_range=17)
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li).copy()
+    h, out = oracle.pbit_sort(keys, nxt, li.head, 32, 4, out=nxt)
+    eh, eo = expected_by_definition(keys, li.order.numpy())
+    assert h == eh and np.array_equal(nxt, eo) and np.shares_memory(out, nxt)
