@@ -1,0 +1,346 @@
+#!/usr/bin/env python
+"""bench.py -- sorted list nodes/s on B200 (BASELINE.json metric), one JSON line.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl ours|reference]
+
+A step is one pbit_sort_list call (the whole hot path) on the
+configured synthetic list, inputs resident in HBM.  Default workload: C3 (n = 2^28
+u32 Zipf(1.1) keys, random-permutation links) -- the 1-GPU config the north star gates
+on.  Inputs (2 GiB) are larger than L2 (126 MB), so no explicit flush is needed.
+
+N > 1 (torchrun): every rank sorts its own C3-shaped list (independent problems, weak
+scaling); value = all ranks' nodes / max-over-ranks time.
+
+--impl reference: the CPU oracle (the paper's algorithm, oracle/) timed on the host on
+bounded samples of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sorted list nodes/sec at 1/2/4/8 B200; achieved HBM GB/s vs peak"
+UNIT = "nodes/s"
+
+# Algorithmic bytes per node of each kernel phase: every
+# array element the phase must read or write, counted once at element size.
+#   kb = key bytes as stored in the pass buffers (4 for u8/u16/u32, 8 for u64)
+def phase_bytes_per_node(key_bits: int):
+    kin = key_bits // 8
+    kb = 8 if key_bits == 64 else 4
+    rec = 16 if key_bits == 64 else 8
+    return {
+        "pack": kin + 4 + rec,          # read key, next; write AoS record
+        "walk": rec + (kb + 4),         # read record (random), write (key,id) to its slot
+        "rank": 0,                      # per-ruler, ~n/64 entries: not per node
+        "gather": (kb + 4) * 2,         # read slot, write list-order key + id
+        "pass": (kb + 4) * 2,           # read key+id, write key+id
+        "pass_last": (kb + 4) + 4,      # read key+id, write id
+        "relink": 4 + 4,                # read sorted ids, write out_next (random)
+    }
+
+
+def method_bytes_per_node(key_bits: int):
+    """The one-read-one-write lower bound of the method: read key and next, write
+    out_next."""
+    return key_bits // 8 + 4 + 4
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.25)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = max(mx, float(f[1]))
+            except ValueError:
+                continue
+            for name, v in zip(names, f[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(cfg: str, sample_n: int, reps: int = 1):
+    """The oracle as it stands (paper-literal Pbit, K=4, one thread) on a bounded
+    sample of the workload."""
+    import oracle
+    import workloads
+    c = workloads.CONFIGS[cfg]
+    li = workloads.make_config(cfg, n=sample_n)
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li)
+    oracle.build()
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        oracle.pbit_sort(keys, nxt, li.head, c["key_bits"], 4)
+        ts.append(time.perf_counter() - t0)
+    t = statistics.mean(ts)
+    return {"value": sample_n / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"{cfg}-shaped list, n={sample_n} (seed {c['seed']}), paper-literal Pbit K=4, "
+                      f"mean of {reps} run(s), {t:.2f} s each, single thread"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("gloo")
+        if rank != 0:
+            dist.barrier()
+            dist.destroy_process_group()
+            return
+    import workloads
+    c = workloads.CONFIGS[args.config]
+    sample_n = min(c["n"], args.ref_sample)
+    import oracle
+    li = workloads.make_config(args.config, n=sample_n)
+    keys, nxt = workloads.keys_numpy(li), workloads.next_numpy(li)
+    oracle.build()
+    for _ in range(args.warmup):
+        oracle.pbit_sort(keys, nxt, li.head, c["key_bits"], 4)
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        oracle.pbit_sort(keys, nxt, li.head, c["key_bits"], 4)
+        ts.append(time.perf_counter() - t0)
+    t = sum(ts) / len(ts)
+    value = sample_n / t
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "u32" if c["key_bits"] <= 32 else "u64",
+            "data": "synthetic", "config": {"workload": args.config, "desc": c["desc"], "n": sample_n,
+                                            "note": "bounded sample of the workload (oracle is single-threaded)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": f"{args.config}-shaped list n={sample_n}, paper-literal Pbit K=4, "
+                                       f"{args.steps} timed steps"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def load_traffic(cfg: str):
+    """ncu dram bytes per launch for the config's kernels, from the committed profile
+    summary (profiles/traffic_<cfg>.json written by tools/ncu_summary.py)."""
+    p = os.path.join(ROOT, "profiles", f"traffic_{cfg}.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0511020_b200 as pbit
+    import workloads
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    c = workloads.CONFIGS[args.config]
+    K = args.digit_bits or c["digit_bits"]
+    n = c["n"] if args.n is None else args.n
+    li = workloads.make_config(args.config, device="cuda", n=n, seed=c["seed"] + 1000 * rank)
+    keys, nxt, head, kb = li.keys, li.next, li.head, li.key_bits
+    out = torch.empty_like(nxt)
+    st = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+
+    for _ in range(max(args.warmup, 3)):
+        pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out)
+    torch.cuda.synchronize()
+
+    # ---- timed region: K calls, device events on the launching stream
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            h, _ = pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out)
+        e1.record(st)
+        torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms_t = torch.tensor([ms], device="cuda")
+    if ws > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = n * ws / (ms_max / 1e3)
+
+    # ---- per-phase device time (same calls with events between kernels)
+    phases = {}
+    for _ in range(args.steps):
+        _, _, ph = pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out, timing=True)
+        for k_, v in ph.items():
+            phases[k_] = phases.get(k_, 0.0) + v
+    phases = {k_: v / args.steps for k_, v in phases.items()}
+    launches = int(phases.pop("launches"))
+    passes_run = int(phases.pop("passes_run"))
+
+    # ---- end to end through the same C-ABI with host (pinned) buffers
+    kh = keys.cpu().pin_memory()
+    nh = nxt.cpu().pin_memory()
+    oh = torch.empty_like(nh).pin_memory()
+    pbit.sort_list(kh, nh, head, out_next=oh, digit_bits=K)
+    barrier()
+    torch.cuda.synchronize()
+    e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        pbit.sort_list(kh, nh, head, out_next=oh, digit_bits=K)
+    e2e_s = (time.perf_counter() - t0) / e_steps
+    e2e_t = torch.tensor([e2e_s], device="cuda")
+    if ws > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_value = n * ws / float(e2e_t.item())
+
+    # ---- roofline of the dominant kernel
+    bpn = phase_bytes_per_node(kb)
+    pass_ms = [(k_, v) for k_, v in phases.items() if k_.startswith("pass")]
+    cand = {k_: v for k_, v in phases.items() if not k_.startswith("pass")}
+    for i, (k_, v) in enumerate(pass_ms):
+        cand[k_] = v
+    dom = max(cand, key=cand.get)
+    if dom.startswith("pass"):
+        last_idx = len(pass_ms) - 1
+        b = bpn["pass_last"] if dom == pass_ms[last_idx][0] else bpn["pass"]
+    else:
+        b = bpn[dom]
+    peak, peak_src = load_peaks()
+    dom_ms = cand[dom]
+    achieved = b * n / (dom_ms / 1e3) / 1e9
+    traffic = None
+    tr = load_traffic(args.config)
+    if tr and dom in tr:
+        traffic = tr[dom]
+    total_alg = sum(bpn["pass"] if k_.startswith("pass") else bpn.get(k_, 0) for k_ in cand)
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": dom,
+                "kernel_ms": round(dom_ms, 4), "alg_bytes_per_node": b, "peak_source": peak_src,
+                "phase_ms": {k_: round(v, 4) for k_, v in phases.items()},
+                "whole_call_impl_bytes_per_node": total_alg,
+                "whole_call_method_frac": round(method_bytes_per_node(kb) * n / (ms / 1e3) / 1e9 / peak, 4)}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args.config, min(n, args.cpu_sample))
+
+    clocks = clk.summary()
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u32" if kb <= 32 else "u64", "data": "synthetic",
+                "config": {"workload": args.config, "desc": c["desc"], "n_per_gpu": n, "key_bits": kb,
+                           "digit_bits": K, "passes_run": passes_run,
+                           "parallelism": "independent lists per GPU" if ws > 1 else "single GPU",
+                           "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6
+                           else "inputs smaller than L2"},
+                "hbm_gbs_method": round(method_bytes_per_node(kb) * n * ws / (ms_max / 1e3) / 1e9, 1),
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (kb // 8 + 4),
+                        "d2h_bytes_per_step": n * 4 + 4},
+                "gpu_launches": launches * args.steps, "clocks": clocks}
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3")
+    ap.add_argument("--n", type=int, default=None, help="override n (default: the config's)")
+    ap.add_argument("--digit-bits", type=int, default=0)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
+    ap.add_argument("--ref-sample", type=int, default=1 << 21)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,152 @@
+/*
+ * include/pbit.h -- C-ABI of the B200-native Pbit list sort (libpbit.so).
+ *
+ * Pbit (arXiv cs/0511020) sorts a singly-linked list stably by its keys: it splits
+ * the list into Omega = 2^K sub-lists by successive K-bit patterns of the key,
+ * most significant first, recurses, and concatenates the sorted fragments
+ * ("Split the list in relation to the bit pattern ... merge sorted fragments of
+ * the list"; listing P:346-361, ascending loops P:379-380).  On the
+ * GPU the same unique result is reached by list ranking + stable LSD radix passes
+ * + relink.  The paper's `Node *Pbit(Node *L, unsigned M, Node *P)`
+ * returns the new head and relinks `next` in situ.
+ *
+ * Representation.  A node is an index v in [0, n).  `next[v]` (u32) is the
+ * paper's `L->next` and PBIT_NULL is its NULL (P:8).  `keys` holds the
+ * paper's `L->data`: an unsigned key of key_bits = M bits (P:63-64,
+ * `size = sizeof(data)<<3`), little-endian, node-indexed, element size
+ * key_bits/8 bytes.
+ *
+ * Result.  With v_0 = head, v_{i+1} = next[v_i], the output is the list order
+ * sorted ascending and STABLY by unsigned key (equal keys keep input-list order,
+ * P:4):  *out_head = w_0, out_next[w_i] = w_{i+1}, out_next[w_{n-1}] =
+ * PBIT_NULL.  This result is unique, so every digit width K gives bit-identical
+ * output.
+ *
+ * Ownership.  The caller owns every array.  The library allocates stream-ordered
+ * workspace (cudaMallocAsync on the call's stream; memory returns to the device
+ * pool when the call ends) and never keeps pointers after returning.
+ *
+ * Synchronisation.  Every call is synchronous: it returns after the work on
+ * opts->stream has finished (out_head and the status are host values).  Calls on
+ * distinct streams or devices may run concurrently from different host threads.
+ *
+ * Errors.  Functions return a pbit_status and never throw or abort.
+ *   PBIT_ERR_INVALID_ARG  null pointer; key_bits not in {8,16,32,64}; digit_bits out
+ *                         of range; head >= n (n > 0); n > 2^32-1; pointers that mix
+ *                         host and device memory.
+ *   PBIT_ERR_INVALID_LIST the input is not one NULL-terminated chain of exactly n
+ *                         nodes starting at head (cycle, short chain, index >= n,
+ *                         a node reached twice).  out_next is NOT modified (the check
+ *                         completes before the relink kernel writes).
+ *   PBIT_ERR_OOM          workspace allocation failed (the paper's push overflow
+ *                         path).
+ *   PBIT_ERR_CUDA / _NCCL a propagated runtime error.
+ */
+#ifndef PBIT_H_
+#define PBIT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PBIT_NULL 0xFFFFFFFFu /* the list terminator, the paper's NULL (P:8) */
+
+typedef enum {
+    PBIT_OK = 0,
+    PBIT_ERR_INVALID_ARG = 1,
+    PBIT_ERR_INVALID_LIST = 2,
+    PBIT_ERR_OOM = 3,
+    PBIT_ERR_CUDA = 4,
+    PBIT_ERR_NCCL = 5,
+    PBIT_ERR_UNSUPPORTED = 6
+} pbit_status;
+
+/* Phases whose device time is reported in pbit_opts.phase_ms (CUDA events on the
+ * call's stream).  PBIT_PHASE_PASS0 + i is the i-th scheduled radix pass slot. */
+enum {
+    PBIT_PHASE_PACK = 0,      /* AoS (key,next) pack + all-digit histograms       */
+    PBIT_PHASE_WALK = 1,      /* ruling-set walk: segments in list order           */
+    PBIT_PHASE_RANK = 2,      /* ruler-list ranking (segment offsets, validation)  */
+    PBIT_PHASE_GATHER = 3,    /* segments -> list-order (key, id) arrays + plan    */
+    PBIT_PHASE_RELINK = 4,    /* out_next from the sorted ids                      */
+    PBIT_PHASE_PASS0 = 5,     /* radix pass slots follow: PASS0 .. PASS0+63        */
+    PBIT_NUM_PHASES = 5 + 64
+};
+
+typedef struct {
+    int digit_bits;  /* K, the bit-pattern length.  0 = auto (8).  1..8.
+                        The paper's default is K = 4.  Every K gives the
+                        same bytes.                                                 */
+    void *stream;    /* cudaStream_t for every launch; NULL = legacy default stream */
+    int validate;    /* reserved: validation always runs (it is fused into ranking) */
+    float *phase_ms; /* optional host array of PBIT_NUM_PHASES floats: device ms per
+                        phase, filled after the call (adds CUDA events); else NULL  */
+    uint32_t *passes_run; /* optional host out: number of radix passes executed (the
+                        non-trivial digits; trivial ones are skipped)               */
+    uint32_t *launches; /* optional host out: kernels this call launched            */
+} pbit_opts;
+
+/*
+ * pbit_sort_list -- stable ascending sort of one singly-linked list.
+ *
+ *   keys      [in]  n keys, key_bits/8 bytes each, node-indexed (u8/u16/u32/u64).
+ *   next      [in]  n successor ids (u32), PBIT_NULL terminates.
+ *   head      [in]  first node id (PBIT_NULL iff n == 0).
+ *   n         [in]  number of nodes, 0 <= n <= 2^32-1.
+ *   key_bits  [in]  M in {8, 16, 32, 64}.
+ *   out_head  [out] HOST pointer: head of the sorted list.
+ *   out_next  [out] n successor ids of the sorted list.  May alias `next`
+ *                   (in-place relink, as the paper's in situ sort).
+ *   opts      [in]  may be NULL (defaults).
+ *
+ * keys/next/out_next are either all CUDA device pointers on the current device
+ * (the fast path: nothing is copied) or all host pointers (pinned or pageable;
+ * the library stages them through device memory inside the call).
+ */
+int pbit_sort_list(const void *keys, const uint32_t *next, uint32_t head, uint64_t n,
+                   int key_bits, uint32_t *out_head, uint32_t *out_next, const pbit_opts *opts);
+
+/*
+ * pbit_sort_list_mg -- the same sort of ONE list whose nodes are sharded over the
+ * G ranks of an NCCL communicator (one process per GPU).
+ *
+ *   keys_local     [in]  device, n_local keys of nodes [node_lo, node_lo+n_local).
+ *   next_local     [in]  device, their successors as GLOBAL ids (PBIT_NULL ends).
+ *   head           [in]  global id of the first node, identical on every rank.
+ *   n_global       [in]  total nodes over all ranks.
+ *   node_lo,n_local[in]  this rank's contiguous slice; slices must be ordered by rank,
+ *                        contiguous and equal-sized except the last
+ *                        (node_lo = rank * ceil(n_global / G)); else PBIT_ERR_UNSUPPORTED.
+ *   key_bits       [in]  as above.
+ *   out_head       [out] host: head of the sorted list (same on every rank).
+ *   out_next_local [out] device, n_local global successor ids for this rank's nodes.
+ *   nccl_comm      [in]  ncclComm_t (see pbit_mg_comm_init) spanning the G ranks.
+ *   opts           [in]  as above (stream used for every kernel and collective).
+ * Collective: every rank must call it with the same head, n_global, key_bits, K.
+ */
+int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32_t head,
+                      uint64_t n_global, uint64_t node_lo, uint64_t n_local, int key_bits,
+                      uint32_t *out_head, uint32_t *out_next_local, void *nccl_comm,
+                      const pbit_opts *opts);
+
+/* NCCL communicator helpers for callers that do not link NCCL themselves.  The
+ * unique id (PBIT_MG_UNIQUE_ID_BYTES opaque bytes) is created on rank 0 and shared
+ * by the caller (e.g. torch.distributed.broadcast_object_list). */
+#define PBIT_MG_UNIQUE_ID_BYTES 128
+int pbit_mg_get_unique_id(void *id_out /* PBIT_MG_UNIQUE_ID_BYTES host bytes */);
+int pbit_mg_comm_init(void **comm_out, int nranks, const void *id, int rank);
+int pbit_mg_comm_destroy(void *comm);
+
+/* Human-readable name of a status code (static string). */
+const char *pbit_status_string(int status);
+
+/* Library version, (major << 16) | (minor << 8) | patch. */
+uint32_t pbit_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PBIT_H_ */

@@ -1,0 +1,170 @@
+"""paper_cs_0511020_b200 -- thin Python binding of libpbit.so (include/pbit.h).
+
+Argument marshalling only: every step of the sort runs in the library's sm_100a
+kernels.  PyTorch supplies device memory, streams and process groups.  There is
+no CPU fallback: if libpbit.so is missing or fails to load, importing this
+package raises.
+
+    head, out_next = sort_list(keys, next, head)                 # device tensors
+    head, out_next = sort_list(keys, next, head, out_next=next)  # in place
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libpbit.so")
+PBIT_NULL = 0xFFFFFFFF
+NUM_PHASES = 5 + 64
+PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
+SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
+           "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version"]
+
+STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
+          4: "PBIT_ERR_CUDA", 5: "PBIT_ERR_NCCL", 6: "PBIT_ERR_UNSUPPORTED"}
+
+
+class PbitError(RuntimeError):
+    def __init__(self, code: int, what: str = ""):
+        super().__init__(f"{STATUS.get(code, code)}{': ' + what if what else ''}")
+        self.code = code
+
+
+class _Opts(ctypes.Structure):
+    _fields_ = [("digit_bits", ctypes.c_int), ("stream", ctypes.c_void_p), ("validate", ctypes.c_int),
+                ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("passes_run", ctypes.POINTER(ctypes.c_uint32)),
+                ("launches", ctypes.POINTER(ctypes.c_uint32))]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    u32p = ctypes.POINTER(ctypes.c_uint32)
+    lib.pbit_sort_list.restype = ctypes.c_int
+    lib.pbit_sort_list.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
+                                   u32p, ctypes.c_void_p, ctypes.POINTER(_Opts)]
+    lib.pbit_sort_list_mg.restype = ctypes.c_int
+    lib.pbit_sort_list_mg.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64,
+                                      ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, u32p, ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.POINTER(_Opts)]
+    lib.pbit_mg_get_unique_id.restype = ctypes.c_int
+    lib.pbit_mg_get_unique_id.argtypes = [ctypes.c_void_p]
+    lib.pbit_mg_comm_init.restype = ctypes.c_int
+    lib.pbit_mg_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
+    lib.pbit_mg_comm_destroy.restype = ctypes.c_int
+    lib.pbit_mg_comm_destroy.argtypes = [ctypes.c_void_p]
+    lib.pbit_status_string.restype = ctypes.c_char_p
+    lib.pbit_status_string.argtypes = [ctypes.c_int]
+    lib.pbit_version.restype = ctypes.c_uint32
+    return lib
+
+
+lib = _load()
+
+_KEY_BITS = {torch.uint8: 8, torch.int8: 8, torch.int16: 16, torch.uint16: 16, torch.int32: 32,
+             torch.uint32: 32, torch.int64: 64, torch.uint64: 64}
+
+
+def _ptr(t) -> int:
+    if isinstance(t, torch.Tensor):
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        return t.data_ptr()
+    return int(t.ctypes.data)  # numpy (host) array
+
+
+def _opts(digit_bits: int, stream, phase_ms, passes, launches=None):
+    o = _Opts()
+    o.launches = launches
+    o.digit_bits = int(digit_bits)
+    o.stream = ctypes.c_void_p(stream)
+    o.validate = 1
+    o.phase_ms = phase_ms
+    o.passes_run = passes
+    return o
+
+
+def _stream_handle(stream, on_cuda: bool):
+    if stream is not None:
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return torch.cuda.current_stream().cuda_stream if on_cuda and torch.cuda.is_available() else 0
+
+
+def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: int = 0, out_next=None,
+              stream=None, timing: bool = False):
+    """Stable ascending sort of the list (head, next_) by keys; returns (head, out_next)
+    (plus a dict of device ms per phase when timing=True).
+
+    keys / next_ / out_next: CUDA tensors on the current device, or host arrays (torch
+    CPU tensors or numpy) -- then the library stages them through device memory.
+    next_ holds u32 ids (int32 view, NULL = -1 / 0xFFFFFFFF)."""
+    if key_bits is None:
+        key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
+    n = int(next_.shape[0])
+    on_cuda = isinstance(next_, torch.Tensor) and next_.is_cuda
+    if out_next is None:
+        if isinstance(next_, torch.Tensor):
+            out_next = torch.empty_like(next_)
+        else:
+            import numpy as np
+            out_next = np.empty(n, np.uint32)
+    oh = ctypes.c_uint32(0)
+    pm = (ctypes.c_float * NUM_PHASES)() if timing else None
+    passes = ctypes.c_uint32(0)
+    launches = ctypes.c_uint32(0)
+    o = _opts(digit_bits, _stream_handle(stream, on_cuda), pm, ctypes.pointer(passes), ctypes.pointer(launches))
+    rc = lib.pbit_sort_list(_ptr(keys) if n else None, _ptr(next_) if n else None, head & 0xFFFFFFFF, n, key_bits,
+                            ctypes.byref(oh), _ptr(out_next) if n else None, ctypes.byref(o))
+    if rc:
+        raise PbitError(rc, lib.pbit_status_string(rc).decode())
+    if timing:
+        ph = {name: float(pm[i]) for i, name in enumerate(PHASE_NAMES) if i < 5 or pm[i] > 0}
+        ph["passes_run"] = int(passes.value)
+        ph["launches"] = int(launches.value)
+        return int(oh.value), out_next, ph
+    return int(oh.value), out_next
+
+
+# ----------------------------------------------------------------------------- multi-GPU
+def mg_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    rc = lib.pbit_mg_get_unique_id(buf)
+    if rc:
+        raise PbitError(rc, "ncclGetUniqueId")
+    return buf.raw
+
+
+def mg_comm_init(nranks: int, uid: bytes, rank: int) -> int:
+    c = ctypes.c_void_p()
+    rc = lib.pbit_mg_comm_init(ctypes.byref(c), nranks, ctypes.c_char_p(uid), rank)
+    if rc:
+        raise PbitError(rc, "ncclCommInitRank")
+    return c.value
+
+
+def mg_comm_destroy(comm: int) -> None:
+    lib.pbit_mg_comm_destroy(ctypes.c_void_p(comm))
+
+
+def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int, comm: int,
+                 key_bits: int | None = None, digit_bits: int = 0, out_next_local=None, stream=None):
+    """Sort one list sharded over the ranks of `comm` (see include/pbit.h).  Returns
+    (head, out_next_local)."""
+    if key_bits is None:
+        key_bits = _KEY_BITS[keys_local.dtype]
+    n_local = int(next_local.shape[0])
+    if out_next_local is None:
+        out_next_local = torch.empty_like(next_local)
+    oh = ctypes.c_uint32(0)
+    o = _opts(digit_bits, _stream_handle(stream, True), None, None)
+    rc = lib.pbit_sort_list_mg(_ptr(keys_local) if n_local else None, _ptr(next_local) if n_local else None,
+                               head & 0xFFFFFFFF, n_global, node_lo, n_local, key_bits, ctypes.byref(oh),
+                               _ptr(out_next_local) if n_local else None, ctypes.c_void_p(comm), ctypes.byref(o))
+    if rc:
+        raise PbitError(rc, lib.pbit_status_string(rc).decode())
+    return int(oh.value), out_next_local

@@ -1,0 +1,99 @@
+// common.cuh -- shared device/host helpers of the CUDA path (libpbit.so).
+// Nothing here is shared with oracle/ (the two sides share no code).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define PBIT_NULL32 0xFFFFFFFFu
+
+namespace pbit {
+
+// ----------------------------------------------------------------------------- errors
+// Device-side error word (OR of bits); any bit set => PBIT_ERR_INVALID_LIST.
+enum : int {
+  E_BAD_INDEX = 1,   // a next[] entry >= n that is not NULL
+  E_DYN_FULL = 2,    // more split segments than any valid list can need (cycle without ruler)
+  E_CHAIN = 4,       // the ruler chain from the head is cyclic or does not hold exactly n nodes
+};
+
+// ----------------------------------------------------------------------------- records
+// Node record packed by k_pack so that one random 32 B sector read in the walk
+// serves both the key and the successor (the paper's AoS `struct Node{next,data}`,
+// P:14-17).  Keys of <= 32 bits are widened to u32.
+template <int KB> struct Rec { using T = uint2; };      // {key, next}
+template <> struct Rec<8> { using T = uint4; };         // {key lo, key hi, next, 0}
+
+template <int KB> struct KeyOf { using T = uint32_t; };
+template <> struct KeyOf<8> { using T = unsigned long long; };
+
+// ----------------------------------------------------------------------------- rulers
+// Ruling-set selection.  Node ids are cut into blocks of s = 2^s_log2 consecutive ids;
+// block r holds exactly one ruler, at offset hash(r) mod span inside the block.  The
+// ruler index of a ruler node is therefore v >> s_log2: no table, no compaction.  The
+// head becomes ruler R (an extra one) unless it is a ruler already.
+__host__ __device__ __forceinline__ uint32_t ruler_hash(uint32_t x) {
+  x ^= 0x6A09E667u;
+  x ^= x >> 16; x *= 0x21F0AAADu;
+  x ^= x >> 15; x *= 0x735A2D97u;
+  x ^= x >> 15;
+  return x;
+}
+
+struct RulerSel {
+  uint32_t n;        // nodes
+  uint32_t s_log2;   // spacing exponent
+  uint32_t R;        // number of id blocks = ceil(n / s)
+
+  __host__ __device__ __forceinline__ uint32_t offset_in_block(uint32_t r) const {
+    uint32_t base = r << s_log2;
+    uint32_t span = n - base;
+    uint32_t s = 1u << s_log2;
+    uint32_t h = ruler_hash(r);
+    return span >= s ? (h & (s - 1)) : (h % span);
+  }
+  __host__ __device__ __forceinline__ uint32_t node_of(uint32_t r) const {
+    return (r << s_log2) + offset_in_block(r);
+  }
+  __host__ __device__ __forceinline__ bool is_ruler(uint32_t v) const {
+    uint32_t r = v >> s_log2;
+    return (v & ((1u << s_log2) - 1)) == offset_in_block(r);
+  }
+};
+
+// ----------------------------------------------------------------------------- plan
+// Device-side pass plan written by k_plan: the non-trivial digits, low to high.
+// A digit whose histogram has one bin holding all n keys cannot reorder anything
+// and its pass is skipped (the top digits of keys < 2^16).
+struct Plan {
+  uint32_t npasses;
+  uint32_t digit[64];
+};
+
+// ----------------------------------------------------------------------------- loads
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_stream_u4(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long r;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(r) : "l"(p) : "memory");
+  return r;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+}  // namespace pbit

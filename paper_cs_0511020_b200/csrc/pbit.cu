@@ -1,0 +1,355 @@
+// pbit.cu -- host orchestrator + C-ABI entry of the single-GPU Pbit list sort.
+//
+// pbit_sort_list (include/pbit.h) runs, on the caller's stream:
+//   k_pack -> k_walk -> k_rank_init/k_rank_jump^r/k_rank_check -> k_gather -> k_plan
+//   -> k_onesweep x D (trivial digits exit at once) -> k_relink
+// then one small D2H of {head, error} and a stream sync.  No host round-trip sits
+// between kernels: the pass plan lives on the device.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "../../include/pbit.h"
+#include "kernels.cuh"
+#include "pbit_internal.h"
+
+namespace pbit {
+
+// ----------------------------------------------------------------------------- device info
+struct DevInfo {
+  int sms = 0;
+  bool pool_ready = false;
+};
+static std::mutex g_dev_mu;
+static DevInfo g_dev[64];
+
+int device_info(int dev, int* sms) {
+  std::lock_guard<std::mutex> lk(g_dev_mu);
+  if (dev < 0 || dev >= 64) return PBIT_ERR_CUDA;
+  DevInfo& d = g_dev[dev];
+  if (!d.sms) {
+    if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return PBIT_ERR_CUDA;
+  }
+  if (!d.pool_ready) {
+    // keep freed workspace in the device pool between calls (stream-ordered allocator)
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    d.pool_ready = true;
+  }
+  *sms = d.sms;
+  return PBIT_OK;
+}
+
+// ----------------------------------------------------------------------------- planning
+void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
+  p->n = (uint32_t)n;
+  p->key_bits = key_bits;
+  p->K = K;
+  p->D = (key_bits + K - 1) / K;
+  // ruler spacing: ~64 nodes per segment on large lists, more rulers on small ones so the
+  // walk still has enough independent walkers (and short tails)
+  int s_log2 = 6;
+  while (s_log2 > 2 && (n >> s_log2) < (1u << 14)) --s_log2;
+  p->s_log2 = s_log2;
+  p->cap = 4u << s_log2;
+  p->R = (uint32_t)((n + (1ull << s_log2) - 1) >> s_log2);
+  p->dyn_cap = (uint32_t)(n / p->cap + 1);
+}
+
+static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+
+// ----------------------------------------------------------------------------- dispatch
+template <int KB, int RB>
+static void launch_sweeps(const Plan* plan, int D, void* keys0, uint32_t* ids0, void* keys1, uint32_t* ids1,
+                          const uint32_t* bases, unsigned long long* status, uint32_t* tile_ctr, uint32_t n,
+                          const int* err, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
+  using KeyT = typename KeyOf<KB>::T;
+  constexpr int IPT = (KB == 8) ? 12 : 16;
+  constexpr int TILE = SWEEP_THREADS * IPT;
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  for (int s = 0; s < D; ++s) {
+    k_onesweep<KeyT, RB, IPT><<<ntiles, SWEEP_THREADS, 0, st>>>(
+        plan, s, (KeyT*)keys0, ids0, (KeyT*)keys1, ids1, bases, status, tile_ctr, n, err);
+    if (ev) cudaEventRecord(ev[ev_base + s], st);
+  }
+}
+
+template <int KB>
+static void launch_sweeps_k(int K, const Plan* plan, int D, void* keys0, uint32_t* ids0, void* keys1,
+                            uint32_t* ids1, const uint32_t* bases, unsigned long long* status, uint32_t* tile_ctr,
+                            uint32_t n, const int* err, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
+  switch (K) {
+#define PBIT_K(RB) case RB: launch_sweeps<KB, RB>(plan, D, keys0, ids0, keys1, ids1, bases, status, tile_ctr, n, err, st, ev, ev_base); break;
+    PBIT_K(1) PBIT_K(2) PBIT_K(3) PBIT_K(4) PBIT_K(5) PBIT_K(6) PBIT_K(7) PBIT_K(8)
+#undef PBIT_K
+  }
+}
+
+size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64 ? 12 : 16); }
+
+// Workspace layout (all 256-byte aligned).
+struct Ws {
+  void* kn; void* slots; uint32_t* seg_len; uint32_t* seg_succ;
+  unsigned long long* dist[2]; uint32_t* succ[2];
+  void* keys[2]; uint32_t* ids[2]; unsigned long long* status;
+  // control block (zeroed per call)
+  uint32_t* hist; uint32_t* bases; Plan* plan; int* err; uint32_t* dyn_count; uint32_t* tile_ctr; uint32_t* d_head;
+  size_t ctl_bytes; void* ctl; size_t status_bytes;
+};
+
+static size_t carve(const SortPlan& p, char* base, Ws* w) {
+  const size_t n = p.n;
+  const int kb = p.key_bits / 8;
+  const size_t rec = kb == 8 ? 16 : 8;
+  const size_t kbytes = kb == 8 ? 8 : 4;
+  const size_t Rmax = (size_t)p.R + 1 + p.dyn_cap;
+  const int radix = 1 << p.K;
+  const size_t tile = sweep_tile(p.key_bits);
+  const size_t ntiles = (n + tile - 1) / tile;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { char* q = base ? base + off : nullptr; off += align_up(bytes); return (void*)q; };
+  w->kn = take(n * rec);
+  w->slots = take(Rmax * p.cap * rec);
+  w->seg_len = (uint32_t*)take(Rmax * 4);
+  w->seg_succ = (uint32_t*)take(Rmax * 4);
+  for (int i = 0; i < 2; ++i) { w->dist[i] = (unsigned long long*)take(Rmax * 8); w->succ[i] = (uint32_t*)take(Rmax * 4); }
+  for (int i = 0; i < 2; ++i) { w->keys[i] = take(n * kbytes); w->ids[i] = (uint32_t*)take(n * 4); }
+  w->status_bytes = ntiles * radix * 8;
+  w->status = (unsigned long long*)take(w->status_bytes);
+  const size_t ctl0 = off;
+  w->hist = (uint32_t*)take((size_t)p.D * radix * 4);
+  w->bases = (uint32_t*)take((size_t)p.D * radix * 4);
+  w->plan = (Plan*)take(sizeof(Plan));
+  w->err = (int*)take(4);
+  w->dyn_count = (uint32_t*)take(4);
+  w->tile_ctr = (uint32_t*)take(64 * 4);
+  w->d_head = (uint32_t*)take(4);
+  w->ctl = base ? base + ctl0 : nullptr;
+  w->ctl_bytes = off - ctl0;
+  return off;
+}
+
+// ----------------------------------------------------------------------------- the device path
+template <int KB>
+static int run_device(const void* keys, const uint32_t* next, uint32_t head, const SortPlan& p, uint32_t* out_next,
+                      uint32_t* out_head, cudaStream_t st, int sms, float* phase_ms, uint32_t* passes_run,
+                      uint32_t* launches_out) {
+  using RT = typename Rec<KB>::T;
+  Ws w;
+  const size_t bytes = carve(p, nullptr, &w);
+  char* base = nullptr;
+  if (cudaMallocAsync((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  carve(p, base, &w);
+
+  cudaEvent_t ev[PBIT_NUM_PHASES + 1];
+  const bool timing = phase_ms != nullptr;
+  if (timing) {
+    for (int i = 0; i <= PBIT_NUM_PHASES; ++i) cudaEventCreate(&ev[i]);
+    cudaEventRecord(ev[PBIT_NUM_PHASES], st);  // start
+  }
+  const uint32_t n = p.n;
+  const int radix = 1 << p.K;
+  uint32_t launches = 0;
+
+  cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, st);
+  cudaMemsetAsync(w.status, 0, w.status_bytes, st);
+
+  // a1/a2: pack + histograms
+  {
+    const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
+    const size_t smem = (size_t)p.D * radix * 4;
+    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, (RT*)w.kn, w.hist, p.K, p.D, w.err);
+    ++launches;
+  }
+  if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
+
+  // a1: walk
+  RulerSel sel{n, (uint32_t)p.s_log2, p.R};
+  const bool head_is_ruler = sel.is_ruler(head);
+  const uint32_t R_static = p.R + (head_is_ruler ? 0u : 1u);
+  const uint32_t head_ruler = head_is_ruler ? (head >> p.s_log2) : p.R;
+  {
+    int blocks = sms * (2048 / WALK_THREADS);
+    const uint32_t min_per = 4;
+    if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
+    const uint32_t per_cta = (R_static + blocks - 1) / blocks;
+    k_walk<KB><<<blocks, WALK_THREADS, 0, st>>>((const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap,
+                                                w.seg_len, w.seg_succ, w.dyn_count, p.dyn_cap, per_cta, w.err);
+    ++launches;
+  }
+  if (timing) cudaEventRecord(ev[PBIT_PHASE_WALK], st);
+
+  // a1: ruler ranking
+  {
+    const uint32_t Rmax = R_static + p.dyn_cap;
+    int rounds = 1;
+    while ((1ull << rounds) < Rmax) ++rounds;
+    rounds += 1;
+    const int blocks = std::max(1, std::min((int)((Rmax + 255) / 256), sms * 8));
+    k_rank_init<<<blocks, 256, 0, st>>>(w.seg_len, w.seg_succ, R_static, w.dyn_count, p.dyn_cap, w.dist[0],
+                                        w.succ[0], w.err);
+    int cur = 0;
+    for (int i = 0; i < rounds; ++i) {
+      k_rank_jump<<<blocks, 256, 0, st>>>(w.dist[cur], w.succ[cur], w.dist[cur ^ 1], w.succ[cur ^ 1], R_static,
+                                          w.dyn_count, p.dyn_cap, w.err);
+      cur ^= 1;
+    }
+    k_rank_check<<<1, 1, 0, st>>>(w.dist[cur], w.succ[cur], head_ruler, n, w.err);
+    launches += rounds + 2;
+    if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
+    // a1: gather to list order
+    const int gblocks = std::max(1, std::min((int)((Rmax + 7) / 8), sms * 8));
+    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg_len, w.dist[cur], R_static, w.dyn_count,
+                                          p.dyn_cap, n, (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.err);
+    ++launches;
+  }
+  // a3: bucket bases + pass plan
+  k_plan<<<1, 256, 0, st>>>(w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
+  ++launches;
+  if (timing) cudaEventRecord(ev[PBIT_PHASE_GATHER], st);
+
+  // a3/a4: passes
+  launch_sweeps_k<KB>(p.K, w.plan, p.D, w.keys[0], w.ids[0], w.keys[1], w.ids[1], w.bases, w.status, w.tile_ctr, n,
+                      w.err, st, timing ? ev : nullptr, PBIT_PHASE_PASS0);
+  launches += p.D;
+
+  // a5: relink
+  {
+    const int blocks = std::max(1, std::min((int)((n + 255) / 256), sms * 8));
+    k_relink<<<blocks, 256, 0, st>>>(w.plan, w.ids[0], w.ids[1], n, out_next, w.d_head, w.err);
+    ++launches;
+  }
+  if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
+
+  // results: {head, err, npasses}
+  struct Res { uint32_t head; int err; uint32_t npasses; } res{};
+  cudaError_t e1 = cudaMemcpyAsync(&res.head, w.d_head, 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e2 = cudaMemcpyAsync(&res.err, w.err, 4, cudaMemcpyDeviceToHost, st);
+  cudaError_t e3 = cudaMemcpyAsync(&res.npasses, &w.plan->npasses, 4, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(base, st);
+  cudaError_t es = cudaStreamSynchronize(st);
+  cudaError_t el = cudaGetLastError();
+  int rc = PBIT_OK;
+  if (e1 || e2 || e3 || es || el) rc = PBIT_ERR_CUDA;
+  if (timing) {
+    if (rc == PBIT_OK) {
+      for (int i = 0; i < PBIT_NUM_PHASES; ++i) phase_ms[i] = 0.f;
+      cudaEvent_t prev = ev[PBIT_NUM_PHASES];
+      auto el_ms = [&](cudaEvent_t a, cudaEvent_t b) { float ms = 0; cudaEventElapsedTime(&ms, a, b); return ms; };
+      phase_ms[PBIT_PHASE_PACK] = el_ms(prev, ev[PBIT_PHASE_PACK]);
+      phase_ms[PBIT_PHASE_WALK] = el_ms(ev[PBIT_PHASE_PACK], ev[PBIT_PHASE_WALK]);
+      phase_ms[PBIT_PHASE_RANK] = el_ms(ev[PBIT_PHASE_WALK], ev[PBIT_PHASE_RANK]);
+      phase_ms[PBIT_PHASE_GATHER] = el_ms(ev[PBIT_PHASE_RANK], ev[PBIT_PHASE_GATHER]);
+      cudaEvent_t a = ev[PBIT_PHASE_GATHER];
+      for (int s = 0; s < p.D; ++s) { phase_ms[PBIT_PHASE_PASS0 + s] = el_ms(a, ev[PBIT_PHASE_PASS0 + s]); a = ev[PBIT_PHASE_PASS0 + s]; }
+      phase_ms[PBIT_PHASE_RELINK] = el_ms(a, ev[PBIT_PHASE_RELINK]);
+    }
+    for (int i = 0; i <= PBIT_NUM_PHASES; ++i) cudaEventDestroy(ev[i]);
+  }
+  if (rc) return rc;
+  if (res.err) return PBIT_ERR_INVALID_LIST;
+  *out_head = res.head;
+  if (passes_run) *passes_run = res.npasses;
+  if (launches_out) *launches_out = launches;
+  return PBIT_OK;
+}
+
+int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
+                uint32_t* out_head, uint32_t* out_next, cudaStream_t st, float* phase_ms, uint32_t* passes_run,
+                uint32_t* launches) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
+  int sms = 0;
+  if (int rc = device_info(dev, &sms)) return rc;
+  SortPlan p;
+  make_plan(n, key_bits, K, &p);
+  switch (key_bits) {
+    case 8: return run_device<1>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
+    case 16: return run_device<2>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
+    case 32: return run_device<4>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
+    default: return run_device<8>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
+  }
+}
+
+// pointer kind: 1 device (current device), 0 host (registered or pageable), -1 other device / error
+int pointer_kind(const void* ptr, int dev) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if (a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged) return a.device == dev ? 1 : -1;
+  return 0;
+}
+
+}  // namespace pbit
+
+using namespace pbit;
+
+extern "C" {
+
+uint32_t pbit_version(void) { return (0u << 16) | (1u << 8) | 0u; }
+
+const char* pbit_status_string(int s) {
+  switch (s) {
+    case PBIT_OK: return "ok";
+    case PBIT_ERR_INVALID_ARG: return "invalid argument";
+    case PBIT_ERR_INVALID_LIST: return "invalid list";
+    case PBIT_ERR_OOM: return "out of device memory";
+    case PBIT_ERR_CUDA: return "CUDA error";
+    case PBIT_ERR_NCCL: return "NCCL error";
+    case PBIT_ERR_UNSUPPORTED: return "unsupported";
+    default: return "unknown status";
+  }
+}
+
+int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits,
+                   uint32_t* out_head, uint32_t* out_next, const pbit_opts* opts) {
+  if (!out_head) return PBIT_ERR_INVALID_ARG;
+  if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
+  int K = opts && opts->digit_bits ? opts->digit_bits : 8;
+  if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
+  if (n > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+  cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
+  float* phase_ms = opts ? opts->phase_ms : nullptr;
+  uint32_t* passes_run = opts ? opts->passes_run : nullptr;
+  uint32_t* launches = opts ? opts->launches : nullptr;
+  if (passes_run) *passes_run = 0;
+  if (launches) *launches = 0;
+  if (n == 0) {
+    if (head != PBIT_NULL) return PBIT_ERR_INVALID_LIST;
+    *out_head = PBIT_NULL;
+    return PBIT_OK;
+  }
+  if (!keys || !next || !out_next) return PBIT_ERR_INVALID_ARG;
+  if ((uint64_t)head >= n) return PBIT_ERR_INVALID_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
+  const int kk = pointer_kind(keys, dev), kn = pointer_kind(next, dev), ko = pointer_kind(out_next, dev);
+  if (kk < 0 || kn < 0 || ko < 0) return PBIT_ERR_INVALID_ARG;
+  if (kk == 1 && kn == 1 && ko == 1)
+    return sort_device(keys, next, head, n, key_bits, K, out_head, out_next, st, phase_ms, passes_run, launches);
+  if (kk != 0 || kn != 0 || ko != 0) return PBIT_ERR_INVALID_ARG;  // mixed host/device
+
+  // host buffers: stage through device memory inside the call
+  const size_t kbytes = n * (size_t)(key_bits / 8), nbytes = n * 4;
+  char* d = nullptr;
+  const size_t a = align_up(kbytes), b = align_up(nbytes);
+  if (cudaMallocAsync((void**)&d, a + 2 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  int rc = PBIT_OK;
+  if (cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ||
+      cudaMemcpyAsync(d + a, next, nbytes, cudaMemcpyHostToDevice, st))
+    rc = PBIT_ERR_CUDA;
+  if (!rc) rc = sort_device(d, (const uint32_t*)(d + a), head, n, key_bits, K, out_head, (uint32_t*)(d + a + b), st,
+                            phase_ms, passes_run, launches);
+  if (!rc && cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+  cudaFreeAsync(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = PBIT_ERR_CUDA;
+  cudaGetLastError();
+  return rc;
+}
+
+}  // extern "C"

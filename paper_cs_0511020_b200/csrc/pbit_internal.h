@@ -1,0 +1,27 @@
+// pbit_internal.h -- host-side interfaces shared by pbit.cu and mg.cu (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace pbit {
+
+struct SortPlan {
+  uint32_t n;
+  int key_bits;
+  int K;        // digit bits
+  int D;        // digits = ceil(key_bits / K)
+  int s_log2;   // ruler spacing exponent
+  uint32_t cap; // slot capacity per segment
+  uint32_t R;   // static rulers (id blocks)
+  uint32_t dyn_cap;
+};
+
+void make_plan(uint64_t n, int key_bits, int K, SortPlan* p);
+int device_info(int dev, int* sms);
+int pointer_kind(const void* ptr, int dev);
+size_t sweep_tile(int key_bits);
+int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
+                uint32_t* out_head, uint32_t* out_next, cudaStream_t st, float* phase_ms, uint32_t* passes_run,
+                uint32_t* launches);
+
+}  // namespace pbit

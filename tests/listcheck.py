@@ -81,3 +81,70 @@ def check_sorted_list_properties(keys, order, out_head, out_next):
     kv, ks = keys[v], keys[s]
     ok = (kv < ks) | ((kv == ks) & (rank[v] < rank[s]))
     assert ok.all(), f"{int((~ok).sum())} edges break (key, input-rank) order"
+
+
+# ----------------------------------------------------------------------------- torch (any device)
+def unsigned_order_key(keys, key_bits):
+    """int64 tensor whose signed order equals the unsigned order of the keys."""
+    import torch
+    k = keys.to(torch.int64)
+    if key_bits == 8:
+        return k & 0xFF
+    if key_bits == 16:
+        return k & 0xFFFF
+    if key_bits == 32:
+        return k & 0xFFFFFFFF
+    return k ^ (-(1 << 63))
+
+
+def check_properties_torch(keys, key_bits, order, out_head, out_next):
+    """Same proof as check_sorted_list_properties, with torch ops on the tensors'
+    device (used for the full-size configs, up to 2^30 nodes)."""
+    import torch
+    n = int(order.shape[0])
+    if n == 0:
+        assert out_head == NULL
+        return
+    dev = out_next.device
+    on = out_next.to(torch.int64) & 0xFFFFFFFF
+    is_null = on == NULL
+    assert int(is_null.sum()) == 1, "exactly one NULL terminator"
+    rank = torch.empty(n, dtype=torch.int64, device=dev)
+    rank[order.to(dev)] = torch.arange(n, device=dev)
+    v = torch.nonzero(~is_null).squeeze(1)
+    s = on[v]
+    del is_null, on
+    assert bool((s < n).all()), "successor out of range"
+    cnt = torch.bincount(s, minlength=n)
+    assert int(cnt.max()) <= 1, "a node has two predecessors"
+    assert 0 <= out_head < n and int(cnt[out_head]) == 0, "head has a predecessor"
+    del cnt
+    k = unsigned_order_key(keys.to(dev), key_bits)
+    kv, ks = k[v], k[s]
+    ok = (kv < ks) | ((kv == ks) & (rank[v] < rank[s]))
+    bad = int((~ok).sum())
+    assert bad == 0, f"{bad} edges break (key, input-rank) order"
+
+
+def sampled_successors_torch(keys, key_bits, order, samples):
+    """The plain definition evaluated one output at a time: the successor of node v is
+    the node with the smallest (key, input rank) above (key[v], rank[v])."""
+    import torch
+    n = int(order.shape[0])
+    dev = keys.device
+    rank = torch.empty(n, dtype=torch.int64, device=dev)
+    rank[order.to(dev)] = torch.arange(n, device=dev)
+    k = unsigned_order_key(keys, key_bits)
+    out = []
+    for v in samples:
+        kv, rv = k[v], rank[v]
+        above = (k > kv) | ((k == kv) & (rank > rv))
+        if not bool(above.any()):
+            out.append(NULL)
+            continue
+        kk = torch.where(above, k, torch.full_like(k, torch.iinfo(torch.int64).max))
+        kmin = kk.min()
+        cand = above & (k == kmin)
+        rr = torch.where(cand, rank, torch.full_like(rank, torch.iinfo(torch.int64).max))
+        out.append(int(order.to(dev)[rr.min()]))
+    return out

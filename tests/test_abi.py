@@ -1,0 +1,83 @@
+"""The C-ABI library: it loads, exports every symbol include/pbit.h declares, and the
+argument checks that need no device behave as the header says.  CPU only."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "pbit.h")
+
+
+@pytest.fixture(scope="module")
+def pbit():
+    from paper_cs_0511020_b200 import build
+    build.build()
+    import paper_cs_0511020_b200 as p
+    return p
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?\w+\s*\*?\s*(pbit_\w+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_north_star_calls():
+    fns = declared_functions()
+    assert "pbit_sort_list" in fns and "pbit_sort_list_mg" in fns
+
+
+def test_every_declared_symbol_is_exported(pbit):
+    lib = ctypes.CDLL(pbit.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    assert set(declared_functions()) == set(pbit.SYMBOLS)
+
+
+def test_version_and_status_strings(pbit):
+    assert pbit.lib.pbit_version() >= 0x100
+    assert pbit.lib.pbit_status_string(2) == b"invalid list"
+    assert pbit.lib.pbit_status_string(99) == b"unknown status"
+
+
+def test_argument_checks_without_device(pbit):
+    lib = pbit.lib
+    oh = ctypes.c_uint32(7)
+    dummy = np.zeros(4, np.uint32)
+    p = dummy.ctypes.data
+    # out_head NULL
+    assert lib.pbit_sort_list(p, p, 0, 4, 32, None, p, None) == 1
+    # key width not in {8,16,32,64}
+    assert lib.pbit_sort_list(p, p, 0, 4, 24, ctypes.byref(oh), p, None) == 1
+    # digit_bits out of range
+    o = pbit._opts(9, 0, None, None)
+    assert lib.pbit_sort_list(p, p, 0, 4, 32, ctypes.byref(oh), p, ctypes.byref(o)) == 1
+    # empty list: head must be NULL
+    assert lib.pbit_sort_list(None, None, 0xFFFFFFFF, 0, 32, ctypes.byref(oh), None, None) == 0
+    assert oh.value == 0xFFFFFFFF
+    assert lib.pbit_sort_list(None, None, 0, 0, 32, ctypes.byref(oh), None, None) == 2
+    # head >= n, null arrays
+    assert lib.pbit_sort_list(p, p, 4, 4, 32, ctypes.byref(oh), p, None) == 1
+    assert lib.pbit_sort_list(None, p, 0, 4, 32, ctypes.byref(oh), p, None) == 1
+    # n beyond u32 ids
+    assert lib.pbit_sort_list(p, p, 0, 1 << 33, 32, ctypes.byref(oh), p, None) == 1
+
+
+def test_python_wrapper_empty_list(pbit):
+    import torch
+    h, out = pbit.sort_list(torch.zeros(0, dtype=torch.int32), torch.zeros(0, dtype=torch.int32), 0xFFFFFFFF)
+    assert h == 0xFFFFFFFF and out.numel() == 0
+
+
+def test_no_oracle_in_product_path():
+    """The product package never imports or links the oracle (DESIGN.md boundary)."""
+    pkg = os.path.join(ROOT, "paper_cs_0511020_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"(^\s*(import|from)\s+oracle)|(#include\s*[<\"].*oracle)|liboracle|pbit_oracle",
+                                     src, flags=re.M), f

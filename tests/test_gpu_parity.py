@@ -1,0 +1,222 @@
+"""Parity of the CUDA path (through the C-ABI) with the paper-literal oracle.
+
+Bit-exact: the stable result is unique, so (out_head, out_next[]) must equal the
+oracle's bytes for every digit width K.  Full BASELINE.json sizes (2^28-2^30) are
+checked with properties that together force the unique answer
+(tests/listcheck.check_properties_torch) plus sampled outputs evaluated one by one.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+from tests.listcheck import NULL, check_properties_torch, sampled_successors_torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pbit(cuda_ok):
+    import paper_cs_0511020_b200 as p
+    return p
+
+
+def _gpu_sort(pbit, li, K=0, **kw):
+    h, out = pbit.sort_list(li.keys, li.next, li.head, key_bits=li.key_bits, digit_bits=K, **kw)
+    torch.cuda.synchronize()
+    return h, out.cpu().numpy().view(np.uint32)
+
+
+def _oracle(li, K=4):
+    return oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, li.key_bits, K)
+
+
+def _assert_same(got, want, what=""):
+    gh, go = got
+    oh, oo = want
+    assert gh == oh, f"{what}: head {gh} != {oh}"
+    if not np.array_equal(go, oo):
+        bad = np.nonzero(go != oo)[0]
+        raise AssertionError(f"{what}: {len(bad)} of {len(oo)} next[] entries differ, first at {bad[:5]}")
+
+
+# ---------------------------------------------------------------- BASELINE configs C1, C2 vs oracle
+def test_c1_bit_exact_paper_K4(pbit):
+    li = workloads.make_config("C1", device="cuda")
+    _assert_same(_gpu_sort(pbit, li, K=4), _oracle(li), "C1 K=4")
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 5, 6, 7, 8])
+def test_c1_every_digit_width_identical(pbit, K):
+    li = workloads.make_config("C1", device="cuda")
+    _assert_same(_gpu_sort(pbit, li, K=K), _oracle(li), f"C1 K={K}")
+
+
+def test_c2_bit_exact(pbit):
+    li = workloads.make_config("C2", device="cuda")
+    _assert_same(_gpu_sort(pbit, li, K=8), _oracle(li), "C2 K=8")
+
+
+# ---------------------------------------------------------------- ragged sizes, key widths, shapes
+CASES = [
+    (1, 32, "uniform", "random"), (2, 32, "uniform", "random"), (3, 8, "uniform", "push"),
+    (31, 16, "uniform", "random"), (4095, 32, "zipf", "random"), (4097, 64, "uniform", "random"),
+    (65537, 32, "uniform", "random"), (65537, 8, "uniform", "identity"), (100003, 16, "uniform", "push"),
+    (100003, 32, "equal", "random"), (100003, 32, "max", "random"), (100003, 64, "equal", "identity"),
+    (100003, 32, "sorted", "random"), (100003, 32, "reverse", "random"), (250001, 64, "runs4096", "random"),
+    (1000003, 32, "zipf", "random"), (1000003, 64, "uniform", "push"), (1 << 20, 32, "uniform", "identity"),
+]
+
+
+@pytest.mark.parametrize("n,key_bits,keys,links", CASES)
+def test_ragged_shapes_vs_oracle(pbit, n, key_bits, keys, links):
+    li = workloads.make_list(n, key_bits, seed=n ^ key_bits, keys=keys, links=links, device="cuda")
+    _assert_same(_gpu_sort(pbit, li), _oracle(li), f"{li.name}")
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_digit_width_sweep_zipf(pbit, K):
+    li = workloads.make_list(300007, 32, seed=77, keys="zipf", device="cuda")
+    _assert_same(_gpu_sort(pbit, li, K=K), _oracle(li), f"K={K}")
+
+
+@pytest.mark.parametrize("K", [3, 5, 8])
+def test_digit_width_sweep_u64_narrow_top_digit(pbit, K):
+    li = workloads.make_list(70001, 64, seed=78, keys="uniform", device="cuda")
+    _assert_same(_gpu_sort(pbit, li, K=K), _oracle(li), f"u64 K={K}")
+
+
+def test_small_key_range_skips_trivial_digits(pbit):
+    li = workloads.make_list(500000, 32, seed=5, keys="uniform", key_range=1 << 16, device="cuda")
+    h, out, ph = pbit.sort_list(li.keys, li.next, li.head, digit_bits=8, timing=True)
+    torch.cuda.synchronize()
+    assert ph["passes_run"] == 2
+    _assert_same((h, out.cpu().numpy().view(np.uint32)), _oracle(li), "C5-shaped")
+
+
+def test_all_equal_keys_runs_no_pass(pbit):
+    li = workloads.make_list(77777, 32, seed=6, keys="equal", device="cuda")
+    h, out, ph = pbit.sort_list(li.keys, li.next, li.head, timing=True)
+    torch.cuda.synchronize()
+    assert ph["passes_run"] == 0
+    _assert_same((h, out.cpu().numpy().view(np.uint32)), _oracle(li), "all equal")
+
+
+# ---------------------------------------------------------------- API edge cases
+def test_empty_and_singletons(pbit):
+    h, out = pbit.sort_list(torch.zeros(0, dtype=torch.int32, device="cuda"),
+                            torch.zeros(0, dtype=torch.int32, device="cuda"), NULL)
+    assert h == NULL and out.numel() == 0
+    k = torch.tensor([5], dtype=torch.int32, device="cuda")
+    nx = torch.tensor([-1], dtype=torch.int32, device="cuda")
+    h, out = pbit.sort_list(k, nx, 0)
+    assert h == 0 and int(out[0]) == -1
+    k = torch.tensor([9, 2], dtype=torch.int32, device="cuda")
+    nx = torch.tensor([1, -1], dtype=torch.int32, device="cuda")
+    h, out = pbit.sort_list(k, nx, 0)
+    assert h == 1 and out.tolist() == [-1, 0]
+
+
+def test_worked_example_on_gpu(pbit):
+    keys = torch.tensor([21, 3, 209, 14, 156, 47, 3, 214], dtype=torch.uint8, device="cuda")
+    nx = torch.tensor([1, 2, 3, 4, 5, 6, 7, -1], dtype=torch.int32, device="cuda")
+    h, out = pbit.sort_list(keys, nx, 0, digit_bits=4)
+    seq, v = [], h
+    o = out.cpu().numpy().view(np.uint32)
+    while v != NULL:
+        seq.append(v)
+        v = int(o[v])
+    assert [int(keys[i]) for i in seq] == [3, 3, 14, 21, 47, 156, 209, 214]
+    assert seq[:2] == [1, 6]  # stable: list position 1 before 6 (P:4)
+
+
+def test_in_place_alias(pbit):
+    li = workloads.make_list(123457, 32, seed=8, keys="zipf", device="cuda")
+    want = _oracle(li)
+    nx = li.next.clone()
+    h, out = pbit.sort_list(li.keys, nx, li.head, out_next=nx)
+    torch.cuda.synchronize()
+    assert out.data_ptr() == nx.data_ptr()
+    _assert_same((h, nx.cpu().numpy().view(np.uint32)), want, "in place")
+
+
+def test_host_buffers(pbit):
+    li = workloads.make_list(200003, 64, seed=9, keys="runs4096")
+    k = workloads.keys_numpy(li)
+    nx = workloads.next_numpy(li)
+    h, out = pbit.sort_list(k, nx, li.head, key_bits=64)
+    _assert_same((h, out), _oracle(li), "host buffers")
+    kp = li.keys.pin_memory()
+    npin = li.next.pin_memory()
+    h2, out2 = pbit.sort_list(kp, npin, li.head)
+    _assert_same((h2, out2.numpy().view(np.uint32)), _oracle(li), "pinned host buffers")
+
+
+def test_side_stream_and_determinism(pbit):
+    li = workloads.make_list(400009, 32, seed=10, keys="zipf", device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a = pbit.sort_list(li.keys, li.next, li.head, stream=s)
+    b = pbit.sort_list(li.keys, li.next, li.head)
+    torch.cuda.synchronize()
+    assert a[0] == b[0] and torch.equal(a[1], b[1])
+
+
+# ---------------------------------------------------------------- invalid lists
+def _bad_lists():
+    n = 50000
+    base = torch.arange(1, n + 1, dtype=torch.int32)
+    base[-1] = -1
+    cyc_head = base.clone(); cyc_head[-1] = 0                       # tail -> head
+    cyc_off = base.clone(); cyc_off[n // 2] = -1; cyc_off[-1] = n // 2 + 1  # second half is a cycle
+    short = base.clone(); short[n - 10] = -1                          # 10 nodes unreachable
+    bad_idx = base.clone(); bad_idx[777] = n + 5                      # index >= n
+    two_pred = base.clone(); two_pred[n - 2] = 5                      # node 5 reached twice
+    small_cycle = base.clone(); small_cycle[1000] = 999               # 999 <-> 1000 loop
+    return {"cycle_through_head": cyc_head, "cycle_off_path": cyc_off, "short": short,
+            "index_ge_n": bad_idx, "two_predecessors": two_pred, "small_cycle": small_cycle}
+
+
+@pytest.mark.parametrize("name", list(_bad_lists().keys()))
+def test_invalid_list_rejected_and_out_untouched(pbit, name):
+    nx = _bad_lists()[name].cuda()
+    keys = workloads.uniform_u32(nx.shape[0], 1, 1).to(torch.int32).cuda()
+    out = torch.full_like(nx, 0x1234)
+    with pytest.raises(pbit.PbitError) as e:
+        pbit.sort_list(keys, nx, 0, out_next=out)
+    assert e.value.code == 2
+    torch.cuda.synchronize()
+    assert bool((out == 0x1234).all()), "out_next modified on INVALID_LIST"
+    with pytest.raises(oracle.OracleError):
+        oracle.pbit_sort(keys.cpu().numpy().view(np.uint32), nx.cpu().numpy().view(np.uint32), 0, 32, 4)
+
+
+def test_invalid_args(pbit):
+    k = torch.zeros(4, dtype=torch.int32, device="cuda")
+    nx = torch.tensor([1, 2, 3, -1], dtype=torch.int32, device="cuda")
+    with pytest.raises(pbit.PbitError) as e:
+        pbit.sort_list(k, nx, 4)
+    assert e.value.code == 1
+    with pytest.raises(pbit.PbitError) as e:  # mixed host/device
+        pbit.sort_list(k.cpu(), nx, 0)
+    assert e.value.code == 1
+
+
+# ---------------------------------------------------------------- full BASELINE sizes (properties)
+@pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
+def test_full_size_configs(pbit, cfg):
+    c = workloads.CONFIGS[cfg]
+    li = workloads.make_config(cfg, device="cuda")
+    h, out = pbit.sort_list(li.keys, li.next, li.head, digit_bits=c["digit_bits"])
+    torch.cuda.synchronize()
+    check_properties_torch(li.keys, li.key_bits, li.order, h, out)
+    g = torch.Generator().manual_seed(1)
+    samples = torch.randint(0, li.n, (6,), generator=g).tolist() + [h]
+    want = sampled_successors_torch(li.keys, li.key_bits, li.order, samples)
+    got = [int(out[v]) & 0xFFFFFFFF for v in samples]
+    assert got == want
+    del li, out
+    torch.cuda.empty_cache()
