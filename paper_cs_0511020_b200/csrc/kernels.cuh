@@ -5,9 +5,10 @@
 //   k_rank_*    a1     ruler-list ranking by pointer jumping; validates the chain
 //   k_gather    a1     segments -> list-order (key, id) arrays
 //   k_plan      a3     exclusive scans of the digit histograms -> bucket bases, pass plan
-//   k_onesweep  a3/a4  one stable LSD pass: warp-ballot ranking, decoupled lookback,
-//                      smem-staged scatter with 128-bit stores
-//   k_relink    a5     out_next from the sorted ids (the paper's merge)
+//   k_onesweep  a3/a4  one stable LSD pass: TMA tile loads, warp-ballot ranking,
+//                      decoupled lookback, smem-staged coalesced scatter
+//   k_relink_*  a5     out_next from the sorted ids (the paper's merge),
+//                      binned so every write lands in an L2-resident window
 //
 // Paper anchors: the split loop is the stable scatter; the end-marker
 // recursion is the ascending order of the bucket bases; merge is relink.
@@ -68,37 +69,61 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
 template <int KB>
 __global__ void __launch_bounds__(WALK_THREADS)
 k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_static, uint32_t head,
-       typename Rec<KB>::T* __restrict__ slots, uint32_t cap, uint32_t* __restrict__ seg_len,
-       uint32_t* __restrict__ seg_succ, uint32_t* __restrict__ dyn_count, uint32_t dyn_cap,
-       uint32_t per_cta, int* __restrict__ err) {
+       typename Rec<KB>::T* __restrict__ slots, uint32_t cap, uint2* __restrict__ seg,
+       uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t per_cta, int* __restrict__ err) {
   using RT = typename Rec<KB>::T;
+  // Records are staged in registers and stored as whole 32 B sectors: a partial-sector
+  // store costs an HBM read-modify-write on B200.
+  constexpr int B = 32 / sizeof(RT);
   __shared__ uint32_t s_next;
   if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
   const uint32_t n = sel.n;
   const uint32_t lo = blockIdx.x * per_cta;
   const uint32_t hi = min(lo + per_cta, R_static);
+  RT buf[B];
   for (;;) {
     const uint32_t r = lo + atomicAdd(&s_next, 1u);
     if (r >= hi) break;
     uint32_t u = r < sel.R ? sel.node_of(r) : head;
     uint32_t cur = r, j = 0;
     RT* out = slots + (size_t)cur * cap;
+    auto flush_partial = [&](uint32_t jj) {
+      const uint32_t m = jj % B, b0 = jj - m;
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if ((uint32_t)q < m) out[b0 + q] = buf[q];
+    };
     for (;;) {
       RT x;
       if constexpr (KB == 8) x = ld_stream_u4(kn + u); else x = ld_stream_u2(kn + u);
       uint32_t v;
       if constexpr (KB == 8) { v = x.z; x.z = u; } else { v = x.y; x.y = u; }
-      out[j] = x;  // (key, id)
+#pragma unroll
+      for (int q = 0; q < B; ++q)
+        if ((j % B) == (uint32_t)q) buf[q] = x;
       ++j;
-      if (v == PBIT_NULL32) { seg_len[cur] = j; seg_succ[cur] = PBIT_NULL32; break; }
-      if (v >= n) { atomicOr(err, E_BAD_INDEX); seg_len[cur] = j; seg_succ[cur] = PBIT_NULL32; break; }
-      if (sel.is_ruler(v)) { seg_len[cur] = j; seg_succ[cur] = v >> sel.s_log2; break; }
-      if (j == cap) {
+      if ((j % B) == 0) {
+        uint4* o = reinterpret_cast<uint4*>(out + (j - B));
+        const uint4* bb = reinterpret_cast<const uint4*>(buf);
+        o[0] = bb[0];
+        o[1] = bb[1];
+      }
+      bool end = false;
+      uint32_t succ = PBIT_NULL32;
+      if (v == PBIT_NULL32) end = true;
+      else if (v >= n) { atomicOr(err, E_BAD_INDEX); end = true; }
+      else if (sel.is_ruler(v)) { succ = v >> sel.s_log2; end = true; }
+      if (end) {
+        flush_partial(j);
+        seg[cur] = make_uint2(j, succ);
+        break;
+      }
+      if (j == cap) {  // cap is a multiple of B: nothing left in buf
         const uint32_t k = atomicAdd(dyn_count, 1u);
-        if (k >= dyn_cap) { atomicOr(err, E_DYN_FULL); seg_len[cur] = j; seg_succ[cur] = PBIT_NULL32; break; }
+        if (k >= dyn_cap) { atomicOr(err, E_DYN_FULL); seg[cur] = make_uint2(j, PBIT_NULL32); break; }
         const uint32_t r2 = R_static + k;
-        seg_len[cur] = cap; seg_succ[cur] = r2;
+        seg[cur] = make_uint2(cap, r2);
         cur = r2; j = 0; out = slots + (size_t)cur * cap;
       }
       u = v;
@@ -107,28 +132,41 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
 }
 
 // ============================================================================ a1: rank
-// Pointer jumping (Wyllie) over the ruler list: dist[r] = nodes from the first node of
-// segment r to the end of the list.  After ceil(log2 R)+1 rounds every succ is NULL
-// unless the ruler graph has a cycle.
-__global__ void k_rank_init(const uint32_t* __restrict__ seg_len, const uint32_t* __restrict__ seg_succ,
-                            uint32_t R_static, const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap,
-                            unsigned long long* __restrict__ dist, uint32_t* __restrict__ succ,
-                            const int* __restrict__ err) {
+// The segments form the ruler list (seg[r] = {nodes in segment r, next ruler}).  It is
+// ranked by a second ruling set: sub-rulers (one per block of 2^s2 ruler ids, by hash,
+// plus the head's ruler) sum their sub-segments (walk A, L2-resident reads), the short
+// sub-ruler list is ranked by pointer jumping (Wyllie), and walk B hands every ruler its
+// distance to the end of the list: dist[r] = nodes from the first node of segment r to
+// the end.  Segment r then occupies list positions [n - dist[r], n - dist[r] + len[r]).
+__global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
+                              const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
+                              uint32_t nsub, unsigned long long* __restrict__ sdist, uint32_t* __restrict__ ssucc,
+                              int* __restrict__ err) {
   if (*err) return;
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
-    dist[r] = seg_len[r];
-    succ[r] = seg_succ[r];
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
+    const uint32_t rq = q < sub.R ? sub.node_of(q) : head_ruler;
+    if (rq >= R) { sdist[q] = 0; ssucc[q] = PBIT_NULL32; continue; }
+    unsigned long long acc = 0;
+    uint32_t r = rq, steps = 0, succ = PBIT_NULL32;
+    for (;;) {
+      const uint2 x = seg[r];
+      acc += x.x;
+      if (x.y == PBIT_NULL32) break;
+      if (sub.is_ruler(x.y)) { succ = x.y >> sub.s_log2; break; }
+      if (++steps > R) { atomicOr(err, E_CHAIN); break; }  // ruler cycle without a sub-ruler
+      r = x.y;
+    }
+    sdist[q] = acc;
+    ssucc[q] = succ;
   }
 }
 
 __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const uint32_t* __restrict__ s_in,
-                            unsigned long long* __restrict__ d_out, uint32_t* __restrict__ s_out,
-                            uint32_t R_static, const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap,
+                            unsigned long long* __restrict__ d_out, uint32_t* __restrict__ s_out, uint32_t m,
                             const int* __restrict__ err) {
   if (*err) return;
-  const uint32_t R = R_static + min(*dyn_count, dyn_cap);
-  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const uint32_t s = s_in[r];
     unsigned long long d = d_in[r];
     uint32_t s2 = s;
@@ -138,12 +176,33 @@ __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const u
   }
 }
 
-// Validation (reading Q10): the chain from the head ruler must end (succ NULL) and hold
-// exactly n nodes; then every node lies on it.
+// Validation (reading Q10): the chain from the head must end (succ NULL) and hold exactly
+// n nodes; then every node lies on it.
 __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const uint32_t* __restrict__ succ,
-                             uint32_t head_ruler, uint32_t n, int* __restrict__ err) {
+                             uint32_t head_sub, uint32_t n, int* __restrict__ err) {
   if (*err) return;
-  if (succ[head_ruler] != PBIT_NULL32 || dist[head_ruler] != (unsigned long long)n) atomicOr(err, E_CHAIN);
+  if (succ[head_sub] != PBIT_NULL32 || dist[head_sub] != (unsigned long long)n) atomicOr(err, E_CHAIN);
+}
+
+__global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
+                              const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
+                              uint32_t nsub, const unsigned long long* __restrict__ sdist,
+                              uint32_t* __restrict__ dist, const int* __restrict__ err) {
+  if (*err) return;
+  const uint32_t R = R_static + min(*dyn_count, dyn_cap);
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
+    const uint32_t rq = q < sub.R ? sub.node_of(q) : head_ruler;
+    if (rq >= R) continue;
+    uint32_t D = (uint32_t)sdist[q];
+    uint32_t r = rq;
+    for (;;) {
+      dist[r] = D;
+      const uint2 x = seg[r];
+      D -= x.x;
+      if (x.y == PBIT_NULL32 || sub.is_ruler(x.y)) break;
+      r = x.y;
+    }
+  }
 }
 
 // ============================================================================ a1: gather
@@ -151,7 +210,7 @@ __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const 
 // segment copies its slot into the list-order arrays (coalesced both ways).
 template <int KB>
 __global__ void k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
-                         const uint32_t* __restrict__ seg_len, const unsigned long long* __restrict__ dist,
+                         const uint2* __restrict__ seg, const uint32_t* __restrict__ dist,
                          uint32_t R_static, const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t n,
                          typename KeyOf<KB>::T* __restrict__ keys_lo, uint32_t* __restrict__ ids_lo,
                          const int* __restrict__ err) {
@@ -161,8 +220,8 @@ __global__ void k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t r = warp; r < R; r += nwarps) {
-    const uint32_t len = seg_len[r];
-    const uint32_t off = n - (uint32_t)dist[r];
+    const uint32_t len = seg[r].x;
+    const uint32_t off = n - dist[r];
     const typename Rec<KB>::T* src = slots + (size_t)r * cap;
     for (uint32_t j = lane; j < len; j += 32) {
       if constexpr (KB == 8) {
@@ -212,126 +271,224 @@ k_plan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases, Plan* __
 }
 
 // ============================================================================ a3/a4: onesweep
-// One stable counting-sort pass on digit plan->digit[slot] (Merrill & Garland style
-// single-pass scan with decoupled lookback).  Tile = 256 threads x IPT items, taken in
+// One stable counting-sort pass on digit plan->digit[slot] (single-pass scan with
+// decoupled lookback, Merrill & Garland).  Tile = 256 threads x IPT items, taken in
 // launch order from an atomic ticket so every predecessor tile is running or done.
 //
+//  1. TMA bulk copy (cp.async.bulk + mbarrier) of the tile's keys and ids into smem.
+//  2. Stable in-warp ranking: a warp ranks 32 consecutive items at a time, in input
+//     order; equal digits are grouped by K ballots (or match.any), the group leader
+//     bumps the warp's u16 counter for that digit (distinct digits per instruction,
+//     private row per warp: no atomics needed).
+//  3. Per-digit warp offsets + tile totals; the aggregate is published at once.
+//  4. Stage the tile in smem in (digit, input order) order.
+//  5. Decoupled lookback, one thread per digit value.
+//  6. Coalesced write-out: consecutive threads store consecutive staged elements, which
+//     land contiguously inside each digit run.
+//
 // Status word per (tile, digit): count[31:0] | flag[33:32] (1 aggregate, 2 inclusive)
-// | epoch[63:34]; the status array is zeroed once per call and each pass slot uses its
+// | epoch[63:34]; the status array is zeroed once per call and each pass slot has its
 // own epoch, so stale words from earlier passes never match.
 template <typename KeyT, int RADIX_BITS, int IPT>
-__global__ void __launch_bounds__(SWEEP_THREADS)
-k_onesweep(const Plan* __restrict__ plan, int slot, KeyT* keys0, uint32_t* ids0, KeyT* keys1, uint32_t* ids1,
-           const uint32_t* __restrict__ bases, unsigned long long* status, uint32_t* tile_ctr, uint32_t n,
-           const int* __restrict__ err) {
-  constexpr int RADIX = 1 << RADIX_BITS;
-  constexpr int TILE = SWEEP_THREADS * IPT;
+struct SweepSmem {
+  static constexpr int RADIX = 1 << RADIX_BITS;
+  static constexpr int TILE = SWEEP_THREADS * IPT;
+  KeyT k[TILE];            // input keys, later the staged output keys
+  uint32_t iin[TILE];      // input ids
+  uint32_t iout[TILE];     // staged output ids
+  uint16_t wcnt[SWEEP_WARPS][RADIX];
+  uint32_t dstart[RADIX];
+  uint32_t goff[RADIX];
+  uint32_t scan[SWEEP_WARPS];
+  uint32_t tile;
+  unsigned long long mbar;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, unsigned long long* mbar) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(d), "l"(gsrc), "r"(bytes), "r"(m) : "memory");
+}
+
+// What one launch of k_onesweep sorts.  kind 0: a key pass of the plan (digit
+// plan->digit[slot], ping-pong parity = slot & 1).  kind 1: the first relink pass, over
+// the final sorted ids (input parity = plan->npasses & 1); each item's value is its
+// successor in that order.  kind 2: a further relink pass over (v, succ) pairs.
+struct SweepArgs {
+  const void* kin[2];
+  const uint32_t* vin[2];
+  void* kout[2];
+  uint32_t* vout[2];
+  const uint32_t* bases;  // kind 0: [digit][RADIX]; kind 1/2: [RADIX] of this pass
+  unsigned long long* status;
+  uint32_t* tile_ctr;
+  const Plan* plan;
+  const int* err;
+  uint32_t n;
+  int slot;  // ticket counter + epoch, unique per launch in a call
+  int kind;
+  int bit0;  // kind 1/2: digit = (key >> bit0) & (RADIX - 1)
+  int par;   // kind 2: input buffer index
+};
+
+template <typename KeyT, int RADIX_BITS, int IPT, bool USE_MATCH>
+__global__ void __launch_bounds__(SWEEP_THREADS, 4)
+k_onesweep(const __grid_constant__ SweepArgs a) {
+  using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
+  constexpr int RADIX = S::RADIX;
+  constexpr int TILE = S::TILE;
   constexpr int WARP_ITEMS = 32 * IPT;
   static_assert(RADIX <= SWEEP_THREADS, "one thread per digit value");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  S& sm = *reinterpret_cast<S*>(smem_raw);
 
-  __shared__ uint32_t s_tile;
-  __shared__ uint32_t s_wcnt[SWEEP_WARPS][RADIX];
-  __shared__ uint32_t s_dstart[RADIX];
-  __shared__ uint32_t s_goff[RADIX];
-  __shared__ uint32_t s_scan[SWEEP_WARPS];
-  __shared__ __align__(16) KeyT s_keys[TILE];
-  __shared__ __align__(16) uint32_t s_ids[TILE];
-
-  if (*err) return;
-  const uint32_t npasses = plan->npasses;
-  if ((uint32_t)slot >= npasses) return;
-  const int digit_idx = plan->digit[slot];
-  const int shift = digit_idx * RADIX_BITS;
-  const bool last = (uint32_t)slot + 1 == npasses;
-  const KeyT* __restrict__ kin = (slot & 1) ? keys1 : keys0;
-  const uint32_t* __restrict__ iin = (slot & 1) ? ids1 : ids0;
-  KeyT* __restrict__ kout = (slot & 1) ? keys0 : keys1;
-  uint32_t* __restrict__ iout = (slot & 1) ? ids0 : ids1;
+  if (*a.err) return;
+  const uint32_t n = a.n;
+  const int slot = a.slot;
+  int shift, src;
+  bool last = false;
+  const uint32_t* __restrict__ bases;
+  if (a.kind == 0) {
+    const uint32_t npasses = a.plan->npasses;
+    if ((uint32_t)slot >= npasses) return;
+    const int digit_idx = a.plan->digit[slot];
+    shift = digit_idx * RADIX_BITS;
+    last = (uint32_t)slot + 1 == npasses;
+    src = slot & 1;
+    bases = a.bases + digit_idx * RADIX;
+  } else {
+    shift = a.bit0;
+    src = a.kind == 1 ? (int)(a.plan->npasses & 1u) : a.par;
+    bases = a.bases;
+  }
+  const bool succ_mode = a.kind == 1;
+  const KeyT* __restrict__ kin = reinterpret_cast<const KeyT*>(a.kin[src]);
+  const uint32_t* __restrict__ iin = a.vin[src];
+  const int dst = a.kind == 1 ? 0 : (src ^ 1);
+  KeyT* __restrict__ kout = reinterpret_cast<KeyT*>(a.kout[dst]);
+  uint32_t* __restrict__ iout = a.vout[dst];
   const unsigned long long epoch = (unsigned long long)(slot + 1);
-
+  unsigned long long* status = a.status;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  for (int i = t; i < SWEEP_WARPS * RADIX; i += SWEEP_THREADS) (&s_wcnt[0][0])[i] = 0;
-  if (t == 0) s_tile = atomicAdd(tile_ctr + slot, 1u);
+
+  if (t == 0) {
+    sm.tile = atomicAdd(a.tile_ctr + slot, 1u);
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
+    asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(m));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t tile = sm.tile;
   const uint32_t tile_base = tile * (uint32_t)TILE;
   const uint32_t tile_count = min((uint32_t)TILE, n - tile_base);
 
-  // ---- load (warp-striped: each load instruction covers 32 consecutive elements)
-  KeyT key[IPT];
-  uint32_t id[IPT];
-  uint32_t rank[IPT];
-  const uint32_t wbase = tile_base + w * WARP_ITEMS;
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t p = wbase + i * 32 + lane;
-    if (p < n) { key[i] = kin[p]; id[i] = iin[p]; }
-    else { key[i] = 0; id[i] = 0; }
+  // ---- 1. TMA bulk loads (sizes rounded up to 16 B; buffers are padded to 256 B)
+  uint32_t extra = PBIT_NULL32;  // succ_mode: the key just after the tile
+  if (t == 0) {
+    const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
+    const uint32_t ib = succ_mode ? 0u : (tile_count * 4u + 15u) & ~15u;
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(kb + ib) : "memory");
+    bulk_g2s(sm.k, kin + tile_base, kb, &sm.mbar);
+    if (!succ_mode) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
+    else if (tile_base + tile_count < n) extra = (uint32_t)kin[tile_base + tile_count];
   }
-
-  // ---- stable in-warp ranking: items in input order, equal digits grouped by ballots
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t p = wbase + i * 32 + lane;
-    const bool valid = p < n;
-    const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
-    uint32_t peers = __ballot_sync(0xffffffffu, valid);
-#pragma unroll
-    for (int b = 0; b < RADIX_BITS; ++b) {
-      const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
-      peers &= ((d >> b) & 1u) ? bb : ~bb;
+  for (int i = t; i < SWEEP_WARPS * RADIX / 2; i += SWEEP_THREADS) reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
+  {
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
+    uint32_t done = 0;
+    while (!done) {
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(m) : "memory");
     }
-    const int leader = 31 - __clz(peers | 1u);
-    uint32_t before = 0;
-    if (valid && lane == leader) before = atomicAdd(&s_wcnt[w][d], (uint32_t)__popc(peers));
-    before = __shfl_sync(0xffffffffu, before, leader);
-    rank[i] = before + __popc(peers & lanemask_lt());
   }
   __syncthreads();
 
-  // ---- per digit: exclusive over warps, tile total, publish aggregate, scan over digits
+  // ---- 2. stable in-warp ranking
+  KeyT key[IPT];
+  uint32_t rd[IPT];  // rank within (warp, digit) | digit << 16
+  const uint32_t wofs = w * WARP_ITEMS;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const uint32_t j = wofs + i * 32 + lane;
+    const bool valid = j < tile_count;
+    key[i] = sm.k[j];
+    if (succ_mode && valid) {  // the value of item j is the key of item j+1
+      uint32_t sv;
+      if (j + 1 < tile_count) sv = (uint32_t)sm.k[j + 1];
+      else sv = (tile_base + tile_count < n) ? (uint32_t)kin[tile_base + tile_count] : PBIT_NULL32;
+      sm.iin[j] = sv;
+    }
+    const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
+    const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+    uint32_t peers;
+    if constexpr (USE_MATCH) {
+      peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu) & vmask;
+    } else {
+      peers = vmask;
+#pragma unroll
+      for (int b = 0; b < RADIX_BITS; ++b) {
+        const uint32_t bb = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bb : ~bb;
+      }
+    }
+    const int leader = 31 - __clz(peers | 1u);
+    uint32_t before = 0;
+    if (valid && lane == leader) {
+      before = sm.wcnt[w][d];
+      sm.wcnt[w][d] = (uint16_t)(before + __popc(peers));
+    }
+    before = __shfl_sync(0xffffffffu, before, leader);
+    rd[i] = (before + __popc(peers & lanemask_lt())) | (d << 16);
+  }
+  (void)extra;
+  __syncthreads();
+
+  // ---- 3. per digit: exclusive over warps, tile total, publish aggregate, scan over digits
   uint32_t total = 0;
   if (t < RADIX) {
 #pragma unroll
     for (int ww = 0; ww < SWEEP_WARPS; ++ww) {
-      const uint32_t c = s_wcnt[ww][t];
-      s_wcnt[ww][t] = total;
+      const uint32_t c = sm.wcnt[ww][t];
+      sm.wcnt[ww][t] = (uint16_t)total;
       total += c;
     }
-    if (tile > 0 && total)  // zero aggregates are implied by the epoch-matched zero word below
-      st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (1ull << 32) | total);
-    else if (tile > 0)
-      st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (1ull << 32));
+    if (tile > 0) st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (1ull << 32) | total);
   }
   {
-    uint32_t x = total;  // threads >= RADIX contribute 0
+    uint32_t x = total;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) s_scan[w] = x;
+    if (lane == 31) sm.scan[w] = x;
     __syncthreads();
     uint32_t add = 0;
 #pragma unroll
-    for (int ww = 0; ww < SWEEP_WARPS; ++ww) add += (ww < w) ? s_scan[ww] : 0u;
-    if (t < RADIX) s_dstart[t] = x - total + add;
+    for (int ww = 0; ww < SWEEP_WARPS; ++ww) add += (ww < w) ? sm.scan[ww] : 0u;
+    if (t < RADIX) sm.dstart[t] = x - total + add;
   }
   __syncthreads();
 
-  // ---- stage the tile in smem in (digit, input order) order
+  // ---- 4. stage in (digit, input order) order (sm.k is free: every warp finished
+  // reading it before the barrier that ended the ranking)
+  uint32_t idv[IPT];
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) idv[i] = sm.iin[wofs + i * 32 + lane];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
-    const uint32_t p = wbase + i * 32 + lane;
-    if (p < n) {
-      const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
-      const uint32_t lp = s_dstart[d] + s_wcnt[w][d] + rank[i];
-      s_keys[lp] = key[i];
-      s_ids[lp] = id[i];
+    const uint32_t j = wofs + i * 32 + lane;
+    if (j < tile_count) {
+      const uint32_t d = rd[i] >> 16;
+      const uint32_t lp = sm.dstart[d] + sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
+      sm.iout[lp] = idv[i];
+      sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass only needs the digit
     }
   }
 
-  // ---- decoupled lookback, one thread per digit value
+  // ---- 5. decoupled lookback, one thread per digit value
   if (t < RADIX) {
     unsigned long long excl = 0;
     if (tile == 0) {
@@ -347,43 +504,24 @@ k_onesweep(const Plan* __restrict__ plan, int slot, KeyT* keys0, uint32_t* ids0,
       }
       st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (2ull << 32) | (excl + total));
     }
-    s_goff[t] = bases[digit_idx * RADIX + t] + (uint32_t)excl - s_dstart[t];
+    sm.goff[t] = bases[t] + (uint32_t)excl - sm.dstart[t];
   }
   __syncthreads();
 
-  // ---- write out: runs of equal digits land contiguously; 4 consecutive staged items
-  // per thread, one 128-bit store when they share a digit and the target is aligned.
-  const int nq = (int)((tile_count + 3) >> 2);
-  for (int q = t; q < nq; q += SWEEP_THREADS) {
-    const uint32_t j0 = (uint32_t)q * 4;
-    if (j0 + 3 < tile_count) {
-      const uint32_t d0 = (uint32_t)(s_keys[j0] >> shift) & (RADIX - 1);
-      const uint32_t d3 = (uint32_t)(s_keys[j0 + 3] >> shift) & (RADIX - 1);
-      const uint32_t g0 = s_goff[d0] + j0;
-      if (d0 == d3 && (g0 & 3u) == 0) {  // staged order is digit-sorted, so d0==d3 => all equal
-        const uint4 iv = *reinterpret_cast<const uint4*>(&s_ids[j0]);
-        *reinterpret_cast<uint4*>(iout + g0) = iv;
-        if (!last) {
-          if constexpr (sizeof(KeyT) == 4) {
-            *reinterpret_cast<uint4*>(kout + g0) = *reinterpret_cast<const uint4*>(&s_keys[j0]);
-          } else {
-            *reinterpret_cast<uint4*>(kout + g0) = *reinterpret_cast<const uint4*>(&s_keys[j0]);
-            *reinterpret_cast<uint4*>(kout + g0 + 2) = *reinterpret_cast<const uint4*>(&s_keys[j0 + 2]);
-          }
-        }
-        continue;
-      }
+  // ---- 6. coalesced write-out
+  if (!last) {
+#pragma unroll 4
+    for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
+      const KeyT k = sm.k[j];
+      const uint32_t g = sm.goff[(uint32_t)(k >> shift) & (RADIX - 1)] + j;
+      kout[g] = k;
+      iout[g] = sm.iout[j];
     }
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t j = j0 + e;
-      if (j < tile_count) {
-        const KeyT k = s_keys[j];
-        const uint32_t d = (uint32_t)(k >> shift) & (RADIX - 1);
-        const uint32_t g = s_goff[d] + j;
-        iout[g] = s_ids[j];
-        if (!last) kout[g] = k;
-      }
+  } else {
+#pragma unroll 4
+    for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
+      const uint32_t g = sm.goff[(uint32_t)sm.k[j]] + j;
+      iout[g] = sm.iout[j];
     }
   }
 }
@@ -391,17 +529,73 @@ k_onesweep(const Plan* __restrict__ plan, int slot, KeyT* keys0, uint32_t* ids0,
 // ============================================================================ a5: relink
 // out_next[ids[p]] = ids[p+1], out_next[ids[n-1]] = NULL, head = ids[0]: the paper's
 // end-splice merge of sorted fragments, one write per node.
-__global__ void k_relink(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
-                         const uint32_t* __restrict__ ids1, uint32_t n, uint32_t* __restrict__ out_next,
-                         uint32_t* __restrict__ d_head, const int* __restrict__ err) {
+//
+// On B200 a random 4 B store costs a 32 B HBM read + write even when the stores are
+// confined to a 64 KB window (measured: tools/micro/winstore.cu), so no kernel here
+// issues scattered partial-sector stores.  The pairs (v, succ) are first grouped by
+// fine bin v >> RELINK_FINE_SHIFT (streaming radix passes), then each fine bin is
+// applied in a shared-memory window and written out coalesced.
+constexpr int RELINK_FINE_SHIFT = 14;  // 16384 ids = 64 KB smem window
+
+// The pairs are sorted by v's bits [RELINK_FINE_SHIFT, log2 n) with k_onesweep (kind
+// 1 then 2; LSD, 8-bit digits).  Bucket bases need no histogram: the ids are a
+// permutation of [0, n), so the count of each digit value is known in closed form.
+__global__ void k_relink_bases(uint32_t n, int bit0, uint32_t* __restrict__ bases) {
+  __shared__ uint32_t s_warp[8];
+  const int t = threadIdx.x, lane = t & 31, w = t >> 5;  // 256 threads = 256 digit values
+  const unsigned long long B = 1ull << bit0, P = B << 8;
+  const unsigned long long full = n / P, rem = n % P;
+  const unsigned long long lo = (unsigned long long)t * B;
+  const uint32_t c = (uint32_t)(full * B + (rem > lo ? min(rem - lo, B) : 0ull));
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) s_warp[w] = x;
+  __syncthreads();
+  uint32_t add = 0;
+  for (int i = 0; i < w; ++i) add += s_warp[i];
+  bases[t] = x - c + add;
+}
+
+__global__ void k_relink_head(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
+                              const uint32_t* __restrict__ ids1, uint32_t* __restrict__ d_head,
+                              const int* __restrict__ err) {
+  if (*err) return;
+  *d_head = ((plan->npasses & 1) ? ids1 : ids0)[0];
+}
+
+// Level 3: one CTA per fine bin: scatter into a 64 KB smem window, write it coalesced.
+__global__ void __launch_bounds__(512)
+k_relink_apply(const uint32_t* __restrict__ pv, const uint32_t* __restrict__ ps, uint32_t n,
+               uint32_t* __restrict__ out_next, const int* __restrict__ err) {
+  extern __shared__ __align__(16) uint32_t s_win[];
+  if (*err) return;
+  const uint32_t f0 = blockIdx.x << RELINK_FINE_SHIFT;
+  const uint32_t cnt = min((uint32_t)(1u << RELINK_FINE_SHIFT), n - f0);
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) s_win[__ldcs(pv + f0 + i) - f0] = __ldcs(ps + f0 + i);
+  __syncthreads();
+  uint32_t* dst = out_next + f0;
+  if ((cnt & 3u) == 0 && ((uintptr_t)dst & 15u) == 0) {
+    for (uint32_t i = threadIdx.x; i < cnt / 4; i += blockDim.x)
+      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(s_win)[i];
+  } else {
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = s_win[i];
+  }
+}
+
+// n <= 2^14: the whole out_next is one window.
+__global__ void __launch_bounds__(512)
+k_relink_small(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, const uint32_t* __restrict__ ids1,
+               uint32_t n, uint32_t* __restrict__ out_next, const int* __restrict__ err) {
+  extern __shared__ __align__(16) uint32_t s_win[];
   if (*err) return;
   const uint32_t* __restrict__ ids = (plan->npasses & 1) ? ids1 : ids0;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    const uint32_t v = ids[p];
-    const uint32_t s = (p + 1 < n) ? ids[p + 1] : PBIT_NULL32;
-    out_next[v] = s;
-    if (p == 0) *d_head = v;
-  }
+  for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) s_win[ids[p]] = p + 1 < n ? ids[p + 1] : PBIT_NULL32;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out_next[i] = s_win[i];
 }
 
 }  // namespace pbit

@@ -9,6 +9,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <mutex>
 
@@ -46,6 +48,17 @@ int device_info(int dev, int* sms) {
   return PBIT_OK;
 }
 
+// L2 fetch granularity for the random-access phases (walk, relink): a random 8 B read
+// otherwise pulls a whole 128 B line from HBM (ncu: 4.2 DRAM sectors per node).
+static int l2_fetch_bytes() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("PBIT_L2_FETCH");
+    v = e ? atoi(e) : 32;
+  }
+  return v;
+}
+
 // ----------------------------------------------------------------------------- planning
 void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   p->n = (uint32_t)n;
@@ -54,7 +67,9 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   p->D = (key_bits + K - 1) / K;
   // ruler spacing: ~64 nodes per segment on large lists, more rulers on small ones so the
   // walk still has enough independent walkers (and short tails)
-  int s_log2 = 6;
+  static int env_s = -2;
+  if (env_s == -2) { const char* e = getenv("PBIT_RULER_LOG2"); env_s = e ? atoi(e) : -1; }
+  int s_log2 = env_s > 0 ? env_s : 6;
   while (s_log2 > 2 && (n >> s_log2) < (1u << 14)) --s_log2;
   p->s_log2 = s_log2;
   p->cap = 4u << s_log2;
@@ -63,29 +78,44 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
 }
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
+static constexpr int SUB_LOG2 = 4;  // one sub-ruler per 16 rulers
 
 // ----------------------------------------------------------------------------- dispatch
+static bool use_match() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("PBIT_MATCH"); v = e ? atoi(e) : 0; }
+  return v != 0;
+}
+
+// One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
+template <typename KeyT, int RB, int IPT, bool MATCH>
+static void launch_one(const SweepArgs& a, cudaStream_t st) {
+  using S = SweepSmem<KeyT, RB, IPT>;
+  static bool attr = false;  // benign race: idempotent
+  if (!attr) {
+    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S));
+    attr = true;
+  }
+  const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
+  k_onesweep<KeyT, RB, IPT, MATCH><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+}
+
 template <int KB, int RB>
-static void launch_sweeps(const Plan* plan, int D, void* keys0, uint32_t* ids0, void* keys1, uint32_t* ids1,
-                          const uint32_t* bases, unsigned long long* status, uint32_t* tile_ctr, uint32_t n,
-                          const int* err, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
+static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
   using KeyT = typename KeyOf<KB>::T;
   constexpr int IPT = (KB == 8) ? 12 : 16;
-  constexpr int TILE = SWEEP_THREADS * IPT;
-  const uint32_t ntiles = (n + TILE - 1) / TILE;
   for (int s = 0; s < D; ++s) {
-    k_onesweep<KeyT, RB, IPT><<<ntiles, SWEEP_THREADS, 0, st>>>(
-        plan, s, (KeyT*)keys0, ids0, (KeyT*)keys1, ids1, bases, status, tile_ctr, n, err);
+    a.slot = s;
+    if (use_match()) launch_one<KeyT, RB, IPT, true>(a, st);
+    else launch_one<KeyT, RB, IPT, false>(a, st);
     if (ev) cudaEventRecord(ev[ev_base + s], st);
   }
 }
 
 template <int KB>
-static void launch_sweeps_k(int K, const Plan* plan, int D, void* keys0, uint32_t* ids0, void* keys1,
-                            uint32_t* ids1, const uint32_t* bases, unsigned long long* status, uint32_t* tile_ctr,
-                            uint32_t n, const int* err, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
+static void launch_key_passes_k(int K, const SweepArgs& a, int D, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
   switch (K) {
-#define PBIT_K(RB) case RB: launch_sweeps<KB, RB>(plan, D, keys0, ids0, keys1, ids1, bases, status, tile_ctr, n, err, st, ev, ev_base); break;
+#define PBIT_K(RB) case RB: launch_key_passes<KB, RB>(a, D, st, ev, ev_base); break;
     PBIT_K(1) PBIT_K(2) PBIT_K(3) PBIT_K(4) PBIT_K(5) PBIT_K(6) PBIT_K(7) PBIT_K(8)
 #undef PBIT_K
   }
@@ -95,11 +125,12 @@ size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64
 
 // Workspace layout (all 256-byte aligned).
 struct Ws {
-  void* kn; void* slots; uint32_t* seg_len; uint32_t* seg_succ;
-  unsigned long long* dist[2]; uint32_t* succ[2];
-  void* keys[2]; uint32_t* ids[2]; unsigned long long* status;
+  void* kn; void* slots; uint2* seg; uint32_t* dist;
+  unsigned long long* sdist[2]; uint32_t* ssucc[2];
+  void* keys[2]; uint32_t* ids[2]; unsigned long long* status; uint32_t* rk[2]; uint32_t* rv[2];
   // control block (zeroed per call)
   uint32_t* hist; uint32_t* bases; Plan* plan; int* err; uint32_t* dyn_count; uint32_t* tile_ctr; uint32_t* d_head;
+  uint32_t* rbases;
   size_t ctl_bytes; void* ctl; size_t status_bytes;
 };
 
@@ -115,12 +146,17 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   size_t off = 0;
   auto take = [&](size_t bytes) { char* q = base ? base + off : nullptr; off += align_up(bytes); return (void*)q; };
   w->kn = take(n * rec);
-  w->slots = take(Rmax * p.cap * rec);
-  w->seg_len = (uint32_t*)take(Rmax * 4);
-  w->seg_succ = (uint32_t*)take(Rmax * 4);
-  for (int i = 0; i < 2; ++i) { w->dist[i] = (unsigned long long*)take(Rmax * 8); w->succ[i] = (uint32_t*)take(Rmax * 4); }
+  w->slots = take(Rmax * p.cap * rec);  // also holds the relink pairs (dead slots by then)
+  for (int i = 0; i < 2; ++i) {  // relink (v, succ) buffers: 4 x n u32 <= slot bytes
+    w->rk[i] = base ? (uint32_t*)w->slots + (2 * i) * align_up(n) : nullptr;
+    w->rv[i] = base ? (uint32_t*)w->slots + (2 * i + 1) * align_up(n) : nullptr;
+  }
+  w->seg = (uint2*)take(Rmax * 8);
+  w->dist = (uint32_t*)take(Rmax * 4);
+  const size_t nsub = (Rmax >> SUB_LOG2) + 2;
+  for (int i = 0; i < 2; ++i) { w->sdist[i] = (unsigned long long*)take(nsub * 8); w->ssucc[i] = (uint32_t*)take(nsub * 4); }
   for (int i = 0; i < 2; ++i) { w->keys[i] = take(n * kbytes); w->ids[i] = (uint32_t*)take(n * 4); }
-  w->status_bytes = ntiles * radix * 8;
+  w->status_bytes = ntiles * (radix > 256 ? radix : 256) * 8;  // relink passes use 256
   w->status = (unsigned long long*)take(w->status_bytes);
   const size_t ctl0 = off;
   w->hist = (uint32_t*)take((size_t)p.D * radix * 4);
@@ -128,8 +164,9 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   w->plan = (Plan*)take(sizeof(Plan));
   w->err = (int*)take(4);
   w->dyn_count = (uint32_t*)take(4);
-  w->tile_ctr = (uint32_t*)take(64 * 4);
+  w->tile_ctr = (uint32_t*)take(80 * 4);
   w->d_head = (uint32_t*)take(4);
+  w->rbases = (uint32_t*)take(4 * 256 * 4);
   w->ctl = base ? base + ctl0 : nullptr;
   w->ctl_bytes = off - ctl0;
   return off;
@@ -157,6 +194,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   const int radix = 1 << p.K;
   uint32_t launches = 0;
 
+  if (l2_fetch_bytes() > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch_bytes());
   cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, st);
   cudaMemsetAsync(w.status, 0, w.status_bytes, st);
 
@@ -179,33 +217,38 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t min_per = 4;
     if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
-    k_walk<KB><<<blocks, WALK_THREADS, 0, st>>>((const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap,
-                                                w.seg_len, w.seg_succ, w.dyn_count, p.dyn_cap, per_cta, w.err);
+    k_walk<KB><<<blocks, WALK_THREADS, 0, st>>>((const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap, w.seg,
+                                                w.dyn_count, p.dyn_cap, per_cta, w.err);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_WALK], st);
 
-  // a1: ruler ranking
+  // a1: ruler ranking (second ruling set + pointer jumping over the sub-rulers)
   {
     const uint32_t Rmax = R_static + p.dyn_cap;
+    RulerSel sub{Rmax, (uint32_t)SUB_LOG2, (Rmax + (1u << SUB_LOG2) - 1) >> SUB_LOG2};
+    const bool hs = sub.is_ruler(head_ruler);
+    const uint32_t nsub = sub.R + (hs ? 0u : 1u);
+    const uint32_t head_sub = hs ? (head_ruler >> SUB_LOG2) : sub.R;
+    const int sblocks = std::max(1, std::min((int)((nsub + 255) / 256), sms * 8));
+    k_rank_walk_a<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
+                                           w.sdist[0], w.ssucc[0], w.err);
     int rounds = 1;
-    while ((1ull << rounds) < Rmax) ++rounds;
+    while ((1ull << rounds) < nsub) ++rounds;
     rounds += 1;
-    const int blocks = std::max(1, std::min((int)((Rmax + 255) / 256), sms * 8));
-    k_rank_init<<<blocks, 256, 0, st>>>(w.seg_len, w.seg_succ, R_static, w.dyn_count, p.dyn_cap, w.dist[0],
-                                        w.succ[0], w.err);
     int cur = 0;
     for (int i = 0; i < rounds; ++i) {
-      k_rank_jump<<<blocks, 256, 0, st>>>(w.dist[cur], w.succ[cur], w.dist[cur ^ 1], w.succ[cur ^ 1], R_static,
-                                          w.dyn_count, p.dyn_cap, w.err);
+      k_rank_jump<<<sblocks, 256, 0, st>>>(w.sdist[cur], w.ssucc[cur], w.sdist[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
       cur ^= 1;
     }
-    k_rank_check<<<1, 1, 0, st>>>(w.dist[cur], w.succ[cur], head_ruler, n, w.err);
-    launches += rounds + 2;
+    k_rank_check<<<1, 1, 0, st>>>(w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
+    k_rank_walk_b<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
+                                           w.sdist[cur], w.dist, w.err);
+    launches += rounds + 3;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
     // a1: gather to list order
     const int gblocks = std::max(1, std::min((int)((Rmax + 7) / 8), sms * 8));
-    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg_len, w.dist[cur], R_static, w.dyn_count,
+    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, R_static, w.dyn_count,
                                           p.dyn_cap, n, (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.err);
     ++launches;
   }
@@ -215,14 +258,58 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (timing) cudaEventRecord(ev[PBIT_PHASE_GATHER], st);
 
   // a3/a4: passes
-  launch_sweeps_k<KB>(p.K, w.plan, p.D, w.keys[0], w.ids[0], w.keys[1], w.ids[1], w.bases, w.status, w.tile_ctr, n,
-                      w.err, st, timing ? ev : nullptr, PBIT_PHASE_PASS0);
+  SweepArgs sa{};
+  sa.kin[0] = w.keys[0]; sa.kin[1] = w.keys[1]; sa.vin[0] = w.ids[0]; sa.vin[1] = w.ids[1];
+  sa.kout[0] = w.keys[0]; sa.kout[1] = w.keys[1]; sa.vout[0] = w.ids[0]; sa.vout[1] = w.ids[1];
+  sa.bases = w.bases; sa.status = w.status; sa.tile_ctr = w.tile_ctr; sa.plan = w.plan; sa.err = w.err; sa.n = n;
+  sa.kind = 0;
+  launch_key_passes_k<KB>(p.K, sa, p.D, st, timing ? ev : nullptr, PBIT_PHASE_PASS0);
   launches += p.D;
 
-  // a5: relink
+  // a5: relink: sort (v, succ) by v >> RELINK_FINE_SHIFT (LSD, 8-bit digits), then apply
+  // each 2^14-id bin in a shared-memory window
   {
-    const int blocks = std::max(1, std::min((int)((n + 255) / 256), sms * 8));
-    k_relink<<<blocks, 256, 0, st>>>(w.plan, w.ids[0], w.ids[1], n, out_next, w.d_head, w.err);
+    int top = 1;
+    while ((1ull << top) < n) ++top;
+    const int npass = top > RELINK_FINE_SHIFT ? (top - RELINK_FINE_SHIFT + 7) / 8 : 0;
+    k_relink_head<<<1, 1, 0, st>>>(w.plan, w.ids[0], w.ids[1], w.d_head, w.err);
+    ++launches;
+    SweepArgs ra = sa;
+    ra.kin[0] = w.ids[0]; ra.kin[1] = w.ids[1];  // kind 1 reads the final ids
+    const uint32_t* fin_k = nullptr; const uint32_t* fin_v = nullptr;
+    for (int q = 0; q < npass; ++q) {
+      const int bit0 = RELINK_FINE_SHIFT + 8 * q;
+      k_relink_bases<<<1, 256, 0, st>>>(n, bit0, w.rbases + 256 * q);
+      ra.bases = w.rbases + 256 * q;
+      ra.slot = 64 + q;  // key passes use slots 0..63
+      ra.bit0 = bit0;
+      if (q == 0) {
+        ra.kind = 1;
+        ra.kout[0] = w.rk[0]; ra.vout[0] = w.rv[0];
+      } else {
+        ra.kind = 2;
+        ra.par = (q - 1) & 1;
+        ra.kin[0] = w.rk[0]; ra.kin[1] = w.rk[1]; ra.vin[0] = w.rv[0]; ra.vin[1] = w.rv[1];
+        ra.kout[0] = w.rk[0]; ra.kout[1] = w.rk[1]; ra.vout[0] = w.rv[0]; ra.vout[1] = w.rv[1];
+      }
+      if (use_match()) launch_one<uint32_t, 8, 16, true>(ra, st);
+      else launch_one<uint32_t, 8, 16, false>(ra, st);
+      fin_k = w.rk[q & 1]; fin_v = w.rv[q & 1];
+      launches += 2;
+    }
+    const uint32_t nfine = (n + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_relink_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
+      cudaFuncSetAttribute(k_relink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
+      attr = true;
+    }
+    if (npass == 0) {
+      // n <= 2^14: one window; the pairs come straight from the final ids
+      k_relink_small<<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(w.plan, w.ids[0], w.ids[1], n, out_next, w.err);
+    } else {
+      k_relink_apply<<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(fin_k, fin_v, n, out_next, w.err);
+    }
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
