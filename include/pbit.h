@@ -139,6 +139,9 @@ int pbit_mg_get_unique_id(void *id_out /* PBIT_MG_UNIQUE_ID_BYTES host bytes */)
 int pbit_mg_comm_init(void **comm_out, int nranks, const void *id, int rank);
 int pbit_mg_comm_destroy(void *comm);
 
+/* Text of the last CUDA or NCCL error seen by the calling host thread ("" if none). */
+const char *pbit_last_error(void);
+
 /* Human-readable name of a status code (static string). */
 const char *pbit_status_string(int status);
 

@@ -21,7 +21,7 @@ PBIT_NULL = 0xFFFFFFFF
 NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
 SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
-           "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version"]
+           "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version", "pbit_last_error"]
 
 STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
           4: "PBIT_ERR_CUDA", 5: "PBIT_ERR_NCCL", 6: "PBIT_ERR_UNSUPPORTED"}
@@ -61,6 +61,7 @@ def _load():
     lib.pbit_status_string.restype = ctypes.c_char_p
     lib.pbit_status_string.argtypes = [ctypes.c_int]
     lib.pbit_version.restype = ctypes.c_uint32
+    lib.pbit_last_error.restype = ctypes.c_char_p
     return lib
 
 
@@ -68,6 +69,13 @@ lib = _load()
 
 _KEY_BITS = {torch.uint8: 8, torch.int8: 8, torch.int16: 16, torch.uint16: 16, torch.int32: 32,
              torch.uint32: 32, torch.int64: 64, torch.uint64: 64}
+
+
+def _errtext(rc: int) -> str:
+    t = lib.pbit_status_string(rc).decode()
+    if rc in (4, 5):
+        t += f" ({lib.pbit_last_error().decode()})"
+    return t
 
 
 def _ptr(t) -> int:
@@ -121,7 +129,7 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
     rc = lib.pbit_sort_list(_ptr(keys) if n else None, _ptr(next_) if n else None, head & 0xFFFFFFFF, n, key_bits,
                             ctypes.byref(oh), _ptr(out_next) if n else None, ctypes.byref(o))
     if rc:
-        raise PbitError(rc, lib.pbit_status_string(rc).decode())
+        raise PbitError(rc, _errtext(rc))
     if timing:
         ph = {name: float(pm[i]) for i, name in enumerate(PHASE_NAMES) if i < 5 or pm[i] > 0}
         ph["passes_run"] = int(passes.value)
@@ -166,5 +174,5 @@ def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int,
                                head & 0xFFFFFFFF, n_global, node_lo, n_local, key_bits, ctypes.byref(oh),
                                _ptr(out_next_local) if n_local else None, ctypes.c_void_p(comm), ctypes.byref(o))
     if rc:
-        raise PbitError(rc, lib.pbit_status_string(rc).decode())
+        raise PbitError(rc, _errtext(rc))
     return int(oh.value), out_next_local

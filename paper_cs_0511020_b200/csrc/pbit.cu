@@ -7,11 +7,13 @@
 // between kernels: the pass plan lives on the device.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <string.h>
 
 #include <stdlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "../../include/pbit.h"
@@ -19,6 +21,12 @@
 #include "pbit_internal.h"
 
 namespace pbit {
+
+// Text of the last CUDA/NCCL failure seen by this host thread (pbit_last_error()).
+static thread_local char g_last_err[256] = "";
+void set_last_error(const char* what, const char* detail) {
+  snprintf(g_last_err, sizeof g_last_err, "%s: %s", what, detail ? detail : "");
+}
 
 // ----------------------------------------------------------------------------- device info
 struct DevInfo {
@@ -77,27 +85,60 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   p->dyn_cap = (uint32_t)(n / p->cap + 1);
 }
 
+static int debug_env(const char* name) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : 0;
+}
+
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 static constexpr int SUB_LOG2 = 4;  // one sub-ruler per 16 rulers
 
 // ----------------------------------------------------------------------------- dispatch
-static bool use_match() {
-  static int v = -1;
-  if (v < 0) { const char* e = getenv("PBIT_MATCH"); v = e ? atoi(e) : 0; }
-  return v != 0;
+// In-warp ranking mode for the stable key passes: RANK_ATOMIC unless the load-time
+// self-test fails (or PBIT_RANK=ballot|match|atomic overrides, for experiments).
+static std::atomic<int> g_rank_mode{-1};
+
+static int rank_mode() { return g_rank_mode.load(std::memory_order_relaxed); }
+
+static void init_rank_mode(cudaStream_t st) {
+  if (g_rank_mode.load() >= 0) return;
+  int mode = RANK_ATOMIC;
+  if (const char* e = getenv("PBIT_RANK")) {
+    mode = !strcmp(e, "ballot") ? RANK_BALLOT : !strcmp(e, "match") ? RANK_MATCH : RANK_ATOMIC;
+  } else {
+    uint32_t* d_bad = nullptr;
+    uint32_t bad = 1;
+    if (cudaMallocAsync((void**)&d_bad, 4, st) == cudaSuccess) {
+      cudaMemsetAsync(d_bad, 0, 4, st);
+      k_selftest_atomic_order<<<64, SWEEP_THREADS, 0, st>>>(4096, d_bad);
+      cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st);
+      cudaFreeAsync(d_bad, st);
+      if (cudaStreamSynchronize(st) != cudaSuccess) bad = 1;
+    }
+    cudaGetLastError();
+    if (bad) mode = RANK_BALLOT;
+  }
+  g_rank_mode.store(mode);
 }
 
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
-template <typename KeyT, int RB, int IPT, bool MATCH>
-static void launch_one(const SweepArgs& a, cudaStream_t st) {
+template <typename KeyT, int RB, int IPT, int RANK>
+static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
   static bool attr = false;  // benign race: idempotent
   if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, MATCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S));
+    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S));
     attr = true;
   }
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  k_onesweep<KeyT, RB, IPT, MATCH><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+  k_onesweep<KeyT, RB, IPT, RANK><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+}
+
+template <typename KeyT, int RB, int IPT>
+static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
+  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC>(a, st);
+  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH>(a, st);
+  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT>(a, st);
 }
 
 template <int KB, int RB>
@@ -106,8 +147,7 @@ static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* 
   constexpr int IPT = (KB == 8) ? 12 : 16;
   for (int s = 0; s < D; ++s) {
     a.slot = s;
-    if (use_match()) launch_one<KeyT, RB, IPT, true>(a, st);
-    else launch_one<KeyT, RB, IPT, false>(a, st);
+    launch_one<KeyT, RB, IPT>(a, st, rank_mode());
     if (ev) cudaEventRecord(ev[ev_base + s], st);
   }
 }
@@ -193,6 +233,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   const uint32_t n = p.n;
   const int radix = 1 << p.K;
   uint32_t launches = 0;
+  init_rank_mode(st);
 
   if (l2_fetch_bytes() > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch_bytes());
   cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, st);
@@ -218,7 +259,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
     k_walk<KB><<<blocks, WALK_THREADS, 0, st>>>((const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap, w.seg,
-                                                w.dyn_count, p.dyn_cap, per_cta, w.err);
+                                                w.dyn_count, p.dyn_cap, per_cta, w.err, debug_env("PBIT_DEBUG_WALK_NOWRITE"));
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_WALK], st);
@@ -263,18 +304,20 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   sa.kout[0] = w.keys[0]; sa.kout[1] = w.keys[1]; sa.vout[0] = w.ids[0]; sa.vout[1] = w.ids[1];
   sa.bases = w.bases; sa.status = w.status; sa.tile_ctr = w.tile_ctr; sa.plan = w.plan; sa.err = w.err; sa.n = n;
   sa.kind = 0;
+  { const char* e = getenv("PBIT_DEBUG_NO_LOOKBACK"); sa.debug_no_lookback = e ? atoi(e) : 0; }
   launch_key_passes_k<KB>(p.K, sa, p.D, st, timing ? ev : nullptr, PBIT_PHASE_PASS0);
   launches += p.D;
 
   // a5: relink: sort (v, succ) by v >> RELINK_FINE_SHIFT (LSD, 8-bit digits), then apply
   // each 2^14-id bin in a shared-memory window
-  {
+  if (!sa.debug_no_lookback) {
     int top = 1;
     while ((1ull << top) < n) ++top;
     const int npass = top > RELINK_FINE_SHIFT ? (top - RELINK_FINE_SHIFT + 7) / 8 : 0;
     k_relink_head<<<1, 1, 0, st>>>(w.plan, w.ids[0], w.ids[1], w.d_head, w.err);
     ++launches;
     SweepArgs ra = sa;
+    ra.debug_no_lookback = 0;
     ra.kin[0] = w.ids[0]; ra.kin[1] = w.ids[1];  // kind 1 reads the final ids
     const uint32_t* fin_k = nullptr; const uint32_t* fin_v = nullptr;
     for (int q = 0; q < npass; ++q) {
@@ -292,8 +335,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
         ra.kin[0] = w.rk[0]; ra.kin[1] = w.rk[1]; ra.vin[0] = w.rv[0]; ra.vin[1] = w.rv[1];
         ra.kout[0] = w.rk[0]; ra.kout[1] = w.rk[1]; ra.vout[0] = w.rv[0]; ra.vout[1] = w.rv[1];
       }
-      if (use_match()) launch_one<uint32_t, 8, 16, true>(ra, st);
-      else launch_one<uint32_t, 8, 16, false>(ra, st);
+      // LSD over two digits: the relink passes must be stable too
+      launch_one<uint32_t, 8, 16>(ra, st, rank_mode());
       fin_k = w.rk[q & 1]; fin_v = w.rv[q & 1];
       launches += 2;
     }
@@ -323,7 +366,11 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   cudaError_t es = cudaStreamSynchronize(st);
   cudaError_t el = cudaGetLastError();
   int rc = PBIT_OK;
-  if (e1 || e2 || e3 || es || el) rc = PBIT_ERR_CUDA;
+  if (e1 || e2 || e3 || es || el) {
+    rc = PBIT_ERR_CUDA;
+    const cudaError_t e = es ? es : el ? el : e1 ? e1 : e2 ? e2 : e3;
+    set_last_error("pbit_sort_list", cudaGetErrorString(e));
+  }
   if (timing) {
     if (rc == PBIT_OK) {
       for (int i = 0; i < PBIT_NUM_PHASES; ++i) phase_ms[i] = 0.f;
@@ -379,6 +426,8 @@ using namespace pbit;
 extern "C" {
 
 uint32_t pbit_version(void) { return (0u << 16) | (1u << 8) | 0u; }
+
+const char* pbit_last_error(void) { return g_last_err; }
 
 const char* pbit_status_string(int s) {
   switch (s) {

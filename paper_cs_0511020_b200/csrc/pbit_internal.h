@@ -16,6 +16,7 @@ struct SortPlan {
   uint32_t dyn_cap;
 };
 
+void set_last_error(const char* what, const char* detail);
 void make_plan(uint64_t n, int key_bits, int K, SortPlan* p);
 int device_info(int dev, int* sms);
 int pointer_kind(const void* ptr, int dev);
