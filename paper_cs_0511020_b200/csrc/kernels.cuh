@@ -19,7 +19,7 @@ namespace pbit {
 
 constexpr int PACK_THREADS = 256;
 constexpr int WALK_THREADS = 256;
-constexpr int SWEEP_THREADS = 256;
+constexpr int SWEEP_THREADS = 512;  // 16 warps x 16 items: 8192-item tiles halve the lookback traffic
 constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
 
 // ============================================================================ a1/a2: pack
@@ -141,13 +141,13 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
 // the end.  Segment r then occupies list positions [n - dist[r], n - dist[r] + len[r]).
 __global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
                               const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
-                              uint32_t nsub, unsigned long long* __restrict__ sdist, uint32_t* __restrict__ ssucc,
-                              int* __restrict__ err) {
+                              uint32_t nsub, unsigned long long* __restrict__ sdist, uint32_t* __restrict__ scnt,
+                              uint32_t* __restrict__ ssucc, int* __restrict__ err) {
   if (*err) return;
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
     const uint32_t rq = q < sub.R ? sub.node_of(q) : head_ruler;
-    if (rq >= R) { sdist[q] = 0; ssucc[q] = PBIT_NULL32; continue; }
+    if (rq >= R) { sdist[q] = 0; scnt[q] = 0; ssucc[q] = PBIT_NULL32; continue; }
     unsigned long long acc = 0;
     uint32_t r = rq, steps = 0, succ = PBIT_NULL32;
     for (;;) {
@@ -159,20 +159,24 @@ __global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint3
       r = x.y;
     }
     sdist[q] = acc;
+    scnt[q] = steps + 1;  // rulers in this sub-segment
     ssucc[q] = succ;
   }
 }
 
-__global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const uint32_t* __restrict__ s_in,
-                            unsigned long long* __restrict__ d_out, uint32_t* __restrict__ s_out, uint32_t m,
+__global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const uint32_t* __restrict__ c_in,
+                            const uint32_t* __restrict__ s_in, unsigned long long* __restrict__ d_out,
+                            uint32_t* __restrict__ c_out, uint32_t* __restrict__ s_out, uint32_t m,
                             const int* __restrict__ err) {
   if (*err) return;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const uint32_t s = s_in[r];
     unsigned long long d = d_in[r];
+    uint32_t c = c_in[r];
     uint32_t s2 = s;
-    if (s != PBIT_NULL32) { d += d_in[s]; s2 = s_in[s]; }
+    if (s != PBIT_NULL32) { d += d_in[s]; c += c_in[s]; s2 = s_in[s]; }
     d_out[r] = d;
+    c_out[r] = c;
     s_out[r] = s2;
   }
 }
@@ -185,19 +189,28 @@ __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const 
   if (succ[head_sub] != PBIT_NULL32 || dist[head_sub] != (unsigned long long)n) atomicOr(err, E_CHAIN);
 }
 
+// Walk B also numbers the segments in list order: seg_ord[k] = the k-th segment of the
+// list, so later kernels visit segments in list order (adjacent output runs are then
+// written close together in time and their shared boundary sectors merge in L2).
 __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
                               const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
-                              uint32_t nsub, const unsigned long long* __restrict__ sdist,
-                              uint32_t* __restrict__ dist, const int* __restrict__ err) {
+                              uint32_t nsub, uint32_t head_sub, const unsigned long long* __restrict__ sdist,
+                              const uint32_t* __restrict__ scnt, uint32_t* __restrict__ dist,
+                              uint32_t* __restrict__ seg_ord, uint32_t* __restrict__ nseg_out,
+                              const int* __restrict__ err) {
   if (*err) return;
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
+  const uint32_t total = scnt[head_sub];  // segments on the chain (= R for a valid list)
+  if (blockIdx.x == 0 && threadIdx.x == 0) *nseg_out = total;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
     const uint32_t rq = q < sub.R ? sub.node_of(q) : head_ruler;
     if (rq >= R) continue;
     uint32_t D = (uint32_t)sdist[q];
+    uint32_t k = total - scnt[q];
     uint32_t r = rq;
     for (;;) {
       dist[r] = D;
+      seg_ord[k++] = r;
       const uint2 x = seg[r];
       D -= x.x;
       if (x.y == PBIT_NULL32 || sub.is_ruler(x.y)) break;
@@ -207,32 +220,51 @@ __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint3
 }
 
 // ============================================================================ a1: gather
-// Segment r occupies list positions [n - dist[r], n - dist[r] + len[r]).  One warp per
-// segment copies its slot into the list-order arrays (coalesced both ways).
+// Segment r occupies list positions [n - dist[r], n - dist[r] + len[r]).  Each warp
+// copies GATHER_SEGS consecutive segments of the list at once (their loads in flight
+// together) from the slots to the list-order arrays; both sides are contiguous runs.
+constexpr int GATHER_SEGS = 4;
 template <int KB>
-__global__ void k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
-                         const uint2* __restrict__ seg, const uint32_t* __restrict__ dist,
-                         uint32_t R_static, const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t n,
-                         typename KeyOf<KB>::T* __restrict__ keys_lo, uint32_t* __restrict__ ids_lo,
-                         const int* __restrict__ err) {
+__global__ void __launch_bounds__(256)
+k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
+         const uint2* __restrict__ seg, const uint32_t* __restrict__ dist,
+         const uint32_t* __restrict__ seg_ord, const uint32_t* __restrict__ nseg, uint32_t n,
+         typename KeyOf<KB>::T* __restrict__ keys_lo, uint32_t* __restrict__ ids_lo,
+         const int* __restrict__ err) {
+  using RT = typename Rec<KB>::T;
   if (*err) return;
-  const uint32_t R = R_static + min(*dyn_count, dyn_cap);
+  const uint32_t R = *nseg;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t r = warp; r < R; r += nwarps) {
-    const uint32_t len = seg[r].x;
-    const uint32_t off = n - dist[r];
-    const typename Rec<KB>::T* src = slots + (size_t)r * cap;
-    for (uint32_t j = lane; j < len; j += 32) {
-      if constexpr (KB == 8) {
-        uint4 x = src[j];
-        keys_lo[off + j] = ((unsigned long long)x.y << 32) | x.x;
-        ids_lo[off + j] = x.z;
-      } else {
-        uint2 x = src[j];
-        keys_lo[off + j] = x.x;
-        ids_lo[off + j] = x.y;
+  for (uint32_t r0 = warp * GATHER_SEGS; r0 < R; r0 += nwarps * GATHER_SEGS) {
+    uint32_t len[GATHER_SEGS], off[GATHER_SEGS], rr[GATHER_SEGS];
+#pragma unroll
+    for (int q = 0; q < GATHER_SEGS; ++q) {
+      const uint32_t k = r0 + q;
+      rr[q] = k < R ? seg_ord[k] : 0u;
+      len[q] = k < R ? seg[rr[q]].x : 0u;
+      off[q] = k < R ? n - dist[rr[q]] : 0u;
+    }
+    uint32_t mx = 0;
+#pragma unroll
+    for (int q = 0; q < GATHER_SEGS; ++q) mx = max(mx, len[q]);
+    for (uint32_t j = lane; j < mx; j += 32) {
+      RT x[GATHER_SEGS];
+#pragma unroll
+      for (int q = 0; q < GATHER_SEGS; ++q)
+        if (j < len[q]) x[q] = __ldcs(slots + (size_t)rr[q] * cap + j);
+#pragma unroll
+      for (int q = 0; q < GATHER_SEGS; ++q) {
+        if (j < len[q]) {
+          if constexpr (KB == 8) {
+            keys_lo[off[q] + j] = ((unsigned long long)x[q].y << 32) | x[q].x;
+            ids_lo[off[q] + j] = x[q].z;
+          } else {
+            keys_lo[off[q] + j] = x[q].x;
+            ids_lo[off[q] + j] = x[q].y;
+          }
+        }
       }
     }
   }
@@ -366,7 +398,7 @@ struct SweepArgs {
 enum : int { RANK_BALLOT = 0, RANK_MATCH = 1, RANK_ATOMIC = 2 };
 
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK>
-__global__ void __launch_bounds__(SWEEP_THREADS, 4)
+__global__ void __launch_bounds__(SWEEP_THREADS, 2)
 k_onesweep(const __grid_constant__ SweepArgs a) {
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
   constexpr int RADIX = S::RADIX;

@@ -110,7 +110,7 @@ static void init_rank_mode(cudaStream_t st) {
     uint32_t bad = 1;
     if (cudaMallocAsync((void**)&d_bad, 4, st) == cudaSuccess) {
       cudaMemsetAsync(d_bad, 0, 4, st);
-      k_selftest_atomic_order<<<64, SWEEP_THREADS, 0, st>>>(4096, d_bad);
+      k_selftest_atomic_order<<<64, 256, 0, st>>>(4096, d_bad);
       cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st);
       cudaFreeAsync(d_bad, st);
       if (cudaStreamSynchronize(st) != cudaSuccess) bad = 1;
@@ -166,11 +166,11 @@ size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64
 // Workspace layout (all 256-byte aligned).
 struct Ws {
   void* kn; void* slots; uint2* seg; uint32_t* dist;
-  unsigned long long* sdist[2]; uint32_t* ssucc[2];
+  unsigned long long* sdist[2]; uint32_t* scnt[2]; uint32_t* ssucc[2]; uint32_t* seg_ord;
   void* keys[2]; uint32_t* ids[2]; unsigned long long* status; uint32_t* rk[2]; uint32_t* rv[2];
   // control block (zeroed per call)
   uint32_t* hist; uint32_t* bases; Plan* plan; int* err; uint32_t* dyn_count; uint32_t* tile_ctr; uint32_t* d_head;
-  uint32_t* rbases;
+  uint32_t* rbases; uint32_t* nseg;
   size_t ctl_bytes; void* ctl; size_t status_bytes;
 };
 
@@ -194,7 +194,12 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   w->seg = (uint2*)take(Rmax * 8);
   w->dist = (uint32_t*)take(Rmax * 4);
   const size_t nsub = (Rmax >> SUB_LOG2) + 2;
-  for (int i = 0; i < 2; ++i) { w->sdist[i] = (unsigned long long*)take(nsub * 8); w->ssucc[i] = (uint32_t*)take(nsub * 4); }
+  for (int i = 0; i < 2; ++i) {
+    w->sdist[i] = (unsigned long long*)take(nsub * 8);
+    w->scnt[i] = (uint32_t*)take(nsub * 4);
+    w->ssucc[i] = (uint32_t*)take(nsub * 4);
+  }
+  w->seg_ord = (uint32_t*)take(Rmax * 4);
   for (int i = 0; i < 2; ++i) { w->keys[i] = take(n * kbytes); w->ids[i] = (uint32_t*)take(n * 4); }
   w->status_bytes = ntiles * (radix > 256 ? radix : 256) * 8;  // relink passes use 256
   w->status = (unsigned long long*)take(w->status_bytes);
@@ -207,6 +212,7 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   w->tile_ctr = (uint32_t*)take(80 * 4);
   w->d_head = (uint32_t*)take(4);
   w->rbases = (uint32_t*)take(4 * 256 * 4);
+  w->nseg = (uint32_t*)take(4);
   w->ctl = base ? base + ctl0 : nullptr;
   w->ctl_bytes = off - ctl0;
   return off;
@@ -273,24 +279,25 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t head_sub = hs ? (head_ruler >> SUB_LOG2) : sub.R;
     const int sblocks = std::max(1, std::min((int)((nsub + 255) / 256), sms * 8));
     k_rank_walk_a<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
-                                           w.sdist[0], w.ssucc[0], w.err);
+                                           w.sdist[0], w.scnt[0], w.ssucc[0], w.err);
     int rounds = 1;
     while ((1ull << rounds) < nsub) ++rounds;
     rounds += 1;
     int cur = 0;
     for (int i = 0; i < rounds; ++i) {
-      k_rank_jump<<<sblocks, 256, 0, st>>>(w.sdist[cur], w.ssucc[cur], w.sdist[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
+      k_rank_jump<<<sblocks, 256, 0, st>>>(w.sdist[cur], w.scnt[cur], w.ssucc[cur], w.sdist[cur ^ 1],
+                                           w.scnt[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
       cur ^= 1;
     }
     k_rank_check<<<1, 1, 0, st>>>(w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
     k_rank_walk_b<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
-                                           w.sdist[cur], w.dist, w.err);
+                                           head_sub, w.sdist[cur], w.scnt[cur], w.dist, w.seg_ord, w.nseg, w.err);
     launches += rounds + 3;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
     // a1: gather to list order
-    const int gblocks = std::max(1, std::min((int)((Rmax + 7) / 8), sms * 8));
-    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, R_static, w.dyn_count,
-                                          p.dyn_cap, n, (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.err);
+    const int gblocks = std::max(1, std::min((int)((Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS)), sms * 8));
+    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, w.seg_ord, w.nseg, n,
+                                          (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.err);
     ++launches;
   }
   // a3: bucket bases + pass plan
