@@ -397,7 +397,56 @@ struct SweepArgs {
 // In-warp stable ranking modes (RANK template parameter of k_onesweep).
 enum : int { RANK_BALLOT = 0, RANK_MATCH = 1, RANK_ATOMIC = 2 };
 
-template <typename KeyT, int RADIX_BITS, int IPT, int RANK>
+// Stable rank of each of a warp's IPT x 32 items among the warp's items of the same digit
+// (items in input order), accumulated in the warp's private u16 counters wcnt[w][*].
+// rd[i] = rank | digit << 16.  FULL: every item is valid (all tiles but the last).
+template <typename KeyT, int RADIX_BITS, int IPT, int RANK, bool FULL>
+__device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd)[IPT], int shift,
+                                           uint16_t* __restrict__ wrow, uint32_t wofs, uint32_t lane,
+                                           uint32_t tile_count) {
+  constexpr int RADIX = 1 << RADIX_BITS;
+#pragma unroll
+  for (int i = 0; i < IPT; ++i) {
+    const bool valid = FULL || (wofs + i * 32 + lane < tile_count);
+    const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
+    if constexpr (RANK == RANK_ATOMIC) {
+      // One shared atomic per item on the warp's private counters (two u16 per word).
+      // Conflicting lanes of one ATOMS are served in ascending lane order on sm_100a --
+      // measured, not documented: checked at load time by k_selftest_atomic_order
+      // (pbit.cu), which falls back to RANK_BALLOT if it ever fails.  A warp whose items
+      // share one digit (equal-key runs) lets lane 0 add 32 instead of serialising.
+      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+      const bool uni = __all_sync(0xffffffffu, d == d0 && valid);
+      const uint32_t sh = (d & 1u) << 4;
+      const uint32_t add = uni ? (lane == 0 ? 32u : 0u) : (valid ? 1u : 0u);
+      uint32_t old = 0;
+      uint32_t* wc = reinterpret_cast<uint32_t*>(wrow) + (d >> 1);
+      if (add) old = atomicAdd(wc, add << sh);
+      uint32_t r = (old >> sh) & 0xFFFFu;
+      const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0);
+      r = uni ? r0 + lane : r;
+      rd[i] = r | (d << 16);
+    } else {
+      const uint32_t vmask = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
+      uint32_t peers;
+      if constexpr (RANK == RANK_MATCH) peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu) & vmask;
+      else peers = warp_peers<RADIX_BITS>(d, vmask);
+      const int leader = 31 - __clz(peers | 1u);
+      uint32_t before = 0;
+      if (valid && lane == (uint32_t)leader) {
+        before = wrow[d];
+        wrow[d] = (uint16_t)(before + __popc(peers));
+      }
+      before = __shfl_sync(0xffffffffu, before, leader);
+      rd[i] = (before + __popc(peers & lanemask_lt())) | (d << 16);
+    }
+  }
+}
+
+// KIND of a k_onesweep launch (compile-time, so key passes carry no relink code).
+enum : int { SWEEP_KEY = 0, SWEEP_SUCC = 1, SWEEP_PAIR = 2 };
+
+template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int KIND>
 __global__ void __launch_bounds__(SWEEP_THREADS, 2)
 k_onesweep(const __grid_constant__ SweepArgs a) {
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
@@ -414,7 +463,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   int shift, src;
   bool last = false;
   const uint32_t* __restrict__ bases;
-  if (a.kind == 0) {
+  if constexpr (KIND == SWEEP_KEY) {
     const uint32_t npasses = a.plan->npasses;
     if ((uint32_t)slot >= npasses) return;
     const int digit_idx = a.plan->digit[slot];
@@ -424,18 +473,17 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     bases = a.bases + digit_idx * RADIX;
   } else {
     shift = a.bit0;
-    src = a.kind == 1 ? (int)(a.plan->npasses & 1u) : a.par;
+    src = KIND == SWEEP_SUCC ? (int)(a.plan->npasses & 1u) : a.par;
     bases = a.bases;
   }
-  const bool succ_mode = a.kind == 1;
   const KeyT* __restrict__ kin = reinterpret_cast<const KeyT*>(a.kin[src]);
   const uint32_t* __restrict__ iin = a.vin[src];
-  const int dst = a.kind == 1 ? 0 : (src ^ 1);
+  const int dst = KIND == SWEEP_SUCC ? 0 : (src ^ 1);
   KeyT* __restrict__ kout = reinterpret_cast<KeyT*>(a.kout[dst]);
   uint32_t* __restrict__ iout = a.vout[dst];
   const unsigned long long epoch = (unsigned long long)(slot + 1);
   unsigned long long* status = a.status;
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
 
   if (t == 0) {
     sm.tile = atomicAdd(a.tile_ctr + slot, 1u);
@@ -447,19 +495,18 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   const uint32_t tile = sm.tile;
   const uint32_t tile_base = tile * (uint32_t)TILE;
   const uint32_t tile_count = min((uint32_t)TILE, n - tile_base);
+  const bool full_tile = tile_count == (uint32_t)TILE;
 
-  // ---- 1. TMA bulk loads (sizes rounded up to 16 B; buffers are padded to 256 B)
-  uint32_t extra = PBIT_NULL32;  // succ_mode: the key just after the tile
+  // ---- TMA bulk loads of the tile (sizes rounded up to 16 B; buffers padded to 256 B)
   if (t == 0) {
     const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
-    const uint32_t ib = succ_mode ? 0u : (tile_count * 4u + 15u) & ~15u;
+    const uint32_t ib = KIND == SWEEP_SUCC ? 0u : (tile_count * 4u + 15u) & ~15u;
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(kb + ib) : "memory");
     bulk_g2s(sm.k, kin + tile_base, kb, &sm.mbar);
-    if (!succ_mode) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
-    else if (tile_base + tile_count < n) extra = (uint32_t)kin[tile_base + tile_count];
+    if constexpr (KIND != SWEEP_SUCC) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
   }
-  for (int i = t; i < SWEEP_WARPS * RADIX / 2; i += SWEEP_THREADS) reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
+  for (uint32_t i = t; i < SWEEP_WARPS * RADIX / 2; i += SWEEP_THREADS) reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
   {
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     uint32_t done = 0;
@@ -470,64 +517,27 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   }
   __syncthreads();
 
-  // ---- 2. stable in-warp ranking
-  const bool full_tile = tile_count == (uint32_t)TILE;
-  KeyT key[IPT];
-  uint32_t rd[IPT];  // rank within (warp, digit) | digit << 16
+  // ---- stable in-warp ranking
   const uint32_t wofs = w * WARP_ITEMS;
+  KeyT key[IPT];
+  uint32_t rd[IPT];
 #pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t j = wofs + i * 32 + lane;
-    const bool valid = j < tile_count;
-    key[i] = sm.k[j];
-    if (succ_mode && valid) {  // the value of item j is the key of item j+1
-      uint32_t sv;
-      if (j + 1 < tile_count) sv = (uint32_t)sm.k[j + 1];
-      else sv = (tile_base + tile_count < n) ? (uint32_t)kin[tile_base + tile_count] : PBIT_NULL32;
-      sm.iin[j] = sv;
-    }
-    const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
-    if constexpr (RANK == RANK_ATOMIC) {
-      // One shared atomic per item on the warp's private counters (two u16 counters per
-      // word).  Conflicting lanes of one ATOMS are served in ascending lane order on
-      // sm_100a -- measured, not documented: checked at load time by k_selftest_atomic_order
-      // (pbit.cu), which falls back to RANK_BALLOT if it ever fails.
-      // A warp whose items all share one digit (long equal-key runs: Zipf heavy hitters,
-      // presorted data) would serialise 32 lanes on one counter: one add of 32 instead.
-      uint32_t* wc = reinterpret_cast<uint32_t*>(&sm.wcnt[w][0]);
-      const uint32_t sh = (d & 1u) << 4;
-      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
-      uint32_t before;
-      if (__all_sync(0xffffffffu, d == d0 && valid)) {
-        uint32_t b0 = 0;
-        if (lane == 0) b0 = (atomicAdd(wc + (d >> 1), 32u << sh) >> sh) & 0xFFFFu;
-        before = __shfl_sync(0xffffffffu, b0, 0) + lane;
-      } else {
-        before = valid ? (atomicAdd(wc + (d >> 1), 1u << sh) >> sh) & 0xFFFFu : 0u;
-      }
-      rd[i] = before | (d << 16);
-    } else {
-      const uint32_t vmask = full_tile ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
-      uint32_t peers;
-      if constexpr (RANK == RANK_MATCH) {
-        peers = __match_any_sync(0xffffffffu, valid ? d : 0xFFFFFFFFu) & vmask;
-      } else {
-        peers = warp_peers<RADIX_BITS>(d, vmask);
-      }
-      const int leader = 31 - __clz(peers | 1u);
-      uint32_t before = 0;
-      if (valid && lane == leader) {
-        before = sm.wcnt[w][d];
-        sm.wcnt[w][d] = (uint16_t)(before + __popc(peers));
-      }
-      before = __shfl_sync(0xffffffffu, before, leader);
-      rd[i] = (before + __popc(peers & lanemask_lt())) | (d << 16);
+  for (int i = 0; i < IPT; ++i) key[i] = sm.k[wofs + i * 32 + lane];
+  if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
+  else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
+  if constexpr (KIND == SWEEP_SUCC) {
+    // the value of item j is its successor in the sorted order: the key of item j+1
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const uint32_t j = wofs + i * 32 + lane;
+      if (j < tile_count)
+        sm.iin[j] = j + 1 < tile_count ? (uint32_t)sm.k[j + 1]
+                    : (tile_base + tile_count < n ? (uint32_t)kin[tile_base + tile_count] : PBIT_NULL32);
     }
   }
-  (void)extra;
   __syncthreads();
 
-  // ---- 3. per digit: exclusive over warps, tile total, publish aggregate, scan over digits
+  // ---- per digit (thread t = digit t): exclusive over warps, tile total, aggregate
   uint32_t total = 0;
   if (t < RADIX) {
 #pragma unroll
@@ -543,13 +553,13 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-      if (lane >= o) x += y;
+      if (lane >= (uint32_t)o) x += y;
     }
     if (lane == 31) sm.scan[w] = x;
     __syncthreads();
     uint32_t add = 0;
 #pragma unroll
-    for (int ww = 0; ww < SWEEP_WARPS; ++ww) add += (ww < w) ? sm.scan[ww] : 0u;
+    for (int ww = 0; ww < SWEEP_WARPS; ++ww) add += (ww < (int)w) ? sm.scan[ww] : 0u;
     if (t < RADIX) {
       const uint32_t ds = x - total + add;
       sm.dstart[t] = ds;
@@ -559,30 +569,25 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   }
   __syncthreads();
 
-  // ---- 4. stage in (digit, input order) order (sm.k is free: every warp finished
-  // reading it before the barrier that ended the ranking).  wcnt[w][d] now holds the
-  // tile position of warp w's first item of digit d.
-  uint32_t idv[IPT];
-#pragma unroll
-  for (int i = 0; i < IPT; ++i) idv[i] = sm.iin[wofs + i * 32 + lane];
+  // ---- stage in (digit, input order) order: keys from registers into sm.k (every warp
+  // read its keys before the barriers above), values from sm.iin into sm.iout
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const uint32_t j = wofs + i * 32 + lane;
-    if (j < tile_count) {
+    if (full_tile || j < tile_count) {
       const uint32_t d = rd[i] >> 16;
       const uint32_t lp = sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
-      sm.iout[lp] = idv[i];
-      sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass only needs the digit
+      sm.iout[lp] = sm.iin[j];
+      sm.k[lp] = (KIND == SWEEP_KEY && last) ? (KeyT)d : key[i];  // the last key pass needs only digits
     }
   }
 
-  // ---- 5. decoupled lookback, one thread per digit value, LB_WIN predecessors per step
-  // (independent loads: one L2 round trip per window instead of per predecessor)
+  // ---- decoupled lookback, one thread per digit value, LB_WIN predecessors per step
   if (t < RADIX) {
-    constexpr int LB_WIN = 8;
+    constexpr int LB_WIN = 4;
     unsigned long long excl = 0;
     if (tile == 0 || a.debug_no_lookback) {
-      st_relaxed_u64(status + t, (epoch << 34) | (2ull << 32) | total);
+      st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (2ull << 32) | total);
     } else {
       int64_t hi = (int64_t)tile - 1;  // nearest predecessor not yet accounted for
       for (;;) {
@@ -607,8 +612,9 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   }
   __syncthreads();
 
-  // ---- 6. coalesced write-out
-  if (!last) {
+  // ---- coalesced write-out: consecutive threads store consecutive staged elements,
+  // which land contiguously inside each digit run
+  if (KIND != SWEEP_KEY || !last) {
 #pragma unroll 4
     for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
       const KeyT k = sm.k[j];

@@ -122,23 +122,24 @@ static void init_rank_mode(cudaStream_t st) {
 }
 
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
-template <typename KeyT, int RB, int IPT, int RANK>
+template <typename KeyT, int RB, int IPT, int RANK, int KIND>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
   static bool attr = false;  // benign race: idempotent
   if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(S));
+    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(S));
     attr = true;
   }
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  k_onesweep<KeyT, RB, IPT, RANK><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+  k_onesweep<KeyT, RB, IPT, RANK, KIND><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
 }
 
-template <typename KeyT, int RB, int IPT>
+template <typename KeyT, int RB, int IPT, int KIND>
 static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
-  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC>(a, st);
-  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH>(a, st);
-  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT>(a, st);
+  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, KIND>(a, st);
+  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, KIND>(a, st);
+  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, KIND>(a, st);
 }
 
 template <int KB, int RB>
@@ -147,7 +148,7 @@ static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* 
   constexpr int IPT = (KB == 8) ? 12 : 16;
   for (int s = 0; s < D; ++s) {
     a.slot = s;
-    launch_one<KeyT, RB, IPT>(a, st, rank_mode());
+    launch_one<KeyT, RB, IPT, SWEEP_KEY>(a, st, rank_mode());
     if (ev) cudaEventRecord(ev[ev_base + s], st);
   }
 }
@@ -343,7 +344,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
         ra.kout[0] = w.rk[0]; ra.kout[1] = w.rk[1]; ra.vout[0] = w.rv[0]; ra.vout[1] = w.rv[1];
       }
       // LSD over two digits: the relink passes must be stable too
-      launch_one<uint32_t, 8, 16>(ra, st, rank_mode());
+      if (q == 0) launch_one<uint32_t, 8, 16, SWEEP_SUCC>(ra, st, rank_mode());
+      else launch_one<uint32_t, 8, 16, SWEEP_PAIR>(ra, st, rank_mode());
       fin_k = w.rk[q & 1]; fin_v = w.rv[q & 1];
       launches += 2;
     }
