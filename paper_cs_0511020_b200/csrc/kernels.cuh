@@ -196,8 +196,9 @@ __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint3
                               const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
                               uint32_t nsub, uint32_t head_sub, const unsigned long long* __restrict__ sdist,
                               const uint32_t* __restrict__ scnt, uint32_t* __restrict__ dist,
-                              uint32_t* __restrict__ seg_ord, uint32_t* __restrict__ nseg_out,
-                              const int* __restrict__ err) {
+                              uint32_t* __restrict__ seg_ord, uint32_t* __restrict__ seg_pos,
+                              uint32_t* __restrict__ tile_first, uint32_t tile, uint32_t n,
+                              uint32_t* __restrict__ nseg_out, const int* __restrict__ err) {
   if (*err) return;
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
   const uint32_t total = scnt[head_sub];  // segments on the chain (= R for a valid list)
@@ -210,8 +211,13 @@ __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint3
     uint32_t r = rq;
     for (;;) {
       dist[r] = D;
-      seg_ord[k++] = r;
       const uint2 x = seg[r];
+      const uint32_t pos = n - D;  // list position of the segment's first node
+      seg_pos[k] = pos;
+      // segments are shorter than a pass tile, so each holds at most one tile start
+      const uint32_t tb = (pos + tile - 1) / tile;
+      if (tb * tile < pos + x.x) tile_first[tb] = k;
+      seg_ord[k++] = r;
       D -= x.x;
       if (x.y == PBIT_NULL32 || sub.is_ruler(x.y)) break;
       r = x.y;
@@ -230,9 +236,10 @@ k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
          const uint2* __restrict__ seg, const uint32_t* __restrict__ dist,
          const uint32_t* __restrict__ seg_ord, const uint32_t* __restrict__ nseg, uint32_t n,
          typename KeyOf<KB>::T* __restrict__ keys_lo, uint32_t* __restrict__ ids_lo,
-         const int* __restrict__ err) {
+         const Plan* __restrict__ plan, const int* __restrict__ err) {
   using RT = typename Rec<KB>::T;
   if (*err) return;
+  if (plan->npasses != 0) return;  // the first pass gathers the segments itself
   const uint32_t R = *nseg;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -392,6 +399,14 @@ struct SweepArgs {
   int kind;
   int bit0;  // kind 1/2: digit = (key >> bit0) & (RADIX - 1)
   int par;   // kind 2: input buffer index
+  // first key pass (GATHER): the tile is read from the walk's segment slots, in list order
+  const void* slots;
+  uint32_t cap;
+  const uint2* seg;               // {len, succ} per segment
+  const uint32_t* seg_ord;        // k-th segment of the list
+  const uint32_t* seg_pos;        // list position of the k-th segment's first node
+  const uint32_t* tile_first;     // ordinal of the segment holding each tile's first position
+  const uint32_t* nseg;
 };
 
 // In-warp stable ranking modes (RANK template parameter of k_onesweep).
@@ -446,7 +461,58 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
 // KIND of a k_onesweep launch (compile-time, so key passes carry no relink code).
 enum : int { SWEEP_KEY = 0, SWEEP_SUCC = 1, SWEEP_PAIR = 2 };
 
-template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int KIND>
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
+               "l"(gsrc) : "memory");
+}
+
+// Fill the tile [P, P + count) of the list order straight from the walk's segment slots
+// (replaces a separate gather pass over n x 16 B).  Each warp fetches the metadata of 32
+// consecutive segments at once (one lane each), then copies the overlapping part of each
+// with cp.async (no registers, all copies in flight together).
+template <typename KeyT, int TILE>
+__device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, uint32_t P, uint32_t count,
+                                            KeyT* sk, uint32_t* sv, uint32_t w, uint32_t lane) {
+  constexpr bool WIDE = sizeof(KeyT) == 8;
+  const uint32_t E = P + count;
+  const uint32_t nseg = *a.nseg;
+  for (uint32_t kb = a.tile_first[tile] + w * 32;; kb += SWEEP_WARPS * 32) {
+    const uint32_t k = kb + lane;
+    uint32_t pos = E, r = 0, len = 0;
+    if (k < nseg) {
+      pos = a.seg_pos[k];
+      if (pos < E) { r = a.seg_ord[k]; len = a.seg[r].x; }
+    }
+    uint32_t todo = __ballot_sync(0xffffffffu, pos < E);
+    if (!todo) break;
+    while (todo) {
+      const int q = __ffs(todo) - 1;
+      todo &= todo - 1;
+      const uint32_t sp = __shfl_sync(0xffffffffu, pos, q);
+      const uint32_t sr = __shfl_sync(0xffffffffu, r, q);
+      const uint32_t sl = __shfl_sync(0xffffffffu, len, q);
+      const uint32_t lo = max(P, sp), hi = min(E, sp + sl);
+      for (uint32_t x = lo + lane; x < hi; x += 32) {
+        if constexpr (WIDE) {
+          const uint4* rec = reinterpret_cast<const uint4*>(a.slots) + (size_t)sr * a.cap + (x - sp);
+          cp_async8(sk + (x - P), &rec->x);
+          cp_async4(sv + (x - P), &rec->z);
+        } else {
+          const uint2* rec = reinterpret_cast<const uint2*>(a.slots) + (size_t)sr * a.cap + (x - sp);
+          cp_async4(sk + (x - P), &rec->x);
+          cp_async4(sv + (x - P), &rec->y);
+        }
+      }
+    }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int KIND, bool GATHER = false>
 __global__ void __launch_bounds__(SWEEP_THREADS, 2)
 k_onesweep(const __grid_constant__ SweepArgs a) {
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
@@ -497,8 +563,10 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   const uint32_t tile_count = min((uint32_t)TILE, n - tile_base);
   const bool full_tile = tile_count == (uint32_t)TILE;
 
-  // ---- TMA bulk loads of the tile (sizes rounded up to 16 B; buffers padded to 256 B)
-  if (t == 0) {
+  // ---- TMA bulk loads of the tile (sizes rounded up to 16 B; buffers padded to 256 B);
+  // the first key pass gathers the tile from the segment slots instead
+  if (GATHER) gather_tile<KeyT, TILE>(a, tile, tile_base, tile_count, sm.k, sm.iin, w, lane);
+  if (!GATHER && t == 0) {
     const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
     const uint32_t ib = KIND == SWEEP_SUCC ? 0u : (tile_count * 4u + 15u) & ~15u;
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
@@ -507,7 +575,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     if constexpr (KIND != SWEEP_SUCC) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
   }
   for (uint32_t i = t; i < SWEEP_WARPS * RADIX / 2; i += SWEEP_THREADS) reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
-  {
+  if (!GATHER) {
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     uint32_t done = 0;
     while (!done) {

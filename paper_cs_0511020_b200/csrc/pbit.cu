@@ -122,24 +122,24 @@ static void init_rank_mode(cudaStream_t st) {
 }
 
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
-template <typename KeyT, int RB, int IPT, int RANK, int KIND>
+template <typename KeyT, int RB, int IPT, int RANK, int KIND, bool GATHER>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
   static bool attr = false;  // benign race: idempotent
   if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, KIND, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(S));
     attr = true;
   }
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  k_onesweep<KeyT, RB, IPT, RANK, KIND><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+  k_onesweep<KeyT, RB, IPT, RANK, KIND, GATHER><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
 }
 
-template <typename KeyT, int RB, int IPT, int KIND>
+template <typename KeyT, int RB, int IPT, int KIND, bool GATHER = false>
 static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
-  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, KIND>(a, st);
-  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, KIND>(a, st);
-  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, KIND>(a, st);
+  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, KIND, GATHER>(a, st);
+  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, KIND, GATHER>(a, st);
+  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, KIND, GATHER>(a, st);
 }
 
 template <int KB, int RB>
@@ -148,7 +148,8 @@ static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* 
   constexpr int IPT = (KB == 8) ? 12 : 16;
   for (int s = 0; s < D; ++s) {
     a.slot = s;
-    launch_one<KeyT, RB, IPT, SWEEP_KEY>(a, st, rank_mode());
+    if (s == 0) launch_one<KeyT, RB, IPT, SWEEP_KEY, true>(a, st, rank_mode());
+    else launch_one<KeyT, RB, IPT, SWEEP_KEY, false>(a, st, rank_mode());
     if (ev) cudaEventRecord(ev[ev_base + s], st);
   }
 }
@@ -167,7 +168,8 @@ size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64
 // Workspace layout (all 256-byte aligned).
 struct Ws {
   void* kn; void* slots; uint2* seg; uint32_t* dist;
-  unsigned long long* sdist[2]; uint32_t* scnt[2]; uint32_t* ssucc[2]; uint32_t* seg_ord;
+  unsigned long long* sdist[2]; uint32_t* scnt[2]; uint32_t* ssucc[2]; uint32_t* seg_ord; uint32_t* seg_pos;
+  uint32_t* tile_first;
   void* keys[2]; uint32_t* ids[2]; unsigned long long* status; uint32_t* rk[2]; uint32_t* rv[2];
   // control block (zeroed per call)
   uint32_t* hist; uint32_t* bases; Plan* plan; int* err; uint32_t* dyn_count; uint32_t* tile_ctr; uint32_t* d_head;
@@ -201,6 +203,8 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
     w->ssucc[i] = (uint32_t*)take(nsub * 4);
   }
   w->seg_ord = (uint32_t*)take(Rmax * 4);
+  w->seg_pos = (uint32_t*)take(Rmax * 4);
+  w->tile_first = (uint32_t*)take((ntiles + 1) * 4);
   for (int i = 0; i < 2; ++i) { w->keys[i] = take(n * kbytes); w->ids[i] = (uint32_t*)take(n * 4); }
   w->status_bytes = ntiles * (radix > 256 ? radix : 256) * 8;  // relink passes use 256
   w->status = (unsigned long long*)take(w->status_bytes);
@@ -292,18 +296,21 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     }
     k_rank_check<<<1, 1, 0, st>>>(w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
     k_rank_walk_b<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
-                                           head_sub, w.sdist[cur], w.scnt[cur], w.dist, w.seg_ord, w.nseg, w.err);
+                                           head_sub, w.sdist[cur], w.scnt[cur], w.dist, w.seg_ord, w.seg_pos,
+                                           w.tile_first, (uint32_t)sweep_tile(p.key_bits), n, w.nseg, w.err);
     launches += rounds + 3;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
-    // a1: gather to list order
-    const int gblocks = std::max(1, std::min((int)((Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS)), sms * 8));
-    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, w.seg_ord, w.nseg, n,
-                                          (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.err);
-    ++launches;
   }
-  // a3: bucket bases + pass plan
+  // a3: bucket bases + pass plan (before the gather, which runs only if no pass does)
   k_plan<<<1, 256, 0, st>>>(w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
   ++launches;
+  {  // a1: gather to list order -- only when every digit is trivial (no pass to fuse it into)
+    const uint32_t Rmax = R_static + p.dyn_cap;
+    const int gblocks = std::max(1, std::min((int)((Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS)), sms * 8));
+    k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, w.seg_ord, w.nseg, n,
+                                          (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.plan, w.err);
+    ++launches;
+  }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_GATHER], st);
 
   // a3/a4: passes
@@ -312,6 +319,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   sa.kout[0] = w.keys[0]; sa.kout[1] = w.keys[1]; sa.vout[0] = w.ids[0]; sa.vout[1] = w.ids[1];
   sa.bases = w.bases; sa.status = w.status; sa.tile_ctr = w.tile_ctr; sa.plan = w.plan; sa.err = w.err; sa.n = n;
   sa.kind = 0;
+  sa.slots = w.slots; sa.cap = p.cap; sa.seg = w.seg; sa.seg_ord = w.seg_ord; sa.seg_pos = w.seg_pos;
+  sa.tile_first = w.tile_first; sa.nseg = w.nseg;
   { const char* e = getenv("PBIT_DEBUG_NO_LOOKBACK"); sa.debug_no_lookback = e ? atoi(e) : 0; }
   launch_key_passes_k<KB>(p.K, sa, p.D, st, timing ? ev : nullptr, PBIT_PHASE_PASS0);
   launches += p.D;
