@@ -472,16 +472,17 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
 
 // Fill the tile [P, P + count) of the list order straight from the walk's segment slots
 // (replaces a separate gather pass over n x 16 B).  Each warp fetches the metadata of 32
-// consecutive segments at once (one lane each), then copies the overlapping part of each
-// with cp.async (no registers, all copies in flight together).
+// segments at once (one lane each), then copies the overlapping part of each with
+// cp.async (no registers, all copies in flight together).
 template <typename KeyT, int TILE>
 __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, uint32_t P, uint32_t count,
                                             KeyT* sk, uint32_t* sv, uint32_t w, uint32_t lane) {
   constexpr bool WIDE = sizeof(KeyT) == 8;
   const uint32_t E = P + count;
   const uint32_t nseg = *a.nseg;
-  for (uint32_t kb = a.tile_first[tile] + w * 32;; kb += SWEEP_WARPS * 32) {
-    const uint32_t k = kb + lane;
+  // warp w takes segments first + w + SWEEP_WARPS * i: all warps share the copying
+  for (uint32_t kb = a.tile_first[tile] + w;; kb += SWEEP_WARPS * 32) {
+    const uint32_t k = kb + lane * SWEEP_WARPS;
     uint32_t pos = E, r = 0, len = 0;
     if (k < nseg) {
       pos = a.seg_pos[k];
