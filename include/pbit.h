@@ -116,15 +116,17 @@ int pbit_sort_list(const void *keys, const uint32_t *next, uint32_t head, uint64
  *   next_local     [in]  device, their successors as GLOBAL ids (PBIT_NULL ends).
  *   head           [in]  global id of the first node, identical on every rank.
  *   n_global       [in]  total nodes over all ranks.
- *   node_lo,n_local[in]  this rank's contiguous slice; slices must be ordered by rank,
- *                        contiguous and equal-sized except the last
- *                        (node_lo = rank * ceil(n_global / G)); else PBIT_ERR_UNSUPPORTED.
+ *   node_lo,n_local[in]  this rank's slice of node ids: node_lo = rank * S and
+ *                        n_local = min(S, n_global - node_lo) with S = pbit_mg_slice(n_global,
+ *                        G) (ceil(n_global / G) rounded up to 64); else PBIT_ERR_UNSUPPORTED.
  *   key_bits       [in]  as above.
  *   out_head       [out] host: head of the sorted list (same on every rank).
  *   out_next_local [out] device, n_local global successor ids for this rank's nodes.
  *   nccl_comm      [in]  ncclComm_t (see pbit_mg_comm_init) spanning the G ranks.
  *   opts           [in]  as above (stream used for every kernel and collective).
  * Collective: every rank must call it with the same head, n_global, key_bits, K.
+ * Rank r returns the successors of its own nodes; the sorted positions it computed
+ * internally are [r*S, r*S + S) (top-digit sharding, position-exact).
  */
 int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32_t head,
                       uint64_t n_global, uint64_t node_lo, uint64_t n_local, int key_bits,
@@ -138,6 +140,20 @@ int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32
 int pbit_mg_get_unique_id(void *id_out /* PBIT_MG_UNIQUE_ID_BYTES host bytes */);
 int pbit_mg_comm_init(void **comm_out, int nranks, const void *id, int rank);
 int pbit_mg_comm_destroy(void *comm);
+
+/* Node ids per rank for pbit_sort_list_mg: ceil(n_global / nranks) rounded up to 64. */
+uint64_t pbit_mg_slice(uint64_t n_global, int nranks);
+
+/* Host-side plan of the key-range exchange inside pbit_sort_list_mg (no device work;
+ * exported for tests).  Each rank's chunk (sorted positions [q*slice, (q+1)*slice) of the
+ * list order) is sorted by (key, list position); splitter s sits at global rank
+ * min(n, (s+1)*slice) of the final order with key k*_s.  lt / le: nranks x (nranks-1)
+ * counts, lt[q*(nranks-1)+s] = keys of rank q below k*_s, le[...] = keys up to k*_s.
+ * Outputs (nranks each): the range of its sorted chunk rank `rank` sends to every rank,
+ * and where (offset, count) it receives each source's range, in source-rank order. */
+void pbit_mg_exchange_plan(int nranks, int rank, uint64_t n, uint64_t slice, const uint64_t *lt,
+                           const uint64_t *le, uint64_t *send_off, uint64_t *send_count,
+                           uint64_t *recv_off, uint64_t *recv_count);
 
 /* Text of the last CUDA or NCCL error seen by the calling host thread ("" if none). */
 const char *pbit_last_error(void);

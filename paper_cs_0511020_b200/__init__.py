@@ -21,7 +21,8 @@ PBIT_NULL = 0xFFFFFFFF
 NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
 SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
-           "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version", "pbit_last_error"]
+           "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version", "pbit_last_error",
+           "pbit_mg_slice", "pbit_mg_exchange_plan"]
 
 STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
           4: "PBIT_ERR_CUDA", 5: "PBIT_ERR_NCCL", 6: "PBIT_ERR_UNSUPPORTED"}
@@ -62,6 +63,12 @@ def _load():
     lib.pbit_status_string.argtypes = [ctypes.c_int]
     lib.pbit_version.restype = ctypes.c_uint32
     lib.pbit_last_error.restype = ctypes.c_char_p
+    lib.pbit_mg_slice.restype = ctypes.c_uint64
+    lib.pbit_mg_slice.argtypes = [ctypes.c_uint64, ctypes.c_int]
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    lib.pbit_mg_exchange_plan.restype = None
+    lib.pbit_mg_exchange_plan.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint64, u64p,
+                                          u64p, u64p, u64p, u64p, u64p]
     return lib
 
 
@@ -157,6 +164,27 @@ def mg_comm_init(nranks: int, uid: bytes, rank: int) -> int:
 
 def mg_comm_destroy(comm: int) -> None:
     lib.pbit_mg_comm_destroy(ctypes.c_void_p(comm))
+
+
+def mg_slice(n_global: int, nranks: int) -> int:
+    """Node ids per rank for sort_list_mg (ceil(n/G) rounded up to 64)."""
+    return int(lib.pbit_mg_slice(n_global, nranks))
+
+
+def mg_exchange_plan(nranks: int, rank: int, n: int, slice_: int, lt, le):
+    """The key-range exchange plan pbit_sort_list_mg computes on the host (see pbit.h):
+    returns (send_off, send_count, recv_off, recv_count) for `rank`."""
+    import numpy as np
+    a = np.ascontiguousarray(lt, dtype=np.uint64).reshape(-1)
+    b = np.ascontiguousarray(le, dtype=np.uint64).reshape(-1)
+    if a.size == 0:
+        a = np.zeros(1, np.uint64)
+        b = np.zeros(1, np.uint64)
+    outs = [np.zeros(nranks, np.uint64) for _ in range(4)]
+    u64p = ctypes.POINTER(ctypes.c_uint64)
+    lib.pbit_mg_exchange_plan(nranks, rank, n, slice_, a.ctypes.data_as(u64p), b.ctypes.data_as(u64p),
+                              *[o.ctypes.data_as(u64p) for o in outs])
+    return tuple(o.astype(np.int64) for o in outs)
 
 
 def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int, comm: int,

@@ -27,7 +27,7 @@ constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
 // every digit of every key into a per-CTA smem histogram (flushed once per CTA).
 template <int KB>
 __global__ void __launch_bounds__(PACK_THREADS)
-k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_t n,
+k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_t n, uint32_t n_ids,
        typename Rec<KB>::T* __restrict__ kn, uint32_t* __restrict__ hist, int K, int D,
        int* __restrict__ err) {
   extern __shared__ uint32_t s_hist[];
@@ -39,7 +39,7 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
   int bad = 0;
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
     uint32_t nx = __ldcs(next + v);
-    bad |= (nx != PBIT_NULL32) & (nx >= n);
+    bad |= (nx != PBIT_NULL32) & (nx >= n_ids);
     if constexpr (KB == 8) {
       unsigned long long k = __ldcs(reinterpret_cast<const unsigned long long*>(keys) + v);
       kn[v] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), nx, 0u);
@@ -139,7 +139,7 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
 // sub-ruler list is ranked by pointer jumping (Wyllie), and walk B hands every ruler its
 // distance to the end of the list: dist[r] = nodes from the first node of segment r to
 // the end.  Segment r then occupies list positions [n - dist[r], n - dist[r] + len[r]).
-__global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
+static __global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
                               const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
                               uint32_t nsub, unsigned long long* __restrict__ sdist, uint32_t* __restrict__ scnt,
                               uint32_t* __restrict__ ssucc, int* __restrict__ err) {
@@ -147,7 +147,7 @@ __global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint3
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
     const uint32_t rq = q < sub.R ? sub.node_of(q) : head_ruler;
-    if (rq >= R) { sdist[q] = 0; scnt[q] = 0; ssucc[q] = PBIT_NULL32; continue; }
+    if (rq >= R || seg[rq].x == 0) { sdist[q] = 0; scnt[q] = 0; ssucc[q] = PBIT_NULL32; continue; }  // unused entry
     unsigned long long acc = 0;
     uint32_t r = rq, steps = 0, succ = PBIT_NULL32;
     for (;;) {
@@ -164,7 +164,7 @@ __global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub, uint3
   }
 }
 
-__global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const uint32_t* __restrict__ c_in,
+static __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const uint32_t* __restrict__ c_in,
                             const uint32_t* __restrict__ s_in, unsigned long long* __restrict__ d_out,
                             uint32_t* __restrict__ c_out, uint32_t* __restrict__ s_out, uint32_t m,
                             const int* __restrict__ err) {
@@ -183,7 +183,7 @@ __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, const u
 
 // Validation (reading Q10): the chain from the head must end (succ NULL) and hold exactly
 // n nodes; then every node lies on it.
-__global__ void k_rank_check(const unsigned long long* __restrict__ dist, const uint32_t* __restrict__ succ,
+static __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const uint32_t* __restrict__ succ,
                              uint32_t head_sub, uint32_t n, int* __restrict__ err) {
   if (*err) return;
   if (succ[head_sub] != PBIT_NULL32 || dist[head_sub] != (unsigned long long)n) atomicOr(err, E_CHAIN);
@@ -192,7 +192,7 @@ __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const 
 // Walk B also numbers the segments in list order: seg_ord[k] = the k-th segment of the
 // list, so later kernels visit segments in list order (adjacent output runs are then
 // written close together in time and their shared boundary sectors merge in L2).
-__global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
+static __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint32_t R_static,
                               const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
                               uint32_t nsub, uint32_t head_sub, const unsigned long long* __restrict__ sdist,
                               const uint32_t* __restrict__ scnt, uint32_t* __restrict__ dist,
@@ -205,7 +205,7 @@ __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub, uint3
   if (blockIdx.x == 0 && threadIdx.x == 0) *nseg_out = total;
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
     const uint32_t rq = q < sub.R ? sub.node_of(q) : head_ruler;
-    if (rq >= R) continue;
+    if (rq >= R || seg[rq].x == 0) continue;
     uint32_t D = (uint32_t)sdist[q];
     uint32_t k = total - scnt[q];
     uint32_t r = rq;
@@ -280,7 +280,7 @@ k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
 // ============================================================================ a3: plan
 // Exclusive scan of each digit's histogram (bucket bases, ascending = the ascending
 // end-marker order of P:379-380) and the list of non-trivial digits.  One CTA.
-__global__ void __launch_bounds__(256)
+static __global__ void __launch_bounds__(256)
 k_plan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases, Plan* __restrict__ plan,
        int D, int K, uint32_t n, const int* __restrict__ err) {
   __shared__ uint32_t s_warp[8];
@@ -354,7 +354,7 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
 // Load-time check of the lane order of conflicting shared-memory atomics (RANK_ATOMIC).
 // Every lane adds 1 to a warp-private counter chosen by a hashed digit; the result must
 // equal (value before the instruction) + (number of lower lanes with the same digit).
-__global__ void k_selftest_atomic_order(uint32_t iters, uint32_t* bad) {
+static __global__ void k_selftest_atomic_order(uint32_t iters, uint32_t* bad) {
   __shared__ uint32_t cnt[SWEEP_WARPS][128];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int i = threadIdx.x; i < SWEEP_WARPS * 128; i += blockDim.x) (&cnt[0][0])[i] = 0;
@@ -399,6 +399,7 @@ struct SweepArgs {
   int kind;
   int bit0;  // kind 1/2: digit = (key >> bit0) & (RADIX - 1)
   int par;   // kind 2: input buffer index
+  int keep_keys;  // key pass: write keys even in the plan's last pass (mg partition pass)
   // first key pass (GATHER): the tile is read from the walk's segment slots, in list order
   const void* slots;
   uint32_t cap;
@@ -535,7 +536,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     if ((uint32_t)slot >= npasses) return;
     const int digit_idx = a.plan->digit[slot];
     shift = digit_idx * RADIX_BITS;
-    last = (uint32_t)slot + 1 == npasses;
+    last = (uint32_t)slot + 1 == npasses && !a.keep_keys;
     src = slot & 1;
     bases = a.bases + digit_idx * RADIX;
   } else {
@@ -714,7 +715,7 @@ constexpr int RELINK_FINE_SHIFT = 14;  // 16384 ids = 64 KB smem window
 // The pairs are sorted by v's bits [RELINK_FINE_SHIFT, log2 n) with k_onesweep (kind
 // 1 then 2; LSD, 8-bit digits).  Bucket bases need no histogram: the ids are a
 // permutation of [0, n), so the count of each digit value is known in closed form.
-__global__ void k_relink_bases(uint32_t n, int bit0, uint32_t* __restrict__ bases) {
+static __global__ void k_relink_bases(uint32_t n, int bit0, uint32_t* __restrict__ bases) {
   __shared__ uint32_t s_warp[8];
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;  // 256 threads = 256 digit values
   const unsigned long long B = 1ull << bit0, P = B << 8;
@@ -734,7 +735,7 @@ __global__ void k_relink_bases(uint32_t n, int bit0, uint32_t* __restrict__ base
   bases[t] = x - c + add;
 }
 
-__global__ void k_relink_head(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
+static __global__ void k_relink_head(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
                               const uint32_t* __restrict__ ids1, uint32_t* __restrict__ d_head,
                               const int* __restrict__ err) {
   if (*err) return;
@@ -742,7 +743,7 @@ __global__ void k_relink_head(const Plan* __restrict__ plan, const uint32_t* __r
 }
 
 // Level 3: one CTA per fine bin: scatter into a 64 KB smem window, write it coalesced.
-__global__ void __launch_bounds__(512)
+static __global__ void __launch_bounds__(512)
 k_relink_apply(const uint32_t* __restrict__ pv, const uint32_t* __restrict__ ps, uint32_t n,
                uint32_t* __restrict__ out_next, const int* __restrict__ err) {
   extern __shared__ __align__(16) uint32_t s_win[];
@@ -761,7 +762,7 @@ k_relink_apply(const uint32_t* __restrict__ pv, const uint32_t* __restrict__ ps,
 }
 
 // n <= 2^14: the whole out_next is one window.
-__global__ void __launch_bounds__(512)
+static __global__ void __launch_bounds__(512)
 k_relink_small(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, const uint32_t* __restrict__ ids1,
                uint32_t n, uint32_t* __restrict__ out_next, const int* __restrict__ err) {
   extern __shared__ __align__(16) uint32_t s_win[];

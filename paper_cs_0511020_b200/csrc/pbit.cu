@@ -19,6 +19,7 @@
 #include "../../include/pbit.h"
 #include "kernels.cuh"
 #include "pbit_internal.h"
+#include "launch.cuh"
 
 namespace pbit {
 
@@ -98,9 +99,9 @@ static constexpr int SUB_LOG2 = 4;  // one sub-ruler per 16 rulers
 // self-test fails (or PBIT_RANK=ballot|match|atomic overrides, for experiments).
 static std::atomic<int> g_rank_mode{-1};
 
-static int rank_mode() { return g_rank_mode.load(std::memory_order_relaxed); }
+int rank_mode() { return g_rank_mode.load(std::memory_order_relaxed); }
 
-static void init_rank_mode(cudaStream_t st) {
+void init_rank_mode(cudaStream_t st) {
   if (g_rank_mode.load() >= 0) return;
   int mode = RANK_ATOMIC;
   if (const char* e = getenv("PBIT_RANK")) {
@@ -119,48 +120,6 @@ static void init_rank_mode(cudaStream_t st) {
     if (bad) mode = RANK_BALLOT;
   }
   g_rank_mode.store(mode);
-}
-
-// One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
-template <typename KeyT, int RB, int IPT, int RANK, int KIND, bool GATHER>
-static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
-  using S = SweepSmem<KeyT, RB, IPT>;
-  static bool attr = false;  // benign race: idempotent
-  if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, KIND, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(S));
-    attr = true;
-  }
-  const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  k_onesweep<KeyT, RB, IPT, RANK, KIND, GATHER><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
-}
-
-template <typename KeyT, int RB, int IPT, int KIND, bool GATHER = false>
-static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
-  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, KIND, GATHER>(a, st);
-  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, KIND, GATHER>(a, st);
-  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, KIND, GATHER>(a, st);
-}
-
-template <int KB, int RB>
-static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
-  using KeyT = typename KeyOf<KB>::T;
-  constexpr int IPT = (KB == 8) ? 12 : 16;
-  for (int s = 0; s < D; ++s) {
-    a.slot = s;
-    if (s == 0) launch_one<KeyT, RB, IPT, SWEEP_KEY, true>(a, st, rank_mode());
-    else launch_one<KeyT, RB, IPT, SWEEP_KEY, false>(a, st, rank_mode());
-    if (ev) cudaEventRecord(ev[ev_base + s], st);
-  }
-}
-
-template <int KB>
-static void launch_key_passes_k(int K, const SweepArgs& a, int D, cudaStream_t st, cudaEvent_t* ev, int ev_base) {
-  switch (K) {
-#define PBIT_K(RB) case RB: launch_key_passes<KB, RB>(a, D, st, ev, ev_base); break;
-    PBIT_K(1) PBIT_K(2) PBIT_K(3) PBIT_K(4) PBIT_K(5) PBIT_K(6) PBIT_K(7) PBIT_K(8)
-#undef PBIT_K
-  }
 }
 
 size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64 ? 12 : 16); }
@@ -254,7 +213,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   {
     const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
     const size_t smem = (size_t)p.D * radix * 4;
-    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, (RT*)w.kn, w.hist, p.K, p.D, w.err);
+    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);

@@ -21,6 +21,8 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p);
 int device_info(int dev, int* sms);
 int pointer_kind(const void* ptr, int dev);
 size_t sweep_tile(int key_bits);
+int rank_mode();                      // RANK_ATOMIC / RANK_BALLOT / RANK_MATCH for k_onesweep
+void init_rank_mode(cudaStream_t st); // runs the atomic-order self-test once
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
                 uint32_t* out_head, uint32_t* out_next, cudaStream_t st, float* phase_ms, uint32_t* passes_run,
                 uint32_t* launches);

@@ -1,0 +1,75 @@
+"""pbit_sort_list_mg through the C-ABI on the one GPU available: a 1-rank NCCL
+communicator runs every step of the multi-GPU protocol (pack + all-gather, count walk,
+segment-table exchange, ranking, emit walk, top-digit partition + exchange, local sort,
+stitch, owner routing, relink), compared bit-exactly with the oracle.  The G > 1
+exchange logic is covered on CPU by tests/test_mg_protocol.py (gloo, world_size 2-3)."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mg(cuda_ok):
+    import paper_cs_0511020_b200 as p
+    uid = p.mg_unique_id()
+    comm = p.mg_comm_init(1, uid, 0)
+    yield p, comm
+    p.mg_comm_destroy(comm)
+
+
+CASES = [
+    (1, 32, "uniform", "random"), (2, 32, "uniform", "random"), (77, 8, "uniform", "push"),
+    (4097, 32, "zipf", "random"), (100003, 64, "runs4096", "random"), (65536, 8, "uniform", "random"),
+    (200001, 16, "uniform", "identity"), (300007, 32, "equal", "random"), (1 << 20, 32, "uniform", "random"),
+]
+
+
+@pytest.mark.parametrize("n,key_bits,keys,links", CASES)
+def test_mg_single_rank_vs_oracle(mg, n, key_bits, keys, links):
+    p, comm = mg
+    li = workloads.make_list(n, key_bits, seed=n + 31, keys=keys, links=links, device="cuda")
+    assert p.mg_slice(n, 1) >= n
+    h, out = p.sort_list_mg(li.keys, li.next, li.head, n, 0, comm, key_bits=key_bits)
+    torch.cuda.synchronize()
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4)
+    assert h == oh
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), on)
+
+
+@pytest.mark.parametrize("K", [4, 8])
+def test_mg_digit_widths(mg, K):
+    p, comm = mg
+    li = workloads.make_list(250001, 32, seed=5, keys="zipf", device="cuda")
+    h, out = p.sort_list_mg(li.keys, li.next, li.head, li.n, 0, comm, digit_bits=K)
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, 32, 4)
+    assert h == oh and np.array_equal(out.cpu().numpy().view(np.uint32), on)
+
+
+def test_mg_invalid_list(mg):
+    p, comm = mg
+    n = 10000
+    nx = torch.arange(1, n + 1, dtype=torch.int32)
+    nx[-1] = 0  # cycle through the head
+    keys = torch.arange(n, dtype=torch.int32)
+    out = torch.full((n,), 7, dtype=torch.int32, device="cuda")
+    with pytest.raises(p.PbitError) as e:
+        p.sort_list_mg(keys.cuda(), nx.cuda(), 0, n, 0, comm, out_next_local=out)
+    assert e.value.code == 2
+    assert bool((out == 7).all())
+
+
+def test_mg_bad_slice_rejected(mg):
+    p, comm = mg
+    k = torch.zeros(100, dtype=torch.int32, device="cuda")
+    nx = torch.arange(1, 101, dtype=torch.int32, device="cuda")
+    nx[-1] = -1
+    with pytest.raises(p.PbitError) as e:
+        p.sort_list_mg(k[:50], nx[:50], 0, 100, 0, comm)  # a 1-rank comm must own all 100 nodes
+    assert e.value.code == 6
