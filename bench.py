@@ -8,8 +8,9 @@ configured synthetic list, inputs resident in HBM.  Default workload: C3 (n = 2^
 u32 Zipf(1.1) keys, random-permutation links) -- the 1-GPU config the north star gates
 on.  Inputs (2 GiB) are larger than L2 (126 MB), so no explicit flush is needed.
 
-N > 1 (torchrun): every rank sorts its own C3-shaped list (independent problems, weak
-scaling); value = all ranks' nodes / max-over-ranks time.
+N > 1 (torchrun): ONE list of the config's size is sorted by all ranks together through
+pbit_sort_list_mg (node ids sharded by rank, key-range exchange over NCCL; strong
+scaling); value = n / max-over-ranks device time.
 
 --impl reference: the CPU oracle (the paper's algorithm, oracle/) timed on the host on
 bounded samples of the same workload (rank 0 only).
@@ -200,6 +201,84 @@ def load_traffic(cfg: str):
         return None
 
 
+def run_mg(args):
+    """N > 1: one list sorted by every rank together (pbit_sort_list_mg)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_cs_0511020_b200 as pbit
+    import workloads
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    obj = [pbit.mg_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    comm = pbit.mg_comm_init(ws, obj[0], rank)
+    c = workloads.CONFIGS[args.config]
+    K = args.digit_bits or c["digit_bits"]
+    n = c["n"] if args.n is None else args.n
+    li = workloads.make_config(args.config, device="cuda", n=n)
+    S = pbit.mg_slice(n, ws)
+    lo, hi = min(n, rank * S), min(n, rank * S + S)
+    keys, nxt, head, kb = li.keys[lo:hi].clone(), li.next[lo:hi].clone(), li.head, li.key_bits
+    del li
+    torch.cuda.empty_cache()
+    out = torch.empty_like(nxt)
+    st = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 3)):
+        pbit.sort_list_mg(keys, nxt, head, n, lo, comm, digit_bits=K, out_next_local=out)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(st)
+        for _ in range(args.steps):
+            pbit.sort_list_mg(keys, nxt, head, n, lo, comm, digit_bits=K, out_next_local=out)
+        e1.record(st)
+        torch.cuda.synchronize()
+    dist.barrier()
+    ms_t = torch.tensor([e0.elapsed_time(e1) / args.steps], device="cuda")
+    dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    # end to end: host slice in, host out_next slice back, every step
+    kh, nh = keys.cpu().pin_memory(), nxt.cpu().pin_memory()
+    oh = torch.empty_like(nh).pin_memory()
+    dist.barrier()
+    e_steps = max(1, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e_steps):
+        kd, nd = kh.to("cuda", non_blocking=True), nh.to("cuda", non_blocking=True)
+        pbit.sort_list_mg(kd, nd, head, n, lo, comm, digit_bits=K, out_next_local=out)
+        oh.copy_(out, non_blocking=True)
+        torch.cuda.synchronize()
+    e2e_t = torch.tensor([(time.perf_counter() - t0) / e_steps], device="cuda")
+    dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    cpu = cpu_baseline(args.config, min(n, args.cpu_sample)) if rank == 0 and not args.no_cpu_baseline else None
+    if rank == 0:
+        peak, peak_src = load_peaks()
+        mb = method_bytes_per_node(kb)
+        per_rank_gbs = mb * (n / ws) / (ms / 1e3) / 1e9
+        line = {"metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "u32" if kb <= 32 else "u64", "data": "synthetic",
+                "config": {"workload": args.config, "desc": c["desc"], "n": n, "key_bits": kb, "digit_bits": K,
+                           "parallelism": f"one list, node ids sharded over {ws} ranks, key-range exchange (NCCL)",
+                           "l2": "inputs larger than L2 (no flush needed)"},
+                "roofline": {"bound": "hbm", "achieved": round(per_rank_gbs, 1), "peak": peak, "unit": "GB/s",
+                             "frac": round(per_rank_gbs / peak, 4), "traffic": None,
+                             "kernel": "pbit_sort_list_mg (whole call, method bytes per rank)",
+                             "peak_source": peak_src},
+                "cpu_baseline": cpu,
+                "e2e": {"value": n / float(e2e_t.item()), "unit": UNIT,
+                        "h2d_bytes_per_step": (hi - lo) * (kb // 8 + 4), "d2h_bytes_per_step": (hi - lo) * 4},
+                "gpu_launches": pbit.last_mg_launches * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+    pbit.mg_comm_destroy(comm)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -209,8 +288,6 @@ def run_ours(args):
 
     ws, rank, local = dist_env()
     torch.cuda.set_device(local)
-    if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     c = workloads.CONFIGS[args.config]
     K = args.digit_bits or c["digit_bits"]
     n = c["n"] if args.n is None else args.n
@@ -338,6 +415,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif dist_env()[0] > 1:
+        run_mg(args)
     else:
         run_ours(args)
 

@@ -146,6 +146,9 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
 
 
 # ----------------------------------------------------------------------------- multi-GPU
+last_mg_launches = 0  # kernels the last sort_list_mg call launched
+
+
 def mg_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     rc = lib.pbit_mg_get_unique_id(buf)
@@ -197,10 +200,13 @@ def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int,
     if out_next_local is None:
         out_next_local = torch.empty_like(next_local)
     oh = ctypes.c_uint32(0)
-    o = _opts(digit_bits, _stream_handle(stream, True), None, None)
+    launches = ctypes.c_uint32(0)
+    o = _opts(digit_bits, _stream_handle(stream, True), None, None, ctypes.pointer(launches))
     rc = lib.pbit_sort_list_mg(_ptr(keys_local) if n_local else None, _ptr(next_local) if n_local else None,
                                head & 0xFFFFFFFF, n_global, node_lo, n_local, key_bits, ctypes.byref(oh),
                                _ptr(out_next_local) if n_local else None, ctypes.c_void_p(comm), ctypes.byref(o))
     if rc:
         raise PbitError(rc, _errtext(rc))
+    global last_mg_launches
+    last_mg_launches = int(launches.value)
     return int(oh.value), out_next_local

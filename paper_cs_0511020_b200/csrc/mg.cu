@@ -68,8 +68,9 @@ struct Bump {
 template <int KB>
 int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint32_t n, uint32_t S,
            uint32_t n_local, int K, uint32_t* out_head, uint32_t* out_next_local, ncclComm_t comm, int G, int r,
-           cudaStream_t st) {
+           cudaStream_t st, uint32_t* launches_out) {
   using RT = typename Rec<KB>::T;
+  uint32_t launches = 0;
   using KeyT = typename KeyOf<KB>::T;
   constexpr int REC_WORDS = sizeof(RT) / 4;
   const ncclDataType_t key_t = KB == 8 ? ncclUint64 : ncclUint32;
@@ -180,6 +181,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     // ---- 1. pack the own slice into its place of the replica; local histograms
     if (n_local) {
       const int blocks = std::max(1, std::min((int)((n_local + 255) / 256), sms * 8));
+      ++launches;
       k_pack<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys_local, next_local, n_local, n,
                                                                        kn + lo, hist_l, K, D, err);
     }
@@ -193,6 +195,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       int blocks = sms * (2048 / WALK_THREADS);
       if ((uint32_t)blocks * 4 > total) blocks = std::max(1u, (total + 3) / 4);
       const uint32_t per = (total + blocks - 1) / blocks;
+      ++launches;
       k_walk_count<KB><<<blocks, WALK_THREADS, 0, st>>>(kn, sel, b_lo, b_hi,
                                                         own_head && !head_is_ruler ? Gs : PBIT_NULL32, head, seg, per,
                                                         err);
@@ -204,6 +207,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     // ---- 3. rank the ruler list (identical on every rank)
     {
       const int sblocks = std::max(1, std::min((int)((nsub + 255) / 256), sms * 8));
+      ++launches;
       k_rank_walk_a<<<sblocks, 256, 0, st>>>(seg, sub, Rmax, zero, 0, head_ruler, nsub, sdist[0], scnt[0], ssucc[0],
                                              err);
       int rounds = 1;
@@ -211,14 +215,18 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       rounds += 1;
       int cur = 0;
       for (int i = 0; i < rounds; ++i) {
+        ++launches;
         k_rank_jump<<<sblocks, 256, 0, st>>>(sdist[cur], scnt[cur], ssucc[cur], sdist[cur ^ 1], scnt[cur ^ 1],
                                              ssucc[cur ^ 1], nsub, err);
         cur ^= 1;
       }
+      ++launches;
       k_rank_check<<<1, 1, 0, st>>>(sdist[cur], ssucc[cur], head_sub, n, err);
+      ++launches;
       k_rank_walk_b<<<sblocks, 256, 0, st>>>(seg, sub, Rmax, zero, 0, head_ruler, nsub, head_sub, sdist[cur],
                                              scnt[cur], dist, seg_ord, seg_pos, part_first, S, n, nseg, err);
     }
+    ++launches;
     k_plan<<<1, 256, 0, st>>>(hist_g, bases_l, plan_g, D, K, n, err);
     CUDACHK(cudaMemcpyAsync(&h_plan, plan_g, sizeof(Plan), cudaMemcpyDeviceToHost, st));
     CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
@@ -228,6 +236,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     // ---- 4. emit the list-order chunk of positions [P0, P1)
     if (m) {
       const int blocks = std::max(1, std::min((int)((Gs / G + 2 + 255) / 256), sms * 8));
+      ++launches;
       k_emit_walk<KB><<<blocks, 256, 0, st>>>(kn, sel, head, seg, seg_ord, seg_pos, part_first, r, nseg, P0, P1,
                                               kbuf[0], ibuf[0], err);
     }
@@ -246,11 +255,13 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       pa.kind = SWEEP_KEY;
       pa.keep_keys = 1;  // the sorted keys are needed for the splitters and the exchange
       if (m) {
+        ++launches;
         k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
             kbuf[0], m, K, D, hist_a, err);
       }
+      ++launches;
       k_plan<<<1, 256, 0, st>>>(hist_a, bases_p, plan_p, D, K, m, err);
-      if (m) launch_key_passes_k<KB>(K, pa, D, st, nullptr, 0, false);
+      if (m) { launch_key_passes_k<KB>(K, pa, D, st, nullptr, 0, false); launches += D; }
       Plan h_pp{};
       CUDACHK(cudaMemcpyAsync(&h_pp, plan_p, sizeof(Plan), cudaMemcpyDeviceToHost, st));
       CUDACHK(cudaStreamSynchronize(st));
@@ -271,6 +282,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         for (int sp = 0; sp < NS; ++sp)
           for (int c = 0; c < nc; ++c) h_q[(size_t)sp * nc + c] = ((prefix[sp] << wbits) | (unsigned long long)c) << (K * i);
         CUDACHK(cudaMemcpyAsync(mg_q, h_q.data(), 8ull * NS * nc, cudaMemcpyHostToDevice, st));
+        ++launches;
         k_count_below<KeyT><<<(NS * nc + 255) / 256, 256, 0, st>>>(sk, m, mg_q, NS * nc, 0, mg_c);
         NCCLCHK(ncclAllReduce(mg_c, mg_c, (size_t)NS * nc, ncclUint32, ncclSum, comm, st));
         h_cnt.resize((size_t)NS * nc);
@@ -290,7 +302,9 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         std::vector<uint64_t> h_lt((size_t)G * std::max(NS, 1)), h_le((size_t)G * std::max(NS, 1));
         if (NS > 0) {
           CUDACHK(cudaMemcpyAsync(mg_q, prefix.data(), 8ull * NS, cudaMemcpyHostToDevice, st));
+          ++launches;
           k_count_below<KeyT><<<1, 64, 0, st>>>(sk, m, mg_q, NS, 0, mg_c);
+          ++launches;
           k_count_below<KeyT><<<1, 64, 0, st>>>(sk, m, mg_q, NS, 1, mg_c + NS);
           NCCLCHK(ncclAllGather(mg_c, mg_call, (size_t)2 * NS, ncclUint32, comm, st));
           h_cnt.resize((size_t)2 * NS * G);
@@ -329,20 +343,23 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       CUDACHK(cudaMemsetAsync(tile_ctr, 0, 80 * 4, st));
       CUDACHK(cudaMemsetAsync(hist_b, 0, 4ull * D * radix, st));
       if (m) {
+        ++launches;
         k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
             kbuf[pb], m, K, D, hist_b, err);
       }
+      ++launches;
       k_plan<<<1, 256, 0, st>>>(hist_b, bases_l, plan_l, D, K, m, err);
       SweepArgs la = pa;
       la.kin[0] = kbuf[pb]; la.kin[1] = kbuf[pb ^ 1]; la.vin[0] = ibuf[pb]; la.vin[1] = ibuf[pb ^ 1];
       la.kout[0] = kbuf[pb]; la.kout[1] = kbuf[pb ^ 1]; la.vout[0] = ibuf[pb]; la.vout[1] = ibuf[pb ^ 1];
       la.bases = bases_l; la.plan = plan_l; la.keep_keys = 0;
-      if (m) launch_key_passes_k<KB>(K, la, D, st, nullptr, 0, false);
+      if (m) { launch_key_passes_k<KB>(K, la, D, st, nullptr, 0, false); launches += D; }
       fin[0] = ibuf[pb];
       fin[1] = ibuf[pb ^ 1];
     }
 
     // ---- 7. stitch and relink
+    ++launches;
     k_first_id<<<1, 1, 0, st>>>(final_plan, fin[0], fin[1], m, firsts + G);
     NCCLCHK(ncclAllGather(firsts + G, firsts, 1, ncclUint32, comm, st));
     CUDACHK(cudaMemcpyAsync(h_firsts, firsts, 4ull * G, cudaMemcpyDeviceToHost, st));
@@ -352,6 +369,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       if (h_firsts[d] != PBIT_NULL32) { next_rank = d; break; }
     const int pblocks = std::max(1, std::min((int)((m + 4095) / 4096), sms * 4));
     if (m) {
+      ++launches;
       k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, next_rank, firsts, S, G, cnt, nullptr,
                                              nullptr, nullptr, nullptr, 0, err);
     }
@@ -365,6 +383,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       for (int d = 0; d < G; ++d) { h_offs[d] = acc; acc += h_cntall[(size_t)r * G + d]; }
       CUDACHK(cudaMemcpyAsync(offs, h_offs.data(), 4ull * G, cudaMemcpyHostToDevice, st));
       if (m) {
+        ++launches;
         k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, next_rank, firsts, S, G, nullptr,
                                                offs, fill, send_v, send_s, 1, err);
       }
@@ -386,6 +405,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       if (racc != n_local) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
       // the received pairs: out_next[v] = succ for every own id v, in any order
       if (n_local) {
+        ++launches;
         k_localize<<<std::max(1, std::min((int)((n_local + 255) / 256), sms * 4)), 256, 0, st>>>(pk[0], n_local, lo);
         int topb = 1;
         while ((1ull << topb) < n_local) ++topb;
@@ -398,12 +418,14 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         int par = 0;
         for (int q = 0; q < npass; ++q) {
           const int bit0 = RELINK_FINE_SHIFT + 8 * q;
+          ++launches;
           k_relink_bases<<<1, 256, 0, st>>>(n_local, bit0, rbases + 256 * q);
           ra.bases = rbases + 256 * q;
           ra.slot = 64 + q;
           ra.bit0 = bit0;
           ra.par = par;
           launch_one<uint32_t, 8, 16, SWEEP_PAIR>(ra, st, rank_mode());
+          ++launches;
           par ^= 1;
         }
         static bool attr = false;
@@ -412,6 +434,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
           attr = true;
         }
         const uint32_t nfine = (n_local + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
+        ++launches;
         k_relink_apply<<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(pk[par], pv[par], n_local, out_next_local, err);
       }
     }
@@ -420,6 +443,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     CUDACHK(cudaGetLastError());
     if (h_err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
     *out_head = h_firsts[0];
+    if (launches_out) *launches_out = launches;
   }
 done:
   cudaFreeAsync(base, st);
@@ -535,13 +559,17 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
     return PBIT_ERR_INVALID_ARG;
   switch (key_bits) {
     case 8: return run_mg<1>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
-                             out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st);
+                             out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                             opts ? opts->launches : nullptr);
     case 16: return run_mg<2>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
-                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st);
+                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                             opts ? opts->launches : nullptr);
     case 32: return run_mg<4>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
-                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st);
+                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                             opts ? opts->launches : nullptr);
     default: return run_mg<8>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
-                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st);
+                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                             opts ? opts->launches : nullptr);
   }
 }
 
