@@ -379,10 +379,9 @@ static __global__ void k_selftest_atomic_order(uint32_t iters, uint32_t* bad) {
   if (nb) atomicAdd(bad, nb);
 }
 
-// What one launch of k_onesweep sorts.  kind 0: a key pass of the plan (digit
-// plan->digit[slot], ping-pong parity = slot & 1).  kind 1: the first relink pass, over
-// the final sorted ids (input parity = plan->npasses & 1); each item's value is its
-// successor in that order.  kind 2: a further relink pass over (v, succ) pairs.
+// What one launch of k_onesweep sorts.  KEY: one key pass (digit a.digit, input buffer
+// a.src).  SUCC: the first relink pass, over the final sorted ids; each item's value is
+// its successor in that order.  PAIR: a further relink pass over (v, succ) pairs.
 struct SweepArgs {
   const void* kin[2];
   const uint32_t* vin[2];
@@ -399,7 +398,12 @@ struct SweepArgs {
   int kind;
   int bit0;  // kind 1/2: digit = (key >> bit0) & (RADIX - 1)
   int par;   // kind 2: input buffer index
-  int keep_keys;  // key pass: write keys even in the plan's last pass (mg partition pass)
+  int keep_keys;  // unused on the device (the host folds it into `last`)
+  // host-resolved pass parameters (the host reads the plan after one sync, so no CTA
+  // starts with dependent loads of the plan or the error word)
+  int digit;      // key pass: digit index
+  int last;       // key pass: the last pass of the sort (write ids only)
+  int src;        // input buffer index
   // first key pass (GATHER): the tile is read from the walk's segment slots, in list order
   const void* slots;
   uint32_t cap;
@@ -525,23 +529,18 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   S& sm = *reinterpret_cast<S*>(smem_raw);
 
-  if (*a.err) return;
   const uint32_t n = a.n;
   const int slot = a.slot;
-  int shift, src;
+  const int src = a.src;
+  int shift;
   bool last = false;
   const uint32_t* __restrict__ bases;
   if constexpr (KIND == SWEEP_KEY) {
-    const uint32_t npasses = a.plan->npasses;
-    if ((uint32_t)slot >= npasses) return;
-    const int digit_idx = a.plan->digit[slot];
-    shift = digit_idx * RADIX_BITS;
-    last = (uint32_t)slot + 1 == npasses && !a.keep_keys;
-    src = slot & 1;
-    bases = a.bases + digit_idx * RADIX;
+    shift = a.digit * RADIX_BITS;
+    last = a.last != 0;
+    bases = a.bases + a.digit * RADIX;
   } else {
     shift = a.bit0;
-    src = KIND == SWEEP_SUCC ? (int)(a.plan->npasses & 1u) : a.par;
     bases = a.bases;
   }
   const KeyT* __restrict__ kin = reinterpret_cast<const KeyT*>(a.kin[src]);

@@ -28,12 +28,18 @@ static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
   else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, KIND, GATHER>(a, st);
 }
 
+// The key passes of a host-side plan: pass i sorts digit plan.digit[i] (slot i, its own
+// ticket counter and lookback epoch), reading buffer i & 1.
 template <int KB, int RB>
-static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* ev, int ev_base, bool gather_first) {
+static void launch_key_passes(SweepArgs a, const Plan& plan, bool keep_keys, cudaStream_t st, cudaEvent_t* ev,
+                              int ev_base, bool gather_first) {
   using KeyT = typename KeyOf<KB>::T;
   constexpr int IPT = (KB == 8) ? 12 : 16;
-  for (int s = 0; s < D; ++s) {
-    a.slot = s;
+  for (uint32_t s = 0; s < plan.npasses; ++s) {
+    a.slot = (int)s;
+    a.digit = (int)plan.digit[s];
+    a.src = (int)(s & 1);
+    a.last = (s + 1 == plan.npasses) && !keep_keys;
     if (s == 0 && gather_first) launch_one<KeyT, RB, IPT, SWEEP_KEY, true>(a, st, rank_mode());
     else launch_one<KeyT, RB, IPT, SWEEP_KEY, false>(a, st, rank_mode());
     if (ev) cudaEventRecord(ev[ev_base + s], st);
@@ -41,10 +47,10 @@ static void launch_key_passes(SweepArgs a, int D, cudaStream_t st, cudaEvent_t* 
 }
 
 template <int KB>
-static void launch_key_passes_k(int K, const SweepArgs& a, int D, cudaStream_t st, cudaEvent_t* ev, int ev_base,
-                                bool gather_first = true) {
+static void launch_key_passes_k(int K, const SweepArgs& a, const Plan& plan, bool keep_keys, cudaStream_t st,
+                                cudaEvent_t* ev, int ev_base, bool gather_first) {
   switch (K) {
-#define PBIT_K(RB) case RB: launch_key_passes<KB, RB>(a, D, st, ev, ev_base, gather_first); break;
+#define PBIT_K(RB) case RB: launch_key_passes<KB, RB>(a, plan, keep_keys, st, ev, ev_base, gather_first); break;
     PBIT_K(1) PBIT_K(2) PBIT_K(3) PBIT_K(4) PBIT_K(5) PBIT_K(6) PBIT_K(7) PBIT_K(8)
 #undef PBIT_K
   }

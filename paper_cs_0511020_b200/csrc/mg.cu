@@ -261,10 +261,10 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       }
       ++launches;
       k_plan<<<1, 256, 0, st>>>(hist_a, bases_p, plan_p, D, K, m, err);
-      if (m) { launch_key_passes_k<KB>(K, pa, D, st, nullptr, 0, false); launches += D; }
       Plan h_pp{};
       CUDACHK(cudaMemcpyAsync(&h_pp, plan_p, sizeof(Plan), cudaMemcpyDeviceToHost, st));
       CUDACHK(cudaStreamSynchronize(st));
+      if (m) { launch_key_passes_k<KB>(K, pa, h_pp, true, st, nullptr, 0, false); launches += h_pp.npasses; }
       const int pa_par = (int)(h_pp.npasses & 1u);  // sorted chunk in kbuf/ibuf[pa_par]
       const KeyT* sk = kbuf[pa_par];
 
@@ -349,11 +349,14 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       }
       ++launches;
       k_plan<<<1, 256, 0, st>>>(hist_b, bases_l, plan_l, D, K, m, err);
+      Plan h_pl{};
+      CUDACHK(cudaMemcpyAsync(&h_pl, plan_l, sizeof(Plan), cudaMemcpyDeviceToHost, st));
+      CUDACHK(cudaStreamSynchronize(st));
       SweepArgs la = pa;
       la.kin[0] = kbuf[pb]; la.kin[1] = kbuf[pb ^ 1]; la.vin[0] = ibuf[pb]; la.vin[1] = ibuf[pb ^ 1];
       la.kout[0] = kbuf[pb]; la.kout[1] = kbuf[pb ^ 1]; la.vout[0] = ibuf[pb]; la.vout[1] = ibuf[pb ^ 1];
       la.bases = bases_l; la.plan = plan_l; la.keep_keys = 0;
-      if (m) { launch_key_passes_k<KB>(K, la, D, st, nullptr, 0, false); launches += D; }
+      if (m) { launch_key_passes_k<KB>(K, la, h_pl, false, st, nullptr, 0, false); launches += h_pl.npasses; }
       fin[0] = ibuf[pb];
       fin[1] = ibuf[pb ^ 1];
     }
@@ -424,6 +427,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
           ra.slot = 64 + q;
           ra.bit0 = bit0;
           ra.par = par;
+          ra.src = par;
           launch_one<uint32_t, 8, 16, SWEEP_PAIR>(ra, st, rank_mode());
           ++launches;
           par ^= 1;

@@ -260,10 +260,17 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     launches += rounds + 3;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
   }
-  // a3: bucket bases + pass plan (before the gather, which runs only if no pass does)
+  // a3: bucket bases + pass plan; the host reads {plan, error} once here, so every pass
+  // gets its digit and parity as kernel parameters and trivial digits are not launched
   k_plan<<<1, 256, 0, st>>>(w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
   ++launches;
-  {  // a1: gather to list order -- only when every digit is trivial (no pass to fuse it into)
+  Plan hplan{};
+  int herr = 0;
+  cudaMemcpyAsync(&hplan, w.plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&herr, w.err, 4, cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) herr = -1;
+  const bool ok = herr == 0;
+  if (ok && hplan.npasses == 0) {  // a1: gather to list order -- only when no pass can fuse it
     const uint32_t Rmax = R_static + p.dyn_cap;
     const int gblocks = std::max(1, std::min((int)((Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS)), sms * 8));
     k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, w.seg_ord, w.nseg, n,
@@ -281,20 +288,25 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   sa.slots = w.slots; sa.cap = p.cap; sa.seg = w.seg; sa.seg_ord = w.seg_ord; sa.seg_pos = w.seg_pos;
   sa.tile_first = w.tile_first; sa.nseg = w.nseg;
   { const char* e = getenv("PBIT_DEBUG_NO_LOOKBACK"); sa.debug_no_lookback = e ? atoi(e) : 0; }
-  launch_key_passes_k<KB>(p.K, sa, p.D, st, timing ? ev : nullptr, PBIT_PHASE_PASS0);
-  launches += p.D;
+  if (ok) {
+    launch_key_passes_k<KB>(p.K, sa, hplan, false, st, timing ? ev : nullptr, PBIT_PHASE_PASS0, true);
+    launches += hplan.npasses;
+  }
+  if (timing)
+    for (int s2 = ok ? (int)hplan.npasses : 0; s2 < p.D; ++s2) cudaEventRecord(ev[PBIT_PHASE_PASS0 + s2], st);
 
   // a5: relink: sort (v, succ) by v >> RELINK_FINE_SHIFT (LSD, 8-bit digits), then apply
   // each 2^14-id bin in a shared-memory window
-  if (!sa.debug_no_lookback) {
+  if (ok && !sa.debug_no_lookback) {
     int top = 1;
     while ((1ull << top) < n) ++top;
     const int npass = top > RELINK_FINE_SHIFT ? (top - RELINK_FINE_SHIFT + 7) / 8 : 0;
+    const int fin = (int)(hplan.npasses & 1u);  // buffer holding the final ids
     k_relink_head<<<1, 1, 0, st>>>(w.plan, w.ids[0], w.ids[1], w.d_head, w.err);
     ++launches;
     SweepArgs ra = sa;
     ra.debug_no_lookback = 0;
-    ra.kin[0] = w.ids[0]; ra.kin[1] = w.ids[1];  // kind 1 reads the final ids
+    ra.kin[0] = w.ids[0]; ra.kin[1] = w.ids[1];  // SUCC reads the final ids
     const uint32_t* fin_k = nullptr; const uint32_t* fin_v = nullptr;
     for (int q = 0; q < npass; ++q) {
       const int bit0 = RELINK_FINE_SHIFT + 8 * q;
@@ -304,10 +316,11 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
       ra.bit0 = bit0;
       if (q == 0) {
         ra.kind = 1;
+        ra.src = fin;
         ra.kout[0] = w.rk[0]; ra.vout[0] = w.rv[0];
       } else {
         ra.kind = 2;
-        ra.par = (q - 1) & 1;
+        ra.src = (q - 1) & 1;
         ra.kin[0] = w.rk[0]; ra.kin[1] = w.rk[1]; ra.vin[0] = w.rv[0]; ra.vin[1] = w.rv[1];
         ra.kout[0] = w.rk[0]; ra.kout[1] = w.rk[1]; ra.vout[0] = w.rv[0]; ra.vout[1] = w.rv[1];
       }
