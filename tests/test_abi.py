@@ -13,8 +13,8 @@ HEADER = os.path.join(ROOT, "include", "pbit.h")
 
 @pytest.fixture(scope="module")
 def pbit():
-    from paper_cs_0511020_b200 import build
-    build.build()
+    import __graft_entry__ as g
+    g.build()
     import paper_cs_0511020_b200 as p
     return p
 
