@@ -379,30 +379,23 @@ static __global__ void k_selftest_atomic_order(uint32_t iters, uint32_t* bad) {
   if (nb) atomicAdd(bad, nb);
 }
 
-// What one launch of k_onesweep sorts.  KEY: one key pass (digit a.digit, input buffer
-// a.src).  SUCC: the first relink pass, over the final sorted ids; each item's value is
-// its successor in that order.  PAIR: a further relink pass over (v, succ) pairs.
+// What one launch of k_onesweep sorts: one key pass (digit `digit`, input buffer `src`).
 struct SweepArgs {
   const void* kin[2];
   const uint32_t* vin[2];
   void* kout[2];
   uint32_t* vout[2];
-  const uint32_t* bases;  // kind 0: [digit][RADIX]; kind 1/2: [RADIX] of this pass
+  const uint32_t* bases;  // [digit][RADIX] bucket bases
   unsigned long long* status;
   uint32_t* tile_ctr;
-  const Plan* plan;
   const int* err;
   uint32_t n;
   int slot;  // ticket counter + epoch, unique per launch in a call
   int debug_no_lookback;  // timing experiments only (wrong output)
-  int kind;
-  int bit0;  // kind 1/2: digit = (key >> bit0) & (RADIX - 1)
-  int par;   // kind 2: input buffer index
-  int keep_keys;  // unused on the device (the host folds it into `last`)
   // host-resolved pass parameters (the host reads the plan after one sync, so no CTA
   // starts with dependent loads of the plan or the error word)
-  int digit;      // key pass: digit index
-  int last;       // key pass: the last pass of the sort (write ids only)
+  int digit;      // digit index
+  int last;       // the last pass of the sort (write ids only)
   int src;        // input buffer index
   // first key pass (GATHER): the tile is read from the walk's segment slots, in list order
   const void* slots;
@@ -463,9 +456,6 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
   }
 }
 
-// KIND of a k_onesweep launch (compile-time, so key passes carry no relink code).
-enum : int { SWEEP_KEY = 0, SWEEP_SUCC = 1, SWEEP_PAIR = 2 };
-
 __device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
                "l"(gsrc) : "memory");
@@ -518,7 +508,7 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int KIND, bool GATHER = false>
+template <typename KeyT, int RADIX_BITS, int IPT, int RANK, bool GATHER = false>
 __global__ void __launch_bounds__(SWEEP_THREADS, 2)
 k_onesweep(const __grid_constant__ SweepArgs a) {
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
@@ -532,20 +522,12 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   const uint32_t n = a.n;
   const int slot = a.slot;
   const int src = a.src;
-  int shift;
-  bool last = false;
-  const uint32_t* __restrict__ bases;
-  if constexpr (KIND == SWEEP_KEY) {
-    shift = a.digit * RADIX_BITS;
-    last = a.last != 0;
-    bases = a.bases + a.digit * RADIX;
-  } else {
-    shift = a.bit0;
-    bases = a.bases;
-  }
+  const int shift = a.digit * RADIX_BITS;
+  const bool last = a.last != 0;
+  const uint32_t* __restrict__ bases = a.bases + a.digit * RADIX;
   const KeyT* __restrict__ kin = reinterpret_cast<const KeyT*>(a.kin[src]);
   const uint32_t* __restrict__ iin = a.vin[src];
-  const int dst = KIND == SWEEP_SUCC ? 0 : (src ^ 1);
+  const int dst = src ^ 1;
   KeyT* __restrict__ kout = reinterpret_cast<KeyT*>(a.kout[dst]);
   uint32_t* __restrict__ iout = a.vout[dst];
   const unsigned long long epoch = (unsigned long long)(slot + 1);
@@ -569,11 +551,11 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   if (GATHER) gather_tile<KeyT, TILE>(a, tile, tile_base, tile_count, sm.k, sm.iin, w, lane);
   if (!GATHER && t == 0) {
     const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
-    const uint32_t ib = KIND == SWEEP_SUCC ? 0u : (tile_count * 4u + 15u) & ~15u;
+    const uint32_t ib = (tile_count * 4u + 15u) & ~15u;
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(kb + ib) : "memory");
     bulk_g2s(sm.k, kin + tile_base, kb, &sm.mbar);
-    if constexpr (KIND != SWEEP_SUCC) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
+    bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
   }
   for (uint32_t i = t; i < SWEEP_WARPS * RADIX / 2; i += SWEEP_THREADS) reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
   if (!GATHER) {
@@ -594,16 +576,6 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   for (int i = 0; i < IPT; ++i) key[i] = sm.k[wofs + i * 32 + lane];
   if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
   else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
-  if constexpr (KIND == SWEEP_SUCC) {
-    // the value of item j is its successor in the sorted order: the key of item j+1
-#pragma unroll
-    for (int i = 0; i < IPT; ++i) {
-      const uint32_t j = wofs + i * 32 + lane;
-      if (j < tile_count)
-        sm.iin[j] = j + 1 < tile_count ? (uint32_t)sm.k[j + 1]
-                    : (tile_base + tile_count < n ? (uint32_t)kin[tile_base + tile_count] : PBIT_NULL32);
-    }
-  }
   __syncthreads();
 
   // ---- per digit (thread t = digit t): exclusive over warps, tile total, aggregate
@@ -647,7 +619,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
       const uint32_t d = rd[i] >> 16;
       const uint32_t lp = sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
       sm.iout[lp] = sm.iin[j];
-      sm.k[lp] = (KIND == SWEEP_KEY && last) ? (KeyT)d : key[i];  // the last key pass needs only digits
+      sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass needs only digits
     }
   }
 
@@ -683,7 +655,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 
   // ---- coalesced write-out: consecutive threads store consecutive staged elements,
   // which land contiguously inside each digit run
-  if (KIND != SWEEP_KEY || !last) {
+  if (!last) {
 #pragma unroll 4
     for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
       const KeyT k = sm.k[j];
@@ -705,71 +677,204 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 // end-splice merge of sorted fragments, one write per node.
 //
 // On B200 a random 4 B store costs a 32 B HBM read + write even when the stores are
-// confined to a 64 KB window (measured: tools/micro/winstore.cu), so no kernel here
-// issues scattered partial-sector stores.  The pairs (v, succ) are first grouped by
-// fine bin v >> RELINK_FINE_SHIFT (streaming radix passes), then each fine bin is
-// applied in a shared-memory window and written out coalesced.
+// confined to a 64 KB window (measured: tools/micro/winstore.cu), and distributed shared
+// memory windows are 2-4x slower than one CTA's (tools/micro/dsmem.cu), so no kernel here
+// issues scattered stores to HBM.  The pairs (v, succ) are grouped by fine bin
+// v >> RELINK_FINE_SHIFT with MSD partition levels of <= 8 bits (k_relink_part), then each
+// fine bin is applied in a 64 KB shared-memory window and written out coalesced.
+//
+// The ids are a permutation of [0, n), so every bin's size is known in closed form (bin
+// b of a level with shift s holds exactly the ids [b << s, (b+1) << s)): no histogram,
+// no scan.  Order inside a bin does not matter (each v occurs once), so a tile claims its
+// space in a bin with one global atomicAdd per (tile, bin) -- no lookback.
 constexpr int RELINK_FINE_SHIFT = 14;  // 16384 ids = 64 KB smem window
+constexpr int PART_THREADS = 512;
+constexpr int PART_IPT = 8;
+constexpr int PART_TILE = PART_THREADS * PART_IPT;  // 4096 pairs; divides every parent bin (>= 2^22)
+constexpr int PART_CTAS_PER_SM = 2;
 
-// The pairs are sorted by v's bits [RELINK_FINE_SHIFT, log2 n) with k_onesweep (kind
-// 1 then 2; LSD, 8-bit digits).  Bucket bases need no histogram: the ids are a
-// permutation of [0, n), so the count of each digit value is known in closed form.
-static __global__ void k_relink_bases(uint32_t n, int bit0, uint32_t* __restrict__ bases) {
-  __shared__ uint32_t s_warp[8];
-  const int t = threadIdx.x, lane = t & 31, w = t >> 5;  // 256 threads = 256 digit values
-  const unsigned long long B = 1ull << bit0, P = B << 8;
-  const unsigned long long full = n / P, rem = n % P;
-  const unsigned long long lo = (unsigned long long)t * B;
-  const uint32_t c = (uint32_t)(full * B + (rem > lo ? min(rem - lo, B) : 0ull));
-  uint32_t x = c;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
+// The MSD levels for n ids: level l partitions by v's bits [shift_l, shift_l + bits_l);
+// level 0 takes the top bits, the last level has shift RELINK_FINE_SHIFT.
+struct RelinkLevels {
+  int L = 0;
+  int shift[4] = {0, 0, 0, 0};
+  int bits[4] = {0, 0, 0, 0};
+  __host__ explicit RelinkLevels(uint32_t n) {
+    int top = 0;
+    while (top < 32 && (1ull << top) < (unsigned long long)n) ++top;
+    const int total = top - RELINK_FINE_SHIFT;
+    if (total <= 0) return;
+    L = (total + 7) / 8;
+    int sh = RELINK_FINE_SHIFT + 8 * (L - 1);
+    for (int l = 0; l < L; ++l) {
+      bits[l] = l == 0 ? total - 8 * (L - 1) : 8;
+      shift[l] = sh;
+      sh -= 8;
+    }
   }
-  if (lane == 31) s_warp[w] = x;
-  __syncthreads();
-  uint32_t add = 0;
-  for (int i = 0; i < w; ++i) add += s_warp[i];
-  bases[t] = x - c + add;
-}
+  // cursor words of level l: one per bin of that level over all ids
+  __host__ static size_t cursors(uint32_t n, int shift) { return ((size_t)n >> shift) + 1; }
+};
 
-static __global__ void k_relink_head(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
-                              const uint32_t* __restrict__ ids1, uint32_t* __restrict__ d_head,
-                              const int* __restrict__ err) {
+// One partition level.  FROM_IDS (level 0 of the single-GPU sort): the input is the
+// sorted id array and the pair of position p is (ids[p], ids[p+1]) (NULL after the last).
+// Otherwise the input is pairs; v_off is subtracted from v on load (the multi-GPU path
+// receives global ids).  A tile lies inside one bin of the previous level (tiles divide
+// the bins), so its local bin index is (v >> shift) & (2^bits - 1) and its global bin
+// index is (tile's parent bin) << bits | local.
+//
+// Persistent CTAs (PART_CTAS_PER_SM per SM) walk the tiles round-robin; the next tile's
+// TMA bulk load is issued before the current tile is ranked, so HBM reads stay in flight
+// while the CTA ranks, claims and stores.
+struct PartSmem {
+  uint2 in[2][PART_TILE];  // double-buffered tile loads (FROM_IDS: u32 ids + 4 look-ahead)
+  uint2 stage[PART_TILE];  // the tile in bin order
+  uint32_t cnt[256], start[256], gofs[256], warp[PART_THREADS / 32];
+  unsigned long long mbar[2];
+};
+
+template <bool FROM_IDS>
+__global__ void __launch_bounds__(PART_THREADS, PART_CTAS_PER_SM)
+k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, uint2* __restrict__ pout,
+              uint32_t n, uint32_t v_off, int shift, int bits, uint32_t* __restrict__ cursor,
+              const int* __restrict__ err) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
   if (*err) return;
-  *d_head = ((plan->npasses & 1) ? ids1 : ids0)[0];
+  const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const uint32_t nb = 1u << bits, mask = nb - 1;
+  const uint32_t ntiles = (n + PART_TILE - 1) / PART_TILE;
+  auto issue = [&](uint32_t tile, int buf) {  // thread 0: TMA bulk load of one tile
+    const uint32_t base = tile * (uint32_t)PART_TILE;
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[buf]);
+    uint32_t bytes;
+    const void* src;
+    if constexpr (FROM_IDS) {  // the tile's ids plus the next tile's first (the last succ)
+      const uint32_t c = min((uint32_t)PART_TILE + 4u, n - base);
+      bytes = ((c + 3u) & ~3u) * 4u;
+      src = ids + base;
+    } else {
+      const uint32_t c = min((uint32_t)PART_TILE, n - base);
+      bytes = ((c + 1u) & ~1u) * 8u;
+      src = pin + base;
+    }
+    asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+    bulk_g2s(&sm.in[buf][0], src, bytes, &sm.mbar[buf]);
+  };
+  if (t == 0) {
+    for (int b = 0; b < 2; ++b) {
+      const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[b]);
+      asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(m));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+  }
+  __syncthreads();
+  uint32_t it = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int buf = it & 1;
+    if (t == 0 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
+    if (t < 256) sm.cnt[t] = 0;
+    {
+      const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[buf]);
+      const uint32_t par = (it >> 1) & 1u;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(m), "r"(par) : "memory");
+    }
+    __syncthreads();
+    const uint32_t base = tile * (uint32_t)PART_TILE;
+    const uint32_t cnt = min((uint32_t)PART_TILE, n - base);
+    uint2 x[PART_IPT];
+    uint32_t r[PART_IPT];
+    const uint32_t* in_ids = reinterpret_cast<const uint32_t*>(&sm.in[buf][0]);
+#pragma unroll
+    for (int i = 0; i < PART_IPT; ++i) {
+      const uint32_t j = i * PART_THREADS + t;
+      if (j < cnt) {
+        if constexpr (FROM_IDS) {
+          x[i].x = in_ids[j];
+          x[i].y = base + j + 1 < n ? in_ids[j + 1] : PBIT_NULL32;
+        } else {
+          x[i] = sm.in[buf][j];
+          x[i].x -= v_off;
+        }
+        r[i] = atomicAdd(&sm.cnt[(x[i].x >> shift) & mask], 1u);
+      }
+    }
+    __syncthreads();
+    // exclusive scan of the tile's bin counts; claim the tile's space in every bin
+    const uint32_t parent = FROM_IDS ? 0u : base >> (shift + bits);
+    {
+      const uint32_t c = t < nb ? sm.cnt[t] : 0u;
+      uint32_t y = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= (uint32_t)o) y += z;
+      }
+      if (lane == 31) sm.warp[w] = y;
+      __syncthreads();
+      uint32_t add = 0;
+      for (uint32_t q = 0; q < w; ++q) add += sm.warp[q];
+      if (t < nb) {
+        sm.start[t] = y - c + add;
+        const uint32_t g = (parent << bits) | t;
+        sm.gofs[t] = c ? (g << shift) + atomicAdd(cursor + g, c) : 0u;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < PART_IPT; ++i) {
+      const uint32_t j = i * PART_THREADS + t;
+      if (j < cnt) sm.stage[sm.start[(x[i].x >> shift) & mask] + r[i]] = x[i];
+    }
+    __syncthreads();
+    // coalesced write-out: consecutive threads store consecutive staged pairs, which land
+    // contiguously inside each bin's run
+#pragma unroll 4
+    for (uint32_t j = t; j < cnt; j += PART_THREADS) {
+      const uint2 p = sm.stage[j];
+      const uint32_t b = (p.x >> shift) & mask;
+      __stcs(pout + sm.gofs[b] + (j - sm.start[b]), p);
+    }
+    __syncthreads();  // stage, start and gofs are rewritten by the next tile
+  }
 }
 
-// Level 3: one CTA per fine bin: scatter into a 64 KB smem window, write it coalesced.
-static __global__ void __launch_bounds__(512)
-k_relink_apply(const uint32_t* __restrict__ pv, const uint32_t* __restrict__ ps, uint32_t n,
+static __global__ void k_relink_head(const uint32_t* __restrict__ ids, uint32_t* __restrict__ d_head,
+                                     const int* __restrict__ err) {
+  if (*err) return;
+  *d_head = ids[0];
+}
+
+// Last step: one CTA per fine bin: scatter into a 64 KB smem window, write it coalesced.
+// FROM_IDS: n <= 2^14, one window, the pairs come straight from the sorted ids.
+template <bool FROM_IDS>
+__global__ void __launch_bounds__(512)
+k_relink_apply(const uint32_t* __restrict__ ids, const uint2* __restrict__ pairs, uint32_t n, uint32_t v_off,
                uint32_t* __restrict__ out_next, const int* __restrict__ err) {
   extern __shared__ __align__(16) uint32_t s_win[];
   if (*err) return;
   const uint32_t f0 = blockIdx.x << RELINK_FINE_SHIFT;
   const uint32_t cnt = min((uint32_t)(1u << RELINK_FINE_SHIFT), n - f0);
-  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) s_win[__ldcs(pv + f0 + i) - f0] = __ldcs(ps + f0 + i);
+  for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+    if constexpr (FROM_IDS) {
+      s_win[ids[i]] = i + 1 < n ? ids[i + 1] : PBIT_NULL32;
+    } else {
+      const uint2 p = __ldcs(pairs + f0 + i);
+      s_win[p.x - v_off - f0] = p.y;
+    }
+  }
   __syncthreads();
   uint32_t* dst = out_next + f0;
   if ((cnt & 3u) == 0 && ((uintptr_t)dst & 15u) == 0) {
     for (uint32_t i = threadIdx.x; i < cnt / 4; i += blockDim.x)
-      reinterpret_cast<uint4*>(dst)[i] = reinterpret_cast<const uint4*>(s_win)[i];
+      __stcs(reinterpret_cast<uint4*>(dst) + i, reinterpret_cast<const uint4*>(s_win)[i]);
   } else {
     for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = s_win[i];
   }
-}
-
-// n <= 2^14: the whole out_next is one window.
-static __global__ void __launch_bounds__(512)
-k_relink_small(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, const uint32_t* __restrict__ ids1,
-               uint32_t n, uint32_t* __restrict__ out_next, const int* __restrict__ err) {
-  extern __shared__ __align__(16) uint32_t s_win[];
-  if (*err) return;
-  const uint32_t* __restrict__ ids = (plan->npasses & 1) ? ids1 : ids0;
-  for (uint32_t p = threadIdx.x; p < n; p += blockDim.x) s_win[ids[p]] = p + 1 < n ? ids[p + 1] : PBIT_NULL32;
-  __syncthreads();
-  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) out_next[i] = s_win[i];
 }
 
 }  // namespace pbit

@@ -2,30 +2,32 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "kernels.cuh"
 #include "pbit_internal.h"
 
 namespace pbit {
 
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
-template <typename KeyT, int RB, int IPT, int RANK, int KIND, bool GATHER>
+template <typename KeyT, int RB, int IPT, int RANK, bool GATHER>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
   static bool attr = false;  // benign race: idempotent
   if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, KIND, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(S));
     attr = true;
   }
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  k_onesweep<KeyT, RB, IPT, RANK, KIND, GATHER><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+  k_onesweep<KeyT, RB, IPT, RANK, GATHER><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
 }
 
-template <typename KeyT, int RB, int IPT, int KIND, bool GATHER = false>
+template <typename KeyT, int RB, int IPT, bool GATHER = false>
 static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
-  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, KIND, GATHER>(a, st);
-  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, KIND, GATHER>(a, st);
-  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, KIND, GATHER>(a, st);
+  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, GATHER>(a, st);
+  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, GATHER>(a, st);
+  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, GATHER>(a, st);
 }
 
 // The key passes of a host-side plan: pass i sorts digit plan.digit[i] (slot i, its own
@@ -40,8 +42,8 @@ static void launch_key_passes(SweepArgs a, const Plan& plan, bool keep_keys, cud
     a.digit = (int)plan.digit[s];
     a.src = (int)(s & 1);
     a.last = (s + 1 == plan.npasses) && !keep_keys;
-    if (s == 0 && gather_first) launch_one<KeyT, RB, IPT, SWEEP_KEY, true>(a, st, rank_mode());
-    else launch_one<KeyT, RB, IPT, SWEEP_KEY, false>(a, st, rank_mode());
+    if (s == 0 && gather_first) launch_one<KeyT, RB, IPT, true>(a, st, rank_mode());
+    else launch_one<KeyT, RB, IPT, false>(a, st, rank_mode());
     if (ev) cudaEventRecord(ev[ev_base + s], st);
   }
 }
@@ -54,6 +56,57 @@ static void launch_key_passes_k(int K, const SweepArgs& a, const Plan& plan, boo
     PBIT_K(1) PBIT_K(2) PBIT_K(3) PBIT_K(4) PBIT_K(5) PBIT_K(6) PBIT_K(7) PBIT_K(8)
 #undef PBIT_K
   }
+}
+
+// Cursor words launch_relink needs (zeroed by the caller before the call).
+static inline size_t relink_cursor_words(uint32_t n) {
+  RelinkLevels lv(n);
+  size_t c = 0;
+  for (int l = 0; l < lv.L; ++l) c += RelinkLevels::cursors(n, lv.shift[l]);
+  return c + 1;
+}
+
+// a5 relink of n local ids: out_next[v] = succ.  Source: the sorted ids (`ids`, pairs
+// formed on the fly) or pairs (`pairs`, v - v_off = local id).  pbuf[2]: n pairs each;
+// when the source is pairs it must not be pbuf[0] (level 0 writes pbuf[0]).
+// Returns the number of kernels launched.
+static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t v_off, uint32_t n, uint2* pbuf0,
+                              uint2* pbuf1, uint32_t* cursors, uint32_t* out_next, const int* err, cudaStream_t st,
+                              int sms) {
+  static bool attr = false;  // benign race: idempotent
+  if (!attr) {
+    cudaFuncSetAttribute(k_relink_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
+    cudaFuncSetAttribute(k_relink_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
+    cudaFuncSetAttribute(k_relink_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
+    cudaFuncSetAttribute(k_relink_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
+    attr = true;
+  }
+  if (n == 0) return 0;
+  RelinkLevels lv(n);
+  const uint32_t nfine = (n + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
+  if (lv.L == 0) {
+    if (ids) k_relink_apply<true><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(ids, nullptr, n, 0, out_next, err);
+    else k_relink_apply<false><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, pairs, n, v_off, out_next, err);
+    return 1;
+  }
+  const uint32_t ntiles = (n + PART_TILE - 1) / PART_TILE;
+  const uint32_t grid = std::min<uint32_t>(ntiles, (uint32_t)(sms * PART_CTAS_PER_SM));
+  const size_t psm = sizeof(PartSmem);
+  const uint2* in = pairs;
+  uint2* buf[2] = {pbuf0, pbuf1};
+  for (int l = 0; l < lv.L; ++l) {
+    uint2* out = buf[l & 1];
+    if (l == 0 && ids)
+      k_relink_part<true><<<grid, PART_THREADS, psm, st>>>(ids, nullptr, out, n, 0, lv.shift[l], lv.bits[l], cursors,
+                                                           err);
+    else
+      k_relink_part<false><<<grid, PART_THREADS, psm, st>>>(nullptr, in, out, n, l == 0 ? v_off : 0u, lv.shift[l],
+                                                            lv.bits[l], cursors, err);
+    cursors += RelinkLevels::cursors(n, lv.shift[l]);
+    in = out;
+  }
+  k_relink_apply<false><<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, in, n, 0, out_next, err);
+  return (uint32_t)lv.L + 1;
 }
 
 }  // namespace pbit

@@ -107,9 +107,9 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   RT* kn = nullptr; uint2* seg = nullptr; uint32_t *dist = nullptr, *seg_ord = nullptr, *seg_pos = nullptr;
   uint32_t* part_first = nullptr; unsigned long long* sdist[2] = {}; uint32_t* scnt[2] = {}; uint32_t* ssucc[2] = {};
   KeyT* kbuf[2] = {}; uint32_t* ibuf[2] = {}; unsigned long long* status = nullptr;
-  uint32_t *send_v = nullptr, *send_s = nullptr, *pk[2] = {}, *pv[2] = {};
+  uint2 *send_p = nullptr, *pr[2] = {};
   uint32_t *hist_l = nullptr, *hist_g = nullptr, *hist_a = nullptr, *hist_b = nullptr, *bases_p = nullptr,
-           *bases_l = nullptr, *rbases = nullptr, *cntmat = nullptr, *firsts = nullptr, *cnt = nullptr,
+           *bases_l = nullptr, *cursors = nullptr, *cntmat = nullptr, *firsts = nullptr, *cnt = nullptr,
            *offs = nullptr, *fill = nullptr, *cntall = nullptr, *tile_ctr = nullptr, *nseg = nullptr,
            *zero = nullptr, *tile_first_unused = nullptr, *mg_c = nullptr, *mg_call = nullptr;
   unsigned long long* mg_q = nullptr;
@@ -134,12 +134,10 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       ssucc[i] = b.take<uint32_t>(nsub + 1);
       kbuf[i] = b.take<KeyT>(S);
       ibuf[i] = b.take<uint32_t>(S);
-      pk[i] = b.take<uint32_t>(S);
-      pv[i] = b.take<uint32_t>(S);
+      pr[i] = b.take<uint2>(S);
     }
     status = b.take<unsigned long long>(ntiles * 256);
-    send_v = b.take<uint32_t>(S);
-    send_s = b.take<uint32_t>(S);
+    send_p = b.take<uint2>(S);
     ctl_off = b.off;
     hist_l = b.take<uint32_t>((size_t)D * radix);
     hist_g = b.take<uint32_t>((size_t)D * radix);
@@ -147,7 +145,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     hist_b = b.take<uint32_t>((size_t)D * radix);
     bases_p = b.take<uint32_t>((size_t)D * radix);
     bases_l = b.take<uint32_t>((size_t)D * radix);
-    rbases = b.take<uint32_t>(4 * 256);
+    cursors = b.take<uint32_t>(relink_cursor_words(S));
     cntmat = b.take<uint32_t>((size_t)G * radix);
     firsts = b.take<uint32_t>(G + 1);
     cnt = b.take<uint32_t>(G);
@@ -251,9 +249,8 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       SweepArgs pa{};
       pa.kin[0] = kbuf[0]; pa.kin[1] = kbuf[1]; pa.vin[0] = ibuf[0]; pa.vin[1] = ibuf[1];
       pa.kout[0] = kbuf[0]; pa.kout[1] = kbuf[1]; pa.vout[0] = ibuf[0]; pa.vout[1] = ibuf[1];
-      pa.bases = bases_p; pa.status = status; pa.tile_ctr = tile_ctr; pa.plan = plan_p; pa.err = err; pa.n = m;
-      pa.kind = SWEEP_KEY;
-      pa.keep_keys = 1;  // the sorted keys are needed for the splitters and the exchange
+      pa.bases = bases_p; pa.status = status; pa.tile_ctr = tile_ctr; pa.err = err; pa.n = m;
+      // keep_keys below: the sorted keys are needed for the splitters and the exchange
       if (m) {
         ++launches;
         k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
@@ -355,7 +352,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       SweepArgs la = pa;
       la.kin[0] = kbuf[pb]; la.kin[1] = kbuf[pb ^ 1]; la.vin[0] = ibuf[pb]; la.vin[1] = ibuf[pb ^ 1];
       la.kout[0] = kbuf[pb]; la.kout[1] = kbuf[pb ^ 1]; la.vout[0] = ibuf[pb]; la.vout[1] = ibuf[pb ^ 1];
-      la.bases = bases_l; la.plan = plan_l; la.keep_keys = 0;
+      la.bases = bases_l;
       if (m) { launch_key_passes_k<KB>(K, la, h_pl, false, st, nullptr, 0, false); launches += h_pl.npasses; }
       fin[0] = ibuf[pb];
       fin[1] = ibuf[pb ^ 1];
@@ -374,7 +371,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     if (m) {
       ++launches;
       k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, next_rank, firsts, S, G, cnt, nullptr,
-                                             nullptr, nullptr, nullptr, 0, err);
+                                             nullptr, nullptr, 0, err);
     }
     NCCLCHK(ncclAllGather(cnt, cntall, G, ncclUint32, comm, st));
     h_cntall.resize((size_t)G * G);
@@ -388,59 +385,20 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       if (m) {
         ++launches;
         k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, next_rank, firsts, S, G, nullptr,
-                                               offs, fill, send_v, send_s, 1, err);
+                                               offs, fill, send_p, 1, err);
       }
       uint32_t racc = 0;
       NCCLCHK(ncclGroupStart());
       for (int d = 0; d < G; ++d) {
         const uint32_t sc = h_cntall[(size_t)r * G + d], rcn = h_cntall[(size_t)d * G + r];
-        if (sc) {
-          NCCLCHK(ncclSend(send_v + h_offs[d], sc, ncclUint32, d, comm, st));
-          NCCLCHK(ncclSend(send_s + h_offs[d], sc, ncclUint32, d, comm, st));
-        }
-        if (rcn) {
-          NCCLCHK(ncclRecv(pk[0] + racc, rcn, ncclUint32, d, comm, st));
-          NCCLCHK(ncclRecv(pv[0] + racc, rcn, ncclUint32, d, comm, st));
-        }
+        if (sc) NCCLCHK(ncclSend(send_p + h_offs[d], 2ull * sc, ncclUint32, d, comm, st));
+        if (rcn) NCCLCHK(ncclRecv(pr[1] + racc, 2ull * rcn, ncclUint32, d, comm, st));
         racc += rcn;
       }
       NCCLCHK(ncclGroupEnd());
       if (racc != n_local) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
-      // the received pairs: out_next[v] = succ for every own id v, in any order
-      if (n_local) {
-        ++launches;
-        k_localize<<<std::max(1, std::min((int)((n_local + 255) / 256), sms * 4)), 256, 0, st>>>(pk[0], n_local, lo);
-        int topb = 1;
-        while ((1ull << topb) < n_local) ++topb;
-        const int npass = topb > RELINK_FINE_SHIFT ? (topb - RELINK_FINE_SHIFT + 7) / 8 : 0;
-        SweepArgs ra{};
-        ra.kin[0] = pk[0]; ra.kin[1] = pk[1]; ra.vin[0] = pv[0]; ra.vin[1] = pv[1];
-        ra.kout[0] = pk[0]; ra.kout[1] = pk[1]; ra.vout[0] = pv[0]; ra.vout[1] = pv[1];
-        ra.status = status; ra.tile_ctr = tile_ctr; ra.plan = plan_l; ra.err = err; ra.n = n_local;
-        ra.kind = SWEEP_PAIR;
-        int par = 0;
-        for (int q = 0; q < npass; ++q) {
-          const int bit0 = RELINK_FINE_SHIFT + 8 * q;
-          ++launches;
-          k_relink_bases<<<1, 256, 0, st>>>(n_local, bit0, rbases + 256 * q);
-          ra.bases = rbases + 256 * q;
-          ra.slot = 64 + q;
-          ra.bit0 = bit0;
-          ra.par = par;
-          ra.src = par;
-          launch_one<uint32_t, 8, 16, SWEEP_PAIR>(ra, st, rank_mode());
-          ++launches;
-          par ^= 1;
-        }
-        static bool attr = false;
-        if (!attr) {
-          cudaFuncSetAttribute(k_relink_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
-          attr = true;
-        }
-        const uint32_t nfine = (n_local + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
-        ++launches;
-        k_relink_apply<<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(pk[par], pv[par], n_local, out_next_local, err);
-      }
+      // the received pairs (global v): out_next[v - lo] = succ for every own id v, in any order
+      if (n_local) launches += launch_relink(nullptr, pr[1], lo, n_local, pr[0], pr[1], cursors, out_next_local, err, st, sms);
     }
     CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
     CUDACHK(cudaStreamSynchronize(st));

@@ -148,7 +148,7 @@ static __global__ void __launch_bounds__(256)
 k_pairs_owner(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, const uint32_t* __restrict__ ids1,
               uint32_t m, uint32_t next_first_dev_idx, const uint32_t* __restrict__ firsts, uint32_t S, int G,
               uint32_t* __restrict__ counts, const uint32_t* __restrict__ offsets, uint32_t* __restrict__ fill,
-              uint32_t* __restrict__ send_v, uint32_t* __restrict__ send_s, int scatter, const int* __restrict__ err) {
+              uint2* __restrict__ send, int scatter, const int* __restrict__ err) {
   __shared__ uint32_t s_cnt[64];
   __shared__ uint32_t s_base[64];
   if (*err) return;
@@ -175,8 +175,7 @@ k_pairs_owner(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, 
     const uint32_t s = p + 1 < m ? ids[p + 1] : next_first;
     const uint32_t o = v / S;
     const uint32_t at = s_base[o] + atomicAdd(&s_cnt[o], 1u);
-    send_v[at] = v;
-    send_s[at] = s;
+    send[at] = make_uint2(v, s);
   }
 }
 
@@ -185,11 +184,6 @@ static __global__ void k_first_id(const Plan* __restrict__ plan, const uint32_t*
                            const uint32_t* __restrict__ ids1, uint32_t m, uint32_t* __restrict__ out) {
   const uint32_t* ids = (plan->npasses & 1) ? ids1 : ids0;
   *out = m ? ids[0] : PBIT_NULL32;
-}
-
-// Received pairs carry global ids: make v local to this rank's slice.
-static __global__ void k_localize(uint32_t* __restrict__ v, uint32_t m, uint32_t lo) {
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < m; p += gridDim.x * blockDim.x) v[p] -= lo;
 }
 
 }  // namespace pbit

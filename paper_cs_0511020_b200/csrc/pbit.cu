@@ -129,10 +129,10 @@ struct Ws {
   void* kn; void* slots; uint2* seg; uint32_t* dist;
   unsigned long long* sdist[2]; uint32_t* scnt[2]; uint32_t* ssucc[2]; uint32_t* seg_ord; uint32_t* seg_pos;
   uint32_t* tile_first;
-  void* keys[2]; uint32_t* ids[2]; unsigned long long* status; uint32_t* rk[2]; uint32_t* rv[2];
+  void* keys[2]; uint32_t* ids[2]; unsigned long long* status; uint2* pairs[2];
   // control block (zeroed per call)
   uint32_t* hist; uint32_t* bases; Plan* plan; int* err; uint32_t* dyn_count; uint32_t* tile_ctr; uint32_t* d_head;
-  uint32_t* rbases; uint32_t* nseg;
+  uint32_t* cursors; uint32_t* nseg;
   size_t ctl_bytes; void* ctl; size_t status_bytes;
 };
 
@@ -149,10 +149,8 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   auto take = [&](size_t bytes) { char* q = base ? base + off : nullptr; off += align_up(bytes); return (void*)q; };
   w->kn = take(n * rec);
   w->slots = take(Rmax * p.cap * rec);  // also holds the relink pairs (dead slots by then)
-  for (int i = 0; i < 2; ++i) {  // relink (v, succ) buffers: 4 x n u32 <= slot bytes
-    w->rk[i] = base ? (uint32_t*)w->slots + (2 * i) * align_up(n) : nullptr;
-    w->rv[i] = base ? (uint32_t*)w->slots + (2 * i + 1) * align_up(n) : nullptr;
-  }
+  for (int i = 0; i < 2; ++i)  // relink (v, succ) buffers: 2 x n x 8 B <= slot bytes
+    w->pairs[i] = base ? (uint2*)w->slots + i * align_up(n) : nullptr;
   w->seg = (uint2*)take(Rmax * 8);
   w->dist = (uint32_t*)take(Rmax * 4);
   const size_t nsub = (Rmax >> SUB_LOG2) + 2;
@@ -175,7 +173,7 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   w->dyn_count = (uint32_t*)take(4);
   w->tile_ctr = (uint32_t*)take(80 * 4);
   w->d_head = (uint32_t*)take(4);
-  w->rbases = (uint32_t*)take(4 * 256 * 4);
+  w->cursors = (uint32_t*)take(relink_cursor_words(p.n) * 4);
   w->nseg = (uint32_t*)take(4);
   w->ctl = base ? base + ctl0 : nullptr;
   w->ctl_bytes = off - ctl0;
@@ -283,8 +281,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   SweepArgs sa{};
   sa.kin[0] = w.keys[0]; sa.kin[1] = w.keys[1]; sa.vin[0] = w.ids[0]; sa.vin[1] = w.ids[1];
   sa.kout[0] = w.keys[0]; sa.kout[1] = w.keys[1]; sa.vout[0] = w.ids[0]; sa.vout[1] = w.ids[1];
-  sa.bases = w.bases; sa.status = w.status; sa.tile_ctr = w.tile_ctr; sa.plan = w.plan; sa.err = w.err; sa.n = n;
-  sa.kind = 0;
+  sa.bases = w.bases; sa.status = w.status; sa.tile_ctr = w.tile_ctr; sa.err = w.err; sa.n = n;
   sa.slots = w.slots; sa.cap = p.cap; sa.seg = w.seg; sa.seg_ord = w.seg_ord; sa.seg_pos = w.seg_pos;
   sa.tile_first = w.tile_first; sa.nseg = w.nseg;
   { const char* e = getenv("PBIT_DEBUG_NO_LOOKBACK"); sa.debug_no_lookback = e ? atoi(e) : 0; }
@@ -295,55 +292,13 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (timing)
     for (int s2 = ok ? (int)hplan.npasses : 0; s2 < p.D; ++s2) cudaEventRecord(ev[PBIT_PHASE_PASS0 + s2], st);
 
-  // a5: relink: sort (v, succ) by v >> RELINK_FINE_SHIFT (LSD, 8-bit digits), then apply
-  // each 2^14-id bin in a shared-memory window
+  // a5: relink: (v, succ) pairs grouped by v's fine bin (MSD partition levels), then
+  // each 2^14-id bin applied in a shared-memory window
   if (ok && !sa.debug_no_lookback) {
-    int top = 1;
-    while ((1ull << top) < n) ++top;
-    const int npass = top > RELINK_FINE_SHIFT ? (top - RELINK_FINE_SHIFT + 7) / 8 : 0;
-    const int fin = (int)(hplan.npasses & 1u);  // buffer holding the final ids
-    k_relink_head<<<1, 1, 0, st>>>(w.plan, w.ids[0], w.ids[1], w.d_head, w.err);
+    const uint32_t* fin = w.ids[hplan.npasses & 1u];  // buffer holding the final ids
+    k_relink_head<<<1, 1, 0, st>>>(fin, w.d_head, w.err);
     ++launches;
-    SweepArgs ra = sa;
-    ra.debug_no_lookback = 0;
-    ra.kin[0] = w.ids[0]; ra.kin[1] = w.ids[1];  // SUCC reads the final ids
-    const uint32_t* fin_k = nullptr; const uint32_t* fin_v = nullptr;
-    for (int q = 0; q < npass; ++q) {
-      const int bit0 = RELINK_FINE_SHIFT + 8 * q;
-      k_relink_bases<<<1, 256, 0, st>>>(n, bit0, w.rbases + 256 * q);
-      ra.bases = w.rbases + 256 * q;
-      ra.slot = 64 + q;  // key passes use slots 0..63
-      ra.bit0 = bit0;
-      if (q == 0) {
-        ra.kind = 1;
-        ra.src = fin;
-        ra.kout[0] = w.rk[0]; ra.vout[0] = w.rv[0];
-      } else {
-        ra.kind = 2;
-        ra.src = (q - 1) & 1;
-        ra.kin[0] = w.rk[0]; ra.kin[1] = w.rk[1]; ra.vin[0] = w.rv[0]; ra.vin[1] = w.rv[1];
-        ra.kout[0] = w.rk[0]; ra.kout[1] = w.rk[1]; ra.vout[0] = w.rv[0]; ra.vout[1] = w.rv[1];
-      }
-      // LSD over two digits: the relink passes must be stable too
-      if (q == 0) launch_one<uint32_t, 8, 16, SWEEP_SUCC>(ra, st, rank_mode());
-      else launch_one<uint32_t, 8, 16, SWEEP_PAIR>(ra, st, rank_mode());
-      fin_k = w.rk[q & 1]; fin_v = w.rv[q & 1];
-      launches += 2;
-    }
-    const uint32_t nfine = (n + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_relink_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
-      cudaFuncSetAttribute(k_relink_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
-      attr = true;
-    }
-    if (npass == 0) {
-      // n <= 2^14: one window; the pairs come straight from the final ids
-      k_relink_small<<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(w.plan, w.ids[0], w.ids[1], n, out_next, w.err);
-    } else {
-      k_relink_apply<<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(fin_k, fin_v, n, out_next, w.err);
-    }
-    ++launches;
+    launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_next, w.err, st, sms);
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
 

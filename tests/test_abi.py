@@ -13,8 +13,11 @@ HEADER = os.path.join(ROOT, "include", "pbit.h")
 
 @pytest.fixture(scope="module")
 def pbit():
-    import __graft_entry__ as g
-    g.build()
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_pbit_build", os.path.join(ROOT, "paper_cs_0511020_b200", "build.py"))
+    b = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(b)
+    b.build()  # rebuilds only when a source is newer than libpbit.so
     import paper_cs_0511020_b200 as p
     return p
 
