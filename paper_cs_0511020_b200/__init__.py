@@ -16,7 +16,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpbit.so")
+LIB_PATH = os.environ.get("PBIT_LIB_PATH") or os.path.join(_HERE, "libpbit.so")  # override: experiments only
 PBIT_NULL = 0xFFFFFFFF
 NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]

@@ -19,6 +19,10 @@ namespace pbit {
 
 constexpr int PACK_THREADS = 256;
 constexpr int WALK_THREADS = 256;
+#ifndef PBIT_WALK_FLUSH
+#define PBIT_WALK_FLUSH 128
+#endif
+constexpr int WALK_FLUSH_BYTES = PBIT_WALK_FLUSH;  // walk record stores per group
 constexpr int SWEEP_THREADS = 512;  // 16 warps x 16 items: 8192-item tiles halve the lookback traffic
 constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
 
@@ -73,9 +77,9 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
        uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t per_cta, int* __restrict__ err,
        int no_writes) {  // no_writes: timing experiments only
   using RT = typename Rec<KB>::T;
-  // Records are staged in registers and stored as whole 32 B sectors: a partial-sector
-  // store costs an HBM read-modify-write on B200.
-  constexpr int B = 32 / sizeof(RT);
+  // Records are staged in registers and stored in groups of WALK_FLUSH_BYTES, always as
+  // whole 32 B sectors: a partial-sector store costs an HBM read-modify-write on B200.
+  constexpr int B = WALK_FLUSH_BYTES / sizeof(RT);
   __shared__ uint32_t s_next;
   if (threadIdx.x == 0) s_next = 0;
   __syncthreads();
@@ -87,47 +91,52 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
     const uint32_t r = lo + atomicAdd(&s_next, 1u);
     if (r >= hi) break;
     uint32_t u = r < sel.R ? sel.node_of(r) : head;
-    uint32_t cur = r, j = 0;
+    uint32_t cur = r, j = 0;  // j: records of segment `cur` already stored
     RT* out = slots + (size_t)cur * cap;
-    auto flush_partial = [&](uint32_t jj) {
-      const uint32_t m = jj % B, b0 = jj - m;
-#pragma unroll
-      for (int q = 0; q < B; ++q)
-        if ((uint32_t)q < m) out[b0 + q] = buf[q];
-    };
     for (;;) {
-      RT x;
-      if constexpr (KB == 8) x = ld_stream_u4(kn + u); else x = ld_stream_u2(kn + u);
-      uint32_t v;
-      if constexpr (KB == 8) { v = x.z; x.z = u; } else { v = x.y; x.y = u; }
-#pragma unroll
-      for (int q = 0; q < B; ++q)
-        if ((j % B) == (uint32_t)q) buf[q] = x;
-      ++j;
-      if ((j % B) == 0 && !no_writes) {
-        uint4* o = reinterpret_cast<uint4*>(out + (j - B));
-        const uint4* bb = reinterpret_cast<const uint4*>(buf);
-        o[0] = bb[0];
-        o[1] = bb[1];
-      }
+      // one group of up to B steps, unrolled so that buf[] is indexed statically
+      uint32_t m = 0, succ = PBIT_NULL32;
       bool end = false;
-      uint32_t succ = PBIT_NULL32;
-      if (v == PBIT_NULL32) end = true;
-      else if (v >= n) { atomicOr(err, E_BAD_INDEX); end = true; }
-      else if (sel.is_ruler(v)) { succ = v >> sel.s_log2; end = true; }
+#pragma unroll
+      for (int q = 0; q < B; ++q) {
+        if (!end) {
+          RT x;
+          if constexpr (KB == 8) x = ld_stream_u4(kn + u); else x = ld_stream_u2(kn + u);
+          uint32_t v;
+          if constexpr (KB == 8) { v = x.z; x.z = u; } else { v = x.y; x.y = u; }
+          buf[q] = x;
+          m = q + 1;
+          if (v == PBIT_NULL32) end = true;
+          else if (v >= n) { atomicOr(err, E_BAD_INDEX); end = true; }
+          else if (sel.is_ruler(v)) { succ = v >> sel.s_log2; end = true; }
+          u = v;
+        }
+      }
+      if (!no_writes) {
+        uint4* o = reinterpret_cast<uint4*>(out + j);
+        const uint4* bb = reinterpret_cast<const uint4*>(buf);
+        if (m == (uint32_t)B) {
+#pragma unroll
+          for (int q = 0; q < B * (int)sizeof(RT) / 16; ++q) o[q] = bb[q];
+        } else {  // segment end: whole 32 B sectors (the slot has room: cap % B == 0)
+          const uint32_t nsec = (m * (uint32_t)sizeof(RT) + 31u) / 32u;
+#pragma unroll
+          for (int q = 0; q < B * (int)sizeof(RT) / 32; ++q)
+            if ((uint32_t)q < nsec) { o[2 * q] = bb[2 * q]; o[2 * q + 1] = bb[2 * q + 1]; }
+        }
+      }
+      j += m;
       if (end) {
-        flush_partial(j);
         seg[cur] = make_uint2(j, succ);
         break;
       }
-      if (j == cap) {  // cap is a multiple of B: nothing left in buf
+      if (j == cap) {  // cap is a multiple of B
         const uint32_t k = atomicAdd(dyn_count, 1u);
         if (k >= dyn_cap) { atomicOr(err, E_DYN_FULL); seg[cur] = make_uint2(j, PBIT_NULL32); break; }
         const uint32_t r2 = R_static + k;
         seg[cur] = make_uint2(cap, r2);
         cur = r2; j = 0; out = slots + (size_t)cur * cap;
       }
-      u = v;
     }
   }
 }

@@ -222,7 +222,13 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   const uint32_t R_static = p.R + (head_is_ruler ? 0u : 1u);
   const uint32_t head_ruler = head_is_ruler ? (head >> p.s_log2) : p.R;
   {
-    int blocks = sms * (2048 / WALK_THREADS);
+    static int walk_occ[9] = {0};  // resident walk CTAs per SM, by key bytes
+    if (!walk_occ[KB]) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_occ[KB], k_walk<KB>, WALK_THREADS, 0);
+      if (walk_occ[KB] < 1) walk_occ[KB] = 1;
+      if (int cap_occ = debug_env("PBIT_WALK_OCC")) walk_occ[KB] = std::min(walk_occ[KB], cap_occ);  // experiments
+    }
+    int blocks = sms * walk_occ[KB];  // one wave: the rulers are split statically over the CTAs
     const uint32_t min_per = 4;
     if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
