@@ -50,6 +50,11 @@ def phase_bytes_per_node(key_bits: int):
     }
 
 
+# Measured ceiling of dependent random 8 B reads on this B200 (G lines/s; each read moves a
+# 128 B line): tools/micro/randread.cu, DESIGN.md §6.
+WALK_LINE_CEILING_G = 39.5
+
+
 def method_bytes_per_node(key_bits: int):
     """The one-read-one-write lower bound of the method: read key and next, write
     out_next."""
@@ -304,14 +309,19 @@ def run_ours(args):
         pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out)
     torch.cuda.synchronize()
 
-    # ---- timed region: K calls, device events on the launching stream
+    # ---- timed region: K calls, device events on the launching stream.  The library also
+    # records CUDA events between its kernels on that stream (timing=True, pooled events),
+    # which gives each kernel's live device time inside the same timed calls.
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    phases = {}
     with ClockSampler(local) as clk:
         e0.record(st)
         for _ in range(args.steps):
-            h, _ = pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out)
+            h, _, ph = pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out, timing=True)
+            for k_, v in ph.items():
+                phases[k_] = phases.get(k_, 0.0) + v
         e1.record(st)
         torch.cuda.synchronize()
     barrier()
@@ -321,13 +331,6 @@ def run_ours(args):
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
     value = n * ws / (ms_max / 1e3)
-
-    # ---- per-phase device time (same calls with events between kernels)
-    phases = {}
-    for _ in range(args.steps):
-        _, _, ph = pbit.sort_list(keys, nxt, head, digit_bits=K, out_next=out, timing=True)
-        for k_, v in ph.items():
-            phases[k_] = phases.get(k_, 0.0) + v
     phases = {k_: v / args.steps for k_, v in phases.items()}
     launches = int(phases.pop("launches"))
     passes_run = int(phases.pop("passes_run"))
@@ -375,10 +378,25 @@ def run_ours(args):
                 "phase_ms": {k_: round(v, 4) for k_, v in phases.items()},
                 "whole_call_impl_bytes_per_node": total_alg,
                 "whole_call_method_frac": round(method_bytes_per_node(kb) * n / (ms / 1e3) / 1e9 / peak, 4)}
+    if dom == "walk":
+        # the walk visits every node once in list order = one random 128 B line per node
+        # (tools/micro/randread.cu); its ceiling is the measured random-line rate
+        roofline["walk_random_lines_per_s"] = round(n / (dom_ms / 1e3) / 1e9, 2)
+        roofline["walk_random_line_ceiling_per_s"] = WALK_LINE_CEILING_G
+        roofline["walk_frac_of_random_line_ceiling"] = round(n / (dom_ms / 1e3) / 1e9 / WALK_LINE_CEILING_G, 4)
+    whole = None
+    if tr:
+        # SURVEY Q16 reading of the north star's HBM gate: DRAM bytes of one whole call
+        # (ncu, summed over its launches) / device time of the call
+        dram = sum(v for k_, v in tr.items() if not k_.startswith("_"))
+        whole = {"dram_bytes_per_call": dram, "ms": round(ms, 4), "gbs": round(dram / (ms / 1e3) / 1e9, 1),
+                 "frac_of_peak": round(dram / (ms / 1e3) / 1e9 / peak, 4),
+                 "frac_of_nominal_8tbs": round(dram / (ms / 1e3) / 1e9 / 8000.0, 4),
+                 "source": tr.get("_source")}
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args.config, min(n, args.cpu_sample))
+        cpu = cpu_baseline(args.config, min(n, args.cpu_sample), args.cpu_reps)
 
     clocks = clk.summary()
     if rank == 0:
@@ -391,7 +409,7 @@ def run_ours(args):
                            "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6
                            else "inputs smaller than L2"},
                 "hbm_gbs_method": round(method_bytes_per_node(kb) * n * ws / (ms_max / 1e3) / 1e9, 1),
-                "roofline": roofline, "cpu_baseline": cpu,
+                "roofline": roofline, "whole_call_dram": whole, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (kb // 8 + 4),
                         "d2h_bytes_per_step": n * 4 + 4},
                 "gpu_launches": launches * args.steps, "clocks": clocks}
@@ -409,7 +427,8 @@ def main():
     ap.add_argument("--config", default="C3")
     ap.add_argument("--n", type=int, default=None, help="override n (default: the config's)")
     ap.add_argument("--digit-bits", type=int, default=0)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 22)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24)
+    ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--ref-sample", type=int, default=1 << 21)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -15,6 +15,8 @@
 #pragma once
 #include "common.cuh"
 
+#include <type_traits>
+
 namespace pbit {
 
 constexpr int PACK_THREADS = 256;
@@ -25,6 +27,17 @@ constexpr int WALK_THREADS = 256;
 constexpr int WALK_FLUSH_BYTES = PBIT_WALK_FLUSH;  // walk record stores per group
 constexpr int SWEEP_THREADS = 512;  // 16 warps x 16 items: 8192-item tiles halve the lookback traffic
 constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
+#ifndef PBIT_SWEEP_IPT
+#define PBIT_SWEEP_IPT 16
+#endif
+#ifndef PBIT_WCNT32
+#define PBIT_WCNT32 0
+#endif
+constexpr int SWEEP_IPT32 = PBIT_SWEEP_IPT;                       // items per thread, keys <= 32 bits
+constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT == 16 ? 12 : PBIT_SWEEP_IPT * 3 / 4 + 1;  // 64-bit keys
+// per-warp digit counters of the pass ranking: u32 (one word per digit: no two digits
+// share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
+using WCnt = std::conditional_t<PBIT_WCNT32 != 0, uint32_t, uint16_t>;
 
 // ============================================================================ a1/a2: pack
 // Reads key[v], next[v] (streaming, coalesced), writes the AoS record kn[v], and counts
@@ -345,7 +358,7 @@ struct SweepSmem {
   KeyT k[TILE];            // input keys, later the staged output keys
   uint32_t iin[TILE];      // input ids
   uint32_t iout[TILE];     // staged output ids
-  uint16_t wcnt[SWEEP_WARPS][RADIX];
+  WCnt wcnt[SWEEP_WARPS][RADIX];
   uint32_t dstart[RADIX];
   uint32_t goff[RADIX];
   uint32_t scan[SWEEP_WARPS];
@@ -364,24 +377,29 @@ __device__ __forceinline__ void bulk_g2s(void* smem_dst, const void* gsrc, uint3
 // Every lane adds 1 to a warp-private counter chosen by a hashed digit; the result must
 // equal (value before the instruction) + (number of lower lanes with the same digit).
 static __global__ void k_selftest_atomic_order(uint32_t iters, uint32_t* bad) {
-  __shared__ uint32_t cnt[SWEEP_WARPS][128];
+  __shared__ WCnt cnt[SWEEP_WARPS][256];
   const uint32_t lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int i = threadIdx.x; i < SWEEP_WARPS * 128; i += blockDim.x) (&cnt[0][0])[i] = 0;
+  for (int i = threadIdx.x; i < SWEEP_WARPS * 256; i += blockDim.x) (&cnt[0][0])[i] = 0;
   __syncthreads();
   uint32_t x = ruler_hash(threadIdx.x * 7919u + blockIdx.x * 977u), nb = 0;
   for (uint32_t i = 0; i < iters; ++i) {
     x = ruler_hash(x + i);
     const uint32_t nbins = 2u << (i & 7);  // 2 .. 256 digit values
     const uint32_t d = x & (nbins - 1);
-    const uint32_t sh = (d & 1u) << 4;
-    const uint32_t old = (atomicAdd(&cnt[w][d >> 1], 1u << sh) >> sh) & 0xFFFFu;
+    uint32_t old;
+    if constexpr (sizeof(WCnt) == 4) {
+      old = atomicAdd(reinterpret_cast<uint32_t*>(&cnt[w][d]), 1u);
+    } else {
+      const uint32_t sh = (d & 1u) << 4;
+      old = (atomicAdd(reinterpret_cast<uint32_t*>(&cnt[w][0]) + (d >> 1), 1u << sh) >> sh) & 0xFFFFu;
+    }
     const uint32_t peers = warp_peers<8>(d, 0xffffffffu);
     const int leader = __ffs(peers) - 1;
     const uint32_t base = __shfl_sync(0xffffffffu, old, leader);
     nb += old != base + __popc(peers & lanemask_lt());
-    if ((i & 63) == 63) {  // keep the u16 halves from overflowing
+    if ((i & 63) == 63) {  // keep the counters from overflowing
       __syncwarp();
-      for (int j = lane; j < 128; j += 32) cnt[w][j] = 0;
+      for (int j = lane; j < 256; j += 32) cnt[w][j] = 0;
       __syncwarp();
     }
   }
@@ -424,7 +442,7 @@ enum : int { RANK_BALLOT = 0, RANK_MATCH = 1, RANK_ATOMIC = 2 };
 // rd[i] = rank | digit << 16.  FULL: every item is valid (all tiles but the last).
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK, bool FULL>
 __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd)[IPT], int shift,
-                                           uint16_t* __restrict__ wrow, uint32_t wofs, uint32_t lane,
+                                           WCnt* __restrict__ wrow, uint32_t wofs, uint32_t lane,
                                            uint32_t tile_count) {
   constexpr int RADIX = 1 << RADIX_BITS;
 #pragma unroll
@@ -432,19 +450,22 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
     const bool valid = FULL || (wofs + i * 32 + lane < tile_count);
     const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
     if constexpr (RANK == RANK_ATOMIC) {
-      // One shared atomic per item on the warp's private counters (two u16 per word).
+      // One shared atomic per item on the warp's private counters.
       // Conflicting lanes of one ATOMS are served in ascending lane order on sm_100a --
       // measured, not documented: checked at load time by k_selftest_atomic_order
       // (pbit.cu), which falls back to RANK_BALLOT if it ever fails.  A warp whose items
       // share one digit (equal-key runs) lets lane 0 add 32 instead of serialising.
       const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
       const bool uni = __all_sync(0xffffffffu, d == d0 && valid);
-      const uint32_t sh = (d & 1u) << 4;
       const uint32_t add = uni ? (lane == 0 ? 32u : 0u) : (valid ? 1u : 0u);
-      uint32_t old = 0;
-      uint32_t* wc = reinterpret_cast<uint32_t*>(wrow) + (d >> 1);
-      if (add) old = atomicAdd(wc, add << sh);
-      uint32_t r = (old >> sh) & 0xFFFFu;
+      uint32_t r = 0;
+      if constexpr (sizeof(WCnt) == 4) {
+        if (add) r = atomicAdd(reinterpret_cast<uint32_t*>(wrow + d), add);
+      } else {  // two u16 counters per word
+        const uint32_t sh = (d & 1u) << 4;
+        uint32_t* wc = reinterpret_cast<uint32_t*>(wrow) + (d >> 1);
+        if (add) r = (atomicAdd(wc, add << sh) >> sh) & 0xFFFFu;
+      }
       const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0);
       r = uni ? r0 + lane : r;
       rd[i] = r | (d << 16);
@@ -457,7 +478,7 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
       uint32_t before = 0;
       if (valid && lane == (uint32_t)leader) {
         before = wrow[d];
-        wrow[d] = (uint16_t)(before + __popc(peers));
+        wrow[d] = (WCnt)(before + __popc(peers));
       }
       before = __shfl_sync(0xffffffffu, before, leader);
       rd[i] = (before + __popc(peers & lanemask_lt())) | (d << 16);
@@ -566,7 +587,8 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     bulk_g2s(sm.k, kin + tile_base, kb, &sm.mbar);
     bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
   }
-  for (uint32_t i = t; i < SWEEP_WARPS * RADIX / 2; i += SWEEP_THREADS) reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
+  for (uint32_t i = t; i < SWEEP_WARPS * RADIX * sizeof(WCnt) / 4; i += SWEEP_THREADS)
+    reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
   if (!GATHER) {
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     uint32_t done = 0;
@@ -593,7 +615,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 #pragma unroll
     for (int ww = 0; ww < SWEEP_WARPS; ++ww) {
       const uint32_t c = sm.wcnt[ww][t];
-      sm.wcnt[ww][t] = (uint16_t)total;
+      sm.wcnt[ww][t] = (WCnt)total;
       total += c;
     }
     if (tile > 0) st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (1ull << 32) | total);
@@ -614,7 +636,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
       const uint32_t ds = x - total + add;
       sm.dstart[t] = ds;
 #pragma unroll
-      for (int ww = 0; ww < SWEEP_WARPS; ++ww) sm.wcnt[ww][t] = (uint16_t)(sm.wcnt[ww][t] + ds);
+      for (int ww = 0; ww < SWEEP_WARPS; ++ww) sm.wcnt[ww][t] = (WCnt)(sm.wcnt[ww][t] + ds);
     }
   }
   __syncthreads();

@@ -36,7 +36,7 @@ template <int KB, int RB>
 static void launch_key_passes(SweepArgs a, const Plan& plan, bool keep_keys, cudaStream_t st, cudaEvent_t* ev,
                               int ev_base, bool gather_first) {
   using KeyT = typename KeyOf<KB>::T;
-  constexpr int IPT = (KB == 8) ? 12 : 16;
+  constexpr int IPT = (KB == 8) ? SWEEP_IPT64 : SWEEP_IPT32;
   for (uint32_t s = 0; s < plan.npasses; ++s) {
     a.slot = (int)s;
     a.digit = (int)plan.digit[s];

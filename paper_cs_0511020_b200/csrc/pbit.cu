@@ -122,7 +122,7 @@ void init_rank_mode(cudaStream_t st) {
   g_rank_mode.store(mode);
 }
 
-size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64 ? 12 : 16); }
+size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64 ? SWEEP_IPT64 : SWEEP_IPT32); }
 
 // Workspace layout (all 256-byte aligned).
 struct Ws {
@@ -192,10 +192,19 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (cudaMallocAsync((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   carve(p, base, &w);
 
-  cudaEvent_t ev[PBIT_NUM_PHASES + 1];
+  // phase events come from a per-thread pool (created once), so timed calls carry no
+  // event creation on the host between kernels
+  static thread_local cudaEvent_t ev_pool[64][PBIT_NUM_PHASES + 1];
+  static thread_local bool ev_ready[64] = {};
   const bool timing = phase_ms != nullptr;
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  cudaEvent_t* ev = ev_pool[cur_dev & 63];
   if (timing) {
-    for (int i = 0; i <= PBIT_NUM_PHASES; ++i) cudaEventCreate(&ev[i]);
+    if (!ev_ready[cur_dev & 63]) {
+      for (int i = 0; i <= PBIT_NUM_PHASES; ++i) cudaEventCreate(&ev[i]);
+      ev_ready[cur_dev & 63] = true;
+    }
     cudaEventRecord(ev[PBIT_NUM_PHASES], st);  // start
   }
   const uint32_t n = p.n;
@@ -335,7 +344,6 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
       for (int s = 0; s < p.D; ++s) { phase_ms[PBIT_PHASE_PASS0 + s] = el_ms(a, ev[PBIT_PHASE_PASS0 + s]); a = ev[PBIT_PHASE_PASS0 + s]; }
       phase_ms[PBIT_PHASE_RELINK] = el_ms(a, ev[PBIT_PHASE_RELINK]);
     }
-    for (int i = 0; i <= PBIT_NUM_PHASES; ++i) cudaEventDestroy(ev[i]);
   }
   if (rc) return rc;
   if (res.err) return PBIT_ERR_INVALID_LIST;

@@ -12,7 +12,7 @@ $cmd > $out/plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     --csv --log-file $out/launches.csv $cmd > $out/ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on \
-    -k regex:"k_pack|k_walk|k_gather|k_onesweep|k_relink_apply|k_rank_walk" -c 12 \
+    -k regex:"k_pack|k_walk|k_gather|k_onesweep|k_relink_part|k_relink_apply|k_rank_walk" -c 14 \
     -o $out/full $cmd > $out/ncu_full.log 2>&1
 ncu -i $out/full.ncu-rep --page raw --csv > $out/full_raw.csv 2>/dev/null
 ncu -i $out/full.ncu-rep --page details > $out/full_details.txt 2>/dev/null
