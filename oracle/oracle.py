@@ -59,6 +59,10 @@ def _load():
             lib.oracle_pbit_sort.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32,
                                              ctypes.c_uint64, ctypes.c_uint, ctypes.c_int, u32p,
                                              ctypes.c_void_p, ctypes.POINTER(Counters)]
+            lib.oracle_pbit_sort_kind.restype = ctypes.c_int
+            lib.oracle_pbit_sort_kind.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32,
+                                                  ctypes.c_uint64, ctypes.c_uint, ctypes.c_int, ctypes.c_int, u32p,
+                                                  ctypes.c_void_p, ctypes.POINTER(Counters)]
             lib.oracle_split_once.restype = ctypes.c_int
             lib.oracle_split_once.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32,
                                               ctypes.c_uint64, ctypes.c_uint, ctypes.c_void_p]
@@ -81,14 +85,21 @@ def _keys(keys, key_bits):
     if want is None:  # let the C side reject the width (ORACLE_ERR_ARG)
         return k
     if k.dtype != want:
-        k = k.astype(want)
+        # same-width signed / float keys: pass the bit patterns unchanged
+        k = k.view(want) if k.dtype.itemsize * 8 == key_bits else k.astype(want)
     return k
 
 
+KINDS = {"unsigned": 0, "signed": 1, "float": 2}
+
+
 def pbit_sort(keys, next_, head: int, key_bits: int, K: int = 4, descending: bool = False,
-              with_counters: bool = False, out=None):
+              with_counters: bool = False, out=None, kind: str = "unsigned"):
     """Return (out_head, out_next[, counters]) of the paper-literal Pbit sort.
-    ``out`` (uint32, contiguous) may be ``next_`` itself: the sort relinks in situ."""
+    ``out`` (uint32, contiguous) may be ``next_`` itself: the sort relinks in situ.
+    ``kind``: "unsigned", "signed" (the dispatcher P:444-466, reading Q13) or
+    "float" (IEEE 754 binary16/32/64 by key_bits: mantissa then characteristic, P:1190,
+    reading Q18).  Keys are passed as their bit patterns (any dtype of key_bits width)."""
     lib = _load()
     nxt = np.ascontiguousarray(next_, dtype=np.uint32)
     n = int(nxt.shape[0])
@@ -99,8 +110,9 @@ def pbit_sort(keys, next_, head: int, key_bits: int, K: int = 4, descending: boo
         assert out.dtype == np.uint32 and out.flags.c_contiguous and out.shape[0] >= n
     oh = ctypes.c_uint32(0)
     c = Counters()
-    rc = lib.oracle_pbit_sort(k.ctypes.data, key_bits, nxt.ctypes.data if n else None, head & 0xFFFFFFFF,
-                              n, K, int(descending), ctypes.byref(oh), out.ctypes.data, ctypes.byref(c))
+    rc = lib.oracle_pbit_sort_kind(k.ctypes.data, key_bits, nxt.ctypes.data if n else None, head & 0xFFFFFFFF,
+                                   n, K, KINDS[kind], int(descending), ctypes.byref(oh), out.ctypes.data,
+                                   ctypes.byref(c))
     if rc:
         raise OracleError(rc)
     res = (int(oh.value), out[:n])

@@ -45,20 +45,25 @@ typedef struct {
     unsigned K;              /* pattern length                                      */
     uint32_t omega;          /* Omega = 2^K                                            */
     int descending;          /* 0: ascending loops P:379-380; 1: descending loops P:371-372    */
+    unsigned fshift;         /* the sorted field: (key >> fshift) & fmask (0 / all ones for a  */
+    uint64_t fmask;          /*   whole integer key; the mantissa or characteristic)  */
     uint32_t *tabs;          /* (M/K) root tables of Omega slots, one per recursion level     */
     uint32_t depth, live;
     oracle_counters c;
 } ctx_t;
 
-/* The key of node v as an unsigned integer (the paper's L->data). */
+/* The key of node v as an unsigned integer (the paper's L->data), restricted to
+ * the field being sorted (the whole key unless a float field is sorted). */
 static uint64_t key_of(const ctx_t *x, uint32_t v) {
     const uint8_t *p = x->key + (size_t)v * (size_t)x->key_bytes;
+    uint64_t k;
     switch (x->key_bytes) {
-    case 1: return p[0];
-    case 2: { uint16_t k; memcpy(&k, p, 2); return k; }
-    case 4: { uint32_t k; memcpy(&k, p, 4); return k; }
-    default: { uint64_t k; memcpy(&k, p, 8); return k; }
+    case 1: k = p[0]; break;
+    case 2: { uint16_t t; memcpy(&t, p, 2); k = t; break; }
+    case 4: { uint32_t t; memcpy(&t, p, 4); k = t; break; }
+    default: { uint64_t t; memcpy(&t, p, 8); k = t; break; }
     }
+    return (k >> x->fshift) & x->fmask;
 }
 
 /* bits(number, M) = (number div 2^M) mod Omega, written in C as
@@ -158,6 +163,8 @@ int oracle_pbit_sort(const void *keys, int key_bits, const uint32_t *next, uint3
     x.K = K;
     x.omega = 1u << K;
     x.descending = descending;
+    x.fshift = 0;
+    x.fmask = ~(uint64_t)0;
     unsigned levels = (unsigned)key_bits / K;
     x.tabs = (uint32_t *)malloc((size_t)levels * x.omega * sizeof(uint32_t));
     if (!x.tabs) return ORACLE_ERR_OOM;
@@ -166,6 +173,114 @@ int oracle_pbit_sort(const void *keys, int key_bits, const uint32_t *next, uint3
 
     *out_head = Pbit(&x, head, (unsigned)key_bits, ORACLE_NULL, 0);
 
+    free(x.tabs);
+    if (counters) *counters = x.c;
+    return ORACLE_OK;
+}
+
+/* ---------------------------------------------------------------- key kinds
+ * kind 0: unsigned (above).  kind 1: signed two's complement integers, the dispatcher of
+ * P:444-466.  kind 2: IEEE 754 floats (binary16/32/64 by key_bits).
+ *
+ * Reading Q13: the dispatcher's sign split pushes nodes to the
+ * FRONT of L_negative / L_unsigned, which reverses equal keys once more than the even
+ * number of Pbit levels restores, so the literal listing is reverse-stable.  The oracle
+ * splits by appending at the tails instead (SPEC S:201 makes the same decision); the
+ * split itself is otherwise the listing's (temp->data < 0 <=> sign bit set).
+ *
+ * Reading Q18: floats.  The paper sorts "in relation to mantissa first, and then once
+ * more in relation to its characteristic. Such sorting is correct because Pbit is
+ * stable" with the IEEE layouts of P:1196-1199, and says nothing about the
+ * sign.  The oracle splits by the sign bit as the integer dispatcher does, sorts the
+ * non-negative list by mantissa then by characteristic (ascending), and the negative
+ * list by mantissa then characteristic in the descending direction (larger magnitude =
+ * smaller number), negatives first.  Each field is padded to a multiple of 2K bits so
+ * that M/K is even (reading Q1).  The resulting order is sign-magnitude order of the
+ * bit patterns: -0.0 before +0.0, NaNs outside the infinities (IEEE 754 totalOrder). */
+
+/* Append every node of the list (head, next) to the tail of one of two lists by the sign
+ * bit of its key; returns the two heads (order inside each list = input order). */
+static void split_sign(ctx_t *x, uint32_t head, int sign_bit, uint32_t *neg, uint32_t *nonneg) {
+    uint32_t nh = ORACLE_NULL, nt = ORACLE_NULL, ph = ORACLE_NULL, pt = ORACLE_NULL;
+    unsigned fs = x->fshift; uint64_t fm = x->fmask;
+    x->fshift = 0; x->fmask = ~(uint64_t)0;
+    for (uint32_t temp; (temp = head) != ORACLE_NULL; ) {
+        head = x->next[head];
+        x->next[temp] = ORACLE_NULL;
+        if ((key_of(x, temp) >> sign_bit) & 1u) {                    /* temp->data < 0 */
+            if (nt == ORACLE_NULL) nh = temp; else x->next[nt] = temp;
+            nt = temp;
+        } else {
+            if (pt == ORACLE_NULL) ph = temp; else x->next[pt] = temp;
+            pt = temp;
+        }
+    }
+    x->fshift = fs; x->fmask = fm;
+    *neg = nh; *nonneg = ph;
+}
+
+/* Pbit over one field of the keys: sorts the list L by (key >> shift) & (2^width - 1),
+ * padded to M = a multiple of 2K bits, in the given direction, in front of end marker P. */
+static uint32_t pbit_field(ctx_t *x, uint32_t L, unsigned shift, unsigned width, int desc, uint32_t P) {
+    unsigned M = (width + 2 * x->K - 1) / (2 * x->K) * (2 * x->K);
+    x->fshift = shift;
+    x->fmask = width >= 64 ? ~(uint64_t)0 : (((uint64_t)1 << width) - 1);
+    x->descending = desc;
+    return Pbit(x, L, M, P, 0);
+}
+
+int oracle_pbit_sort_kind(const void *keys, int key_bits, const uint32_t *next, uint32_t head,
+                          uint64_t n, unsigned K, int kind, int descending,
+                          uint32_t *out_head, uint32_t *out_next, oracle_counters *counters) {
+    if (kind == 0)
+        return oracle_pbit_sort(keys, key_bits, next, head, n, K, descending, out_head, out_next, counters);
+    if (!out_head || (n && (!keys || !next || !out_next))) return ORACLE_ERR_ARG;
+    if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return ORACLE_ERR_ARG;
+    if (K < 1 || K > 16 || kind < 0 || kind > 2) return ORACLE_ERR_ARG;
+    if (kind == 1 && (key_bits % K) != 0) return ORACLE_ERR_ARG;        /* reading Q7 */
+    if (kind == 2 && key_bits == 8) return ORACLE_ERR_ARG;              /* no 8-bit IEEE format */
+    if (n > 0xFFFFFFFFull) return ORACLE_ERR_ARG;
+    int rc = oracle_validate_list(next, head, n);
+    if (rc) return rc;
+
+    ctx_t x;
+    memset(&x, 0, sizeof x);
+    x.key = (const uint8_t *)keys;
+    x.key_bytes = key_bits / 8;
+    x.K = K;
+    x.omega = 1u << K;
+    x.fmask = ~(uint64_t)0;
+    unsigned levels = ((unsigned)key_bits + 2 * K - 1) / K + 2;
+    x.tabs = (uint32_t *)malloc((size_t)levels * x.omega * sizeof(uint32_t));
+    if (!x.tabs) return ORACLE_ERR_OOM;
+    if (out_next != next && n) memcpy(out_next, next, (size_t)n * sizeof(uint32_t));
+    x.next = out_next;
+    const int sign_bit = key_bits - 1;
+    uint32_t neg, nonneg;
+    split_sign(&x, head, sign_bit, &neg, &nonneg);                     /* P:450-455 (tail append) */
+    const unsigned size = (unsigned)key_bits;
+    if (kind == 1) {
+        if (descending)   /* Pbit_decreasing(L_unsigned, size, Pbit_decreasing(L_negative, size)) */
+            *out_head = pbit_field(&x, nonneg, 0, size, 1, pbit_field(&x, neg, 0, size, 1, ORACLE_NULL));
+        else              /* Pbit_ascending(L_negative, size, Pbit_ascending(L_unsigned, size)) */
+            *out_head = pbit_field(&x, neg, 0, size, 0, pbit_field(&x, nonneg, 0, size, 0, ORACLE_NULL));
+    } else {
+        /* IEEE 754 layouts: mantissa m bits, characteristic c bits */
+        const unsigned m = key_bits == 16 ? 10 : key_bits == 32 ? 23 : 52;
+        const unsigned c = key_bits == 16 ? 5 : key_bits == 32 ? 8 : 11;
+        /* "sort the number in relation to mantissa first, and then once more in relation
+         * to its characteristic"; the sign list order: see reading Q18 above */
+        const int d_nonneg = descending ? 1 : 0, d_neg = descending ? 0 : 1;
+        uint32_t a = pbit_field(&x, nonneg, 0, m, d_nonneg, ORACLE_NULL);
+        uint32_t b = pbit_field(&x, neg, 0, m, d_neg, ORACLE_NULL);
+        if (descending) {   /* non-negatives (largest first), then negatives */
+            uint32_t tail = pbit_field(&x, b, m, c, d_neg, ORACLE_NULL);
+            *out_head = pbit_field(&x, a, m, c, d_nonneg, tail);
+        } else {            /* negatives (most negative first), then non-negatives */
+            uint32_t tail = pbit_field(&x, a, m, c, d_nonneg, ORACLE_NULL);
+            *out_head = pbit_field(&x, b, m, c, d_neg, tail);
+        }
+    }
     free(x.tabs);
     if (counters) *counters = x.c;
     return ORACLE_OK;
@@ -183,6 +298,7 @@ int oracle_split_once(const void *keys, int key_bits, uint32_t *next, uint32_t h
     ctx_t x;
     memset(&x, 0, sizeof x);
     x.key = (const uint8_t *)keys; x.key_bytes = key_bits / 8; x.K = K; x.omega = 1u << K;
+    x.fmask = ~(uint64_t)0;
     x.next = next;
     unsigned M = (unsigned)key_bits - K;
     for (uint32_t b = 0; b < x.omega; ++b) tab[b] = ORACLE_NULL;

@@ -216,3 +216,179 @@ def test_in_place_alias():
     h, out = oracle.pbit_sort(keys, nxt, li.head, 32, 4, out=nxt)
     eh, eo = expected_by_definition(keys, li.order.numpy())
     assert h == eh and np.array_equal(nxt, eo) and np.shares_memory(out, nxt)
+
+
+# ---------------------------------------------------------------- key kinds (NEXT row N1)
+KINDS_GOLDEN = os.path.join(os.path.dirname(__file__), "golden", "key_kinds.txt")
+
+
+def _kinds_golden():
+    d = {}
+    for line in open(KINDS_GOLDEN):
+        line = line.strip()
+        if line and not line.startswith("#"):
+            k, v = line.split(None, 1)
+            d[k] = v
+    return d
+
+
+def test_worked_example_descending():
+    g = _kinds_golden()
+    keys = np.array([int(x) for x in g["desc_input"].split()], np.uint8)
+    nxt, head = _chain(keys)
+    h, out = oracle.pbit_sort(keys, nxt, head, 8, 4, descending=True)
+    seq = walk(out, h)
+    assert [int(keys[v]) for v in seq] == [int(x) for x in g["desc_output"].split()]
+    val, pos = g["desc_equal_key_positions"].split(":")
+    assert [v for v in seq if keys[v] == int(val)] == [int(p) for p in pos.split(",")]
+
+
+def test_signed_example():
+    g = _kinds_golden()
+    keys = np.array([int(x) for x in g["signed_input"].split()], np.int32)
+    nxt, head = _chain(keys)
+    h, out = oracle.pbit_sort(keys, nxt, head, 32, 4, kind="signed")
+    assert [int(keys[v]) for v in walk(out, h)] == [int(x) for x in g["signed_output"].split()]
+
+
+def test_float_example():
+    g = _kinds_golden()
+    keys = np.array([float(x) for x in g["float_input"].split()], np.float32)
+    nxt, head = _chain(keys)
+    h, out = oracle.pbit_sort(keys, nxt, head, 32, 4, kind="float")
+    assert [float(keys[v]) for v in walk(out, h)] == [float(x) for x in g["float_output"].split()]
+
+
+SIGNED_ALPHABETS = {8: [-128, -1, 0, 1, 127, -16], 16: [-32768, -256, -1, 0, 255, 32767],
+                    32: [-2**31, -1, 0, 1, 2**31 - 1, -65536], 64: [-2**63, -1, 0, 2**63 - 1, -2**32]}
+INT_DT = {8: np.int8, 16: np.int16, 32: np.int32, 64: np.int64}
+FLOAT_DT = {16: np.float16, 32: np.float32, 64: np.float64}
+
+
+def _float_key(x):
+    """Order of the plain definition for floats without NaN: numeric, -0.0 before +0.0."""
+    return (float(x), 0 if np.signbit(x) else 1)
+
+
+@pytest.mark.parametrize("key_bits", [8, 16, 32, 64])
+@pytest.mark.parametrize("descending", [False, True])
+def test_signed_brute_force_all_link_orders(key_bits, descending):
+    """Every link order of n <= 5 over an adversarial signed alphabet vs python's stable
+    sorted() of the list-order sequence by the signed value (reverse=True keeps equal keys
+    in input order)."""
+    alpha = SIGNED_ALPHABETS[key_bits]
+    rng = np.random.default_rng(key_bits)
+    for n in range(0, 6):
+        keys = np.array(rng.choice(alpha, size=n), dtype=INT_DT[key_bits])
+        for perm in itertools.permutations(range(n)):
+            nxt = np.full(n, NULL, np.uint32)
+            for a, b in zip(perm, perm[1:]):
+                nxt[a] = b
+            head = perm[0] if n else NULL
+            h, out = oracle.pbit_sort(keys, nxt, head, key_bits, 4, descending=descending, kind="signed")
+            want = sorted(list(perm), key=lambda v: int(keys[v]), reverse=descending)
+            assert walk(out, h) == want
+
+
+@pytest.mark.parametrize("key_bits", [16, 32, 64])
+@pytest.mark.parametrize("descending", [False, True])
+def test_float_brute_force_all_link_orders(key_bits, descending):
+    alpha = [-np.inf, -2.5, -1.0, -0.0, 0.0, 1.5, 2.5, np.inf, 6e-5, -6e-5]
+    rng = np.random.default_rng(100 + key_bits)
+    for n in range(0, 6):
+        keys = np.array(rng.choice(alpha, size=n), dtype=FLOAT_DT[key_bits])
+        for perm in itertools.permutations(range(n)):
+            nxt = np.full(n, NULL, np.uint32)
+            for a, b in zip(perm, perm[1:]):
+                nxt[a] = b
+            head = perm[0] if n else NULL
+            h, out = oracle.pbit_sort(keys, nxt, head, key_bits, 4, descending=descending, kind="float")
+            want = sorted(list(perm), key=lambda v: _float_key(keys[v]), reverse=descending)
+            assert walk(out, h) == want
+
+
+@pytest.mark.parametrize("key_bits", [16, 32, 64])
+def test_float_random_vs_numpy_stable(key_bits):
+    """Seeded random lists (no NaN, no -0.0) vs numpy's stable argsort of the values."""
+    rng = np.random.default_rng(7 + key_bits)
+    for n in [1, 2, 17, 1000, 4099]:
+        vals = rng.normal(0, 100, n) * rng.choice([1e-3, 1, 1e3], n)
+        vals = np.round(np.clip(vals, -6e4, 6e4), 1).astype(FLOAT_DT[key_bits])  # duplicates; f16 range
+        vals[vals == 0] = 0.0
+        order = rng.permutation(n)
+        nxt = np.full(n, NULL, np.uint32)
+        nxt[order[:-1]] = order[1:]
+        for desc in (False, True):
+            h, out = oracle.pbit_sort(vals, nxt, int(order[0]), key_bits, 4, descending=desc, kind="float")
+            wh, wn = expected_by_definition(vals.astype(np.float64), order, descending=desc)
+            assert h == wh and np.array_equal(out, wn)
+
+
+def test_float_nan_and_signed_zero_total_order():
+    """Reading Q18: sign-magnitude order of the bit patterns (IEEE 754 totalOrder):
+    -NaN < -inf < ... < -0.0 < +0.0 < ... < +inf < +NaN, NaNs by payload."""
+    bits = np.array([0x7FC00001, 0x3F800000, 0xFFC00001, 0xFF800000, 0x7FC00002, 0x00000000, 0x80000000,
+                     0x7F800000], np.uint32)
+    # the same values listed in totalOrder (derived from IEEE 754-2008 section 5.10)
+    want_bits = [0xFFC00001, 0xFF800000, 0x80000000, 0x00000000, 0x3F800000, 0x7F800000, 0x7FC00001, 0x7FC00002]
+    nxt, head = _chain(bits)
+    h, out = oracle.pbit_sort(bits, nxt, head, 32, 4, kind="float")
+    assert [int(bits[v]) for v in walk(out, h)] == want_bits
+    h, out = oracle.pbit_sort(bits, nxt, head, 32, 4, kind="float", descending=True)
+    assert [int(bits[v]) for v in walk(out, h)] == want_bits[::-1]
+
+
+@pytest.mark.parametrize("key_bits", [8, 32, 64])
+def test_signed_random_vs_numpy_stable(key_bits):
+    rng = np.random.default_rng(11 + key_bits)
+    info = np.iinfo(INT_DT[key_bits])
+    for n in [1, 3, 100, 4099]:
+        vals = rng.integers(info.min, info.max, n, dtype=INT_DT[key_bits], endpoint=True)
+        vals[rng.random(n) < 0.3] = vals[0]  # duplicates
+        order = rng.permutation(n)
+        nxt = np.full(n, NULL, np.uint32)
+        nxt[order[:-1]] = order[1:]
+        for desc in (False, True):
+            h, out = oracle.pbit_sort(vals, nxt, int(order[0]), key_bits, 4, descending=desc, kind="signed")
+            wh, wn = expected_by_definition(vals, order, descending=desc)
+            assert h == wh and np.array_equal(out, wn)
+
+
+def test_kind_counter_identities():
+    """relinks = n * (sum of the levels of every Pbit call a node goes through), merge
+    visits = n per call: signed = one call of M/K levels, float = a
+    mantissa call and a characteristic call (fields padded to a multiple of 2K bits)."""
+    rng = np.random.default_rng(3)
+    n = 777
+    order = rng.permutation(n)
+    nxt = np.full(n, NULL, np.uint32)
+    nxt[order[:-1]] = order[1:]
+    si = rng.integers(-1000, 1000, n).astype(np.int32)
+    _, _, c = oracle.pbit_sort(si, nxt, int(order[0]), 32, 4, kind="signed", with_counters=True)
+    assert c["relinks"] == n * 32 // 4 and c["merge_visits"] == n
+    fl = rng.normal(0, 1, n).astype(np.float32)
+    _, _, c = oracle.pbit_sort(fl, nxt, int(order[0]), 32, 4, kind="float", with_counters=True)
+    assert c["relinks"] == n * (24 // 4 + 8 // 4) and c["merge_visits"] == 2 * n
+    f64 = rng.normal(0, 1, n)
+    _, _, c = oracle.pbit_sort(f64, nxt, int(order[0]), 64, 4, kind="float", with_counters=True)
+    assert c["relinks"] == n * (56 // 4 + 16 // 4) and c["merge_visits"] == 2 * n
+
+
+def test_literal_signed_split_is_reverse_stable():
+    """Reading Q13 demonstrated: pushing to the FRONT of the sign lists (the listing,
+    P:450-455) and then sorting with the paper's even number of levels returns equal keys
+    in reverse input order -- which is why the oracle appends at the tails."""
+    keys = np.array([5, -2, 5, -2, 5], np.int32)
+    nxt, head = _chain(keys)
+    # push-front split by hand, then the oracle's unsigned ascending Pbit on each list
+    neg = [v for v in walk(nxt, head) if keys[v] < 0][::-1]
+    pos = [v for v in walk(nxt, head) if keys[v] >= 0][::-1]
+    seq = []
+    for part in (neg, pos):
+        sub_keys = keys[part].view(np.uint32)  # the sub-list as its own node array, in list order
+        sub_next, sub_head = _chain(sub_keys)
+        h, out = oracle.pbit_sort(sub_keys, sub_next, sub_head, 32, 4)
+        seq += [part[i] for i in walk(out, h)]
+    assert seq == [3, 1, 4, 2, 0]  # equal keys reversed: not stable
+    h, out = oracle.pbit_sort(keys, nxt, head, 32, 4, kind="signed")
+    assert walk(out, h) == [1, 3, 0, 2, 4]  # the oracle's reading: stable
