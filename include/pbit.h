@@ -20,7 +20,8 @@
  * sorted ascending and STABLY by unsigned key (equal keys keep input-list order,
  * P:4):  *out_head = w_0, out_next[w_i] = w_{i+1}, out_next[w_{n-1}] =
  * PBIT_NULL.  This result is unique, so every digit width K gives bit-identical
- * output.
+ * output.  pbit_opts.key_kind / .descending select signed or floating-point keys
+ * and the descending order, also stable.
  *
  * Ownership.  The caller owns every array.  The library allocates stream-ordered
  * workspace (cudaMallocAsync on the call's stream; memory returns to the device
@@ -32,8 +33,9 @@
  *
  * Errors.  Functions return a pbit_status and never throw or abort.
  *   PBIT_ERR_INVALID_ARG  null pointer; key_bits not in {8,16,32,64}; digit_bits out
- *                         of range; head >= n (n > 0); n > 2^32-1; pointers that mix
- *                         host and device memory.
+ *                         of range; key_kind not 0/1/2 or float keys of 8 bits;
+ *                         head >= n (n > 0); n > 2^32-1; pointers that mix host and
+ *                         device memory.
  *   PBIT_ERR_INVALID_LIST the input is not one NULL-terminated chain of exactly n
  *                         nodes starting at head (cycle, short chain, index >= n,
  *                         a node reached twice).  out_next is NOT modified (the check
@@ -86,7 +88,21 @@ typedef struct {
     uint32_t *passes_run; /* optional host out: number of radix passes executed (the
                         non-trivial digits; trivial ones are skipped)               */
     uint32_t *launches; /* optional host out: kernels this call launched            */
+    int key_kind;    /* how the key bits are ordered (NEXT row N1):
+                        PBIT_KEY_UNSIGNED (0, default) unsigned integers;
+                        PBIT_KEY_SIGNED   (1) two's complement integers, the dispatcher
+                                          of P:444-466 (stable: DESIGN.md reading Q13);
+                        PBIT_KEY_FLOAT    (2) IEEE 754 binary16/32/64 by key_bits (16,
+                                          32, 64; 8 is INVALID_ARG), ordered as the
+                                          paper's mantissa-then-characteristic passes
+                                          with a sign split give (reading
+                                          Q18): -NaN < -inf < .. < -0.0 < +0.0 < .. <
+                                          +inf < +NaN (IEEE totalOrder).            */
+    int descending;  /* 0 ascending, 1 descending; stable in
+                        both directions: equal keys keep input-list order.          */
 } pbit_opts;
+
+enum { PBIT_KEY_UNSIGNED = 0, PBIT_KEY_SIGNED = 1, PBIT_KEY_FLOAT = 2 };
 
 /*
  * pbit_sort_list -- stable ascending sort of one singly-linked list.

@@ -37,7 +37,11 @@ class PbitError(RuntimeError):
 class _Opts(ctypes.Structure):
     _fields_ = [("digit_bits", ctypes.c_int), ("stream", ctypes.c_void_p), ("validate", ctypes.c_int),
                 ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("passes_run", ctypes.POINTER(ctypes.c_uint32)),
-                ("launches", ctypes.POINTER(ctypes.c_uint32))]
+                ("launches", ctypes.POINTER(ctypes.c_uint32)), ("key_kind", ctypes.c_int),
+                ("descending", ctypes.c_int)]
+
+
+KEY_KINDS = {"unsigned": 0, "signed": 1, "float": 2}  # pbit.h PBIT_KEY_*
 
 
 def _load():
@@ -75,7 +79,8 @@ def _load():
 lib = _load()
 
 _KEY_BITS = {torch.uint8: 8, torch.int8: 8, torch.int16: 16, torch.uint16: 16, torch.int32: 32,
-             torch.uint32: 32, torch.int64: 64, torch.uint64: 64}
+             torch.uint32: 32, torch.int64: 64, torch.uint64: 64, torch.float16: 16, torch.bfloat16: 16,
+             torch.float32: 32, torch.float64: 64}
 
 
 def _errtext(rc: int) -> str:
@@ -93,9 +98,12 @@ def _ptr(t) -> int:
     return int(t.ctypes.data)  # numpy (host) array
 
 
-def _opts(digit_bits: int, stream, phase_ms, passes, launches=None):
+def _opts(digit_bits: int, stream, phase_ms, passes, launches=None, key_kind: str = "unsigned",
+          descending: bool = False):
     o = _Opts()
     o.launches = launches
+    o.key_kind = KEY_KINDS[key_kind]
+    o.descending = int(bool(descending))
     o.digit_bits = int(digit_bits)
     o.stream = ctypes.c_void_p(stream)
     o.validate = 1
@@ -111,13 +119,14 @@ def _stream_handle(stream, on_cuda: bool):
 
 
 def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: int = 0, out_next=None,
-              stream=None, timing: bool = False):
-    """Stable ascending sort of the list (head, next_) by keys; returns (head, out_next)
-    (plus a dict of device ms per phase when timing=True).
+              stream=None, timing: bool = False, key_kind: str = "unsigned", descending: bool = False):
+    """Stable sort of the list (head, next_) by keys; returns (head, out_next) (plus a
+    dict of device ms per phase when timing=True).
 
     keys / next_ / out_next: CUDA tensors on the current device, or host arrays (torch
     CPU tensors or numpy) -- then the library stages them through device memory.
-    next_ holds u32 ids (int32 view, NULL = -1 / 0xFFFFFFFF)."""
+    next_ holds u32 ids (int32 view, NULL = -1 / 0xFFFFFFFF).  key_kind: "unsigned",
+    "signed" or "float" (how the key bits order, pbit.h PBIT_KEY_*); descending: order."""
     if key_bits is None:
         key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
     n = int(next_.shape[0])
@@ -132,7 +141,8 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
     pm = (ctypes.c_float * NUM_PHASES)() if timing else None
     passes = ctypes.c_uint32(0)
     launches = ctypes.c_uint32(0)
-    o = _opts(digit_bits, _stream_handle(stream, on_cuda), pm, ctypes.pointer(passes), ctypes.pointer(launches))
+    o = _opts(digit_bits, _stream_handle(stream, on_cuda), pm, ctypes.pointer(passes), ctypes.pointer(launches),
+              key_kind, descending)
     rc = lib.pbit_sort_list(_ptr(keys) if n else None, _ptr(next_) if n else None, head & 0xFFFFFFFF, n, key_bits,
                             ctypes.byref(oh), _ptr(out_next) if n else None, ctypes.byref(o))
     if rc:
@@ -191,7 +201,8 @@ def mg_exchange_plan(nranks: int, rank: int, n: int, slice_: int, lt, le):
 
 
 def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int, comm: int,
-                 key_bits: int | None = None, digit_bits: int = 0, out_next_local=None, stream=None):
+                 key_bits: int | None = None, digit_bits: int = 0, out_next_local=None, stream=None,
+                 key_kind: str = "unsigned", descending: bool = False):
     """Sort one list sharded over the ranks of `comm` (see include/pbit.h).  Returns
     (head, out_next_local)."""
     if key_bits is None:
@@ -201,7 +212,7 @@ def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int,
         out_next_local = torch.empty_like(next_local)
     oh = ctypes.c_uint32(0)
     launches = ctypes.c_uint32(0)
-    o = _opts(digit_bits, _stream_handle(stream, True), None, None, ctypes.pointer(launches))
+    o = _opts(digit_bits, _stream_handle(stream, True), None, None, ctypes.pointer(launches), key_kind, descending)
     rc = lib.pbit_sort_list_mg(_ptr(keys_local) if n_local else None, _ptr(next_local) if n_local else None,
                                head & 0xFFFFFFFF, n_global, node_lo, n_local, key_bits, ctypes.byref(oh),
                                _ptr(out_next_local) if n_local else None, ctypes.c_void_p(comm), ctypes.byref(o))

@@ -39,6 +39,30 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT == 16 ? 12 : PBIT_SWEEP_IPT * 3 / 4 +
 // share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
 using WCnt = std::conditional_t<PBIT_WCNT32 != 0, uint32_t, uint16_t>;
 
+// ============================================================================ key order
+// Order-preserving map of a key's bits to the unsigned integer the passes sort by
+// (NEXT row N1).  Applied once, in the pack: every later kernel sees sort keys only,
+// and nothing maps them back (the output is the relinked list, not the keys).
+//   signed   flip the sign bit: two's complement order = unsigned order
+//   float    sign bit set: flip all bits; else set the sign bit -- sign-magnitude order
+//            of the bit patterns, the order of the paper's sign split + mantissa-then-
+//            characteristic passes (reading Q18)
+//   descending  complement the result: a stable ascending sort of ~k is the stable
+//            descending sort of k (equal keys keep input order)
+struct KeyMap {
+  int kind;        // PBIT_KEY_UNSIGNED / SIGNED / FLOAT
+  int descending;
+  __host__ __device__ __forceinline__ unsigned long long operator()(unsigned long long k, int bits) const {
+    const unsigned long long all = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+    const unsigned long long sign = 1ull << (bits - 1);
+    if (kind == 1) k ^= sign;
+    else if (kind == 2) k = (k & sign) ? (~k & all) : (k | sign);
+    if (descending) k = ~k & all;
+    return k;
+  }
+  __host__ __device__ __forceinline__ bool identity() const { return kind == 0 && !descending; }
+};
+
 // ============================================================================ a1/a2: pack
 // Reads key[v], next[v] (streaming, coalesced), writes the AoS record kn[v], and counts
 // every digit of every key into a per-CTA smem histogram (flushed once per CTA).
@@ -46,7 +70,7 @@ template <int KB>
 __global__ void __launch_bounds__(PACK_THREADS)
 k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_t n, uint32_t n_ids,
        typename Rec<KB>::T* __restrict__ kn, uint32_t* __restrict__ hist, int K, int D,
-       int* __restrict__ err) {
+       int* __restrict__ err, KeyMap km) {
   extern __shared__ uint32_t s_hist[];
   const int radix = 1 << K;
   const int nb = D * radix;
@@ -59,6 +83,7 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
     bad |= (nx != PBIT_NULL32) & (nx >= n_ids);
     if constexpr (KB == 8) {
       unsigned long long k = __ldcs(reinterpret_cast<const unsigned long long*>(keys) + v);
+      if (!km.identity()) k = km(k, 64);
       kn[v] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), nx, 0u);
       for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
     } else {
@@ -66,6 +91,7 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
       if constexpr (KB == 1) k = reinterpret_cast<const uint8_t*>(keys)[v];
       else if constexpr (KB == 2) k = reinterpret_cast<const uint16_t*>(keys)[v];
       else k = __ldcs(reinterpret_cast<const uint32_t*>(keys) + v);
+      if (!km.identity()) k = (uint32_t)km(k, KB * 8);
       kn[v] = make_uint2(k, nx);
       for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
     }

@@ -67,8 +67,8 @@ struct Bump {
 
 template <int KB>
 int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint32_t n, uint32_t S,
-           uint32_t n_local, int K, uint32_t* out_head, uint32_t* out_next_local, ncclComm_t comm, int G, int r,
-           cudaStream_t st, uint32_t* launches_out) {
+           uint32_t n_local, int K, KeyMap km, uint32_t* out_head, uint32_t* out_next_local, ncclComm_t comm,
+           int G, int r, cudaStream_t st, uint32_t* launches_out) {
   using RT = typename Rec<KB>::T;
   uint32_t launches = 0;
   using KeyT = typename KeyOf<KB>::T;
@@ -181,7 +181,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       const int blocks = std::max(1, std::min((int)((n_local + 255) / 256), sms * 8));
       ++launches;
       k_pack<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys_local, next_local, n_local, n,
-                                                                       kn + lo, hist_l, K, D, err);
+                                                                       kn + lo, hist_l, K, D, err, km);
     }
     NCCLCHK(ncclAllGather(kn + lo, kn, (size_t)S * REC_WORDS, ncclUint32, comm, st));
     NCCLCHK(ncclAllReduce(hist_l, hist_g, (size_t)D * radix, ncclUint32, ncclSum, comm, st));
@@ -497,6 +497,8 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
   int K = opts && opts->digit_bits ? opts->digit_bits : 8;
   if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
   if (n_global > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+  const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
+  if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
   cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
   int G = 0, r = 0;
   if (ncclCommCount((ncclComm_t)nccl_comm, &G) != ncclSuccess) return PBIT_ERR_NCCL;
@@ -520,16 +522,16 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
                   pointer_kind(out_next_local, dev) != 1))
     return PBIT_ERR_INVALID_ARG;
   switch (key_bits) {
-    case 8: return run_mg<1>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
+    case 8: return run_mg<1>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
-    case 16: return run_mg<2>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
+    case 16: return run_mg<2>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
                               out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
-    case 32: return run_mg<4>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
+    case 32: return run_mg<4>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
                               out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
-    default: return run_mg<8>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K,
+    default: return run_mg<8>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
                               out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
   }

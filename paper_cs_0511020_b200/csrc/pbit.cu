@@ -220,7 +220,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   {
     const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
     const size_t smem = (size_t)p.D * radix * 4;
-    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err);
+    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err,
+                                                   KeyMap{p.key_kind, p.descending});
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
@@ -353,15 +354,22 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   return PBIT_OK;
 }
 
+bool key_kind_ok(int key_kind, int key_bits) {
+  if (key_kind == PBIT_KEY_UNSIGNED || key_kind == PBIT_KEY_SIGNED) return true;
+  return key_kind == PBIT_KEY_FLOAT && key_bits >= 16;  // IEEE binary16/32/64
+}
+
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
-                uint32_t* out_head, uint32_t* out_next, cudaStream_t st, float* phase_ms, uint32_t* passes_run,
-                uint32_t* launches) {
+                int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, cudaStream_t st,
+                float* phase_ms, uint32_t* passes_run, uint32_t* launches) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
   int sms = 0;
   if (int rc = device_info(dev, &sms)) return rc;
   SortPlan p;
   make_plan(n, key_bits, K, &p);
+  p.key_kind = key_kind;
+  p.descending = descending ? 1 : 0;
   switch (key_bits) {
     case 8: return run_device<1>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
     case 16: return run_device<2>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
@@ -408,6 +416,9 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   int K = opts && opts->digit_bits ? opts->digit_bits : 8;
   if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
   if (n > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+  const int key_kind = opts ? opts->key_kind : PBIT_KEY_UNSIGNED;
+  const int descending = opts ? opts->descending : 0;
+  if (!key_kind_ok(key_kind, key_bits)) return PBIT_ERR_INVALID_ARG;
   cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
   float* phase_ms = opts ? opts->phase_ms : nullptr;
   uint32_t* passes_run = opts ? opts->passes_run : nullptr;
@@ -426,7 +437,8 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   const int kk = pointer_kind(keys, dev), kn = pointer_kind(next, dev), ko = pointer_kind(out_next, dev);
   if (kk < 0 || kn < 0 || ko < 0) return PBIT_ERR_INVALID_ARG;
   if (kk == 1 && kn == 1 && ko == 1)
-    return sort_device(keys, next, head, n, key_bits, K, out_head, out_next, st, phase_ms, passes_run, launches);
+    return sort_device(keys, next, head, n, key_bits, K, key_kind, descending, out_head, out_next, st, phase_ms,
+                       passes_run, launches);
   if (kk != 0 || kn != 0 || ko != 0) return PBIT_ERR_INVALID_ARG;  // mixed host/device
 
   // host buffers: stage through device memory inside the call
@@ -438,7 +450,8 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   if (cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ||
       cudaMemcpyAsync(d + a, next, nbytes, cudaMemcpyHostToDevice, st))
     rc = PBIT_ERR_CUDA;
-  if (!rc) rc = sort_device(d, (const uint32_t*)(d + a), head, n, key_bits, K, out_head, (uint32_t*)(d + a + b), st,
+  if (!rc) rc = sort_device(d, (const uint32_t*)(d + a), head, n, key_bits, K, key_kind, descending, out_head,
+                            (uint32_t*)(d + a + b), st,
                             phase_ms, passes_run, launches);
   if (!rc && cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
   cudaFreeAsync(d, st);

@@ -14,6 +14,8 @@ struct SortPlan {
   uint32_t cap; // slot capacity per segment
   uint32_t R;   // static rulers (id blocks)
   uint32_t dyn_cap;
+  int key_kind = 0;    // PBIT_KEY_* (key order map applied in the pack)
+  int descending = 0;
 };
 
 void set_last_error(const char* what, const char* detail);
@@ -24,7 +26,9 @@ size_t sweep_tile(int key_bits);
 int rank_mode();                      // RANK_ATOMIC / RANK_BALLOT / RANK_MATCH for k_onesweep
 void init_rank_mode(cudaStream_t st); // runs the atomic-order self-test once
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
-                uint32_t* out_head, uint32_t* out_next, cudaStream_t st, float* phase_ms, uint32_t* passes_run,
-                uint32_t* launches);
+                int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, cudaStream_t st,
+                float* phase_ms, uint32_t* passes_run, uint32_t* launches);
+// key_kind / key_bits combination accepted by the ABI (PBIT_KEY_*, pbit.h)
+bool key_kind_ok(int key_kind, int key_bits);
 
 }  // namespace pbit

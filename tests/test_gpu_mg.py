@@ -73,3 +73,15 @@ def test_mg_bad_slice_rejected(mg):
     with pytest.raises(p.PbitError) as e:
         p.sort_list_mg(k[:50], nx[:50], 0, 100, 0, comm)  # a 1-rank comm must own all 100 nodes
     assert e.value.code == 6
+
+
+@pytest.mark.parametrize("kind,desc", [("signed", False), ("float", True), ("unsigned", True)])
+def test_mg_key_kinds(mg, kind, desc):
+    p, comm = mg
+    li = workloads.make_list(123457, 32, seed=17, keys="uniform", device="cuda")
+    h, out = p.sort_list_mg(li.keys, li.next, li.head, li.n, 0, comm, key_kind=kind, descending=desc)
+    torch.cuda.synchronize()
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, 32, 4,
+                              descending=desc, kind=kind)
+    assert h == oh
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), on)

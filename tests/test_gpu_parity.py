@@ -220,3 +220,65 @@ def test_full_size_configs(pbit, cfg):
     assert got == want
     del li, out
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- key kinds (NEXT row N1)
+# The same seeded bit patterns read as signed integers or IEEE floats (uniform 32/64-bit
+# patterns include NaNs, infinities, subnormals and both zeros), ascending and descending,
+# against the oracle's paper-derived procedures.
+KIND_CASES = [
+    (1, 32, "uniform", "random", "signed", False), (2, 8, "uniform", "random", "signed", True),
+    (4099, 8, "uniform", "push", "signed", False), (65537, 16, "uniform", "random", "signed", True),
+    (100003, 32, "uniform", "random", "signed", False), (100003, 32, "zipf", "random", "signed", True),
+    (70001, 64, "uniform", "identity", "signed", True), (70001, 64, "runs4096", "random", "signed", False),
+    (100003, 32, "max", "random", "signed", True), (33333, 16, "uniform", "random", "float", False),
+    (100003, 32, "uniform", "random", "float", False), (100003, 32, "uniform", "random", "float", True),
+    (70001, 64, "uniform", "random", "float", False), (70001, 64, "uniform", "push", "float", True),
+    (65537, 16, "equal", "random", "float", True), (100003, 32, "uniform", "random", "unsigned", True),
+    (70001, 8, "uniform", "random", "unsigned", True), (250001, 64, "runs4096", "random", "unsigned", True),
+    (1000003, 32, "zipf", "random", "float", True),
+]
+
+
+@pytest.mark.parametrize("n,key_bits,keys,links,kind,desc", KIND_CASES)
+def test_key_kinds_vs_oracle(pbit, n, key_bits, keys, links, kind, desc):
+    li = workloads.make_list(n, key_bits, seed=(n * 3) ^ key_bits, keys=keys, links=links, device="cuda")
+    got = _gpu_sort(pbit, li, key_kind=kind, descending=desc)
+    want = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, li.key_bits, 4,
+                            descending=desc, kind=kind)
+    _assert_same(got, want, f"{li.name} {kind} desc={desc}")
+
+
+@pytest.mark.parametrize("K", [1, 2, 3, 4, 5, 6, 7, 8])
+def test_key_kinds_every_digit_width(pbit, K):
+    li = workloads.make_list(65537, 32, seed=91, keys="uniform", device="cuda")
+    want = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, 32, 4,
+                            descending=True, kind="float")
+    _assert_same(_gpu_sort(pbit, li, K=K, key_kind="float", descending=True), want, f"float desc K={K}")
+
+
+def test_float_special_values(pbit):
+    """±0, ±inf, NaNs with payloads, subnormals, repeated: the IEEE totalOrder reading (Q18)."""
+    special = np.array([0x00000000, 0x80000000, 0x7F800000, 0xFF800000, 0x7FC00000, 0xFFC00000, 0x7FC00001,
+                        0x00000001, 0x80000001, 0x3F800000, 0xBF800000, 0x7F7FFFFF, 0xFF7FFFFF], np.uint32)
+    rng = np.random.default_rng(5)
+    n = 50001
+    bits = special[rng.integers(0, len(special), n)]
+    order = rng.permutation(n)
+    nxt = np.full(n, NULL, np.uint32)
+    nxt[order[:-1]] = order[1:]
+    kd = torch.from_numpy(bits.view(np.int32)).cuda()
+    nd = torch.from_numpy(nxt.view(np.int32)).cuda()
+    for desc in (False, True):
+        h, out = pbit.sort_list(kd, nd, int(order[0]), key_bits=32, key_kind="float", descending=desc)
+        torch.cuda.synchronize()
+        want = oracle.pbit_sort(bits, nxt, int(order[0]), 32, 4, descending=desc, kind="float")
+        _assert_same((h, out.cpu().numpy().view(np.uint32)), want, f"float specials desc={desc}")
+
+
+def test_key_kind_invalid_args(pbit):
+    k = torch.zeros(4, dtype=torch.uint8, device="cuda")
+    nx = torch.tensor([1, 2, 3, -1], dtype=torch.int32, device="cuda")
+    with pytest.raises(pbit.PbitError) as e:  # no 8-bit IEEE format
+        pbit.sort_list(k, nx, 0, key_kind="float")
+    assert e.value.code == 1
