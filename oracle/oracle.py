@@ -63,6 +63,8 @@ def _load():
             lib.oracle_pbit_sort_kind.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32,
                                                   ctypes.c_uint64, ctypes.c_uint, ctypes.c_int, ctypes.c_int, u32p,
                                                   ctypes.c_void_p, ctypes.POINTER(Counters)]
+            lib.oracle_repair_back.restype = ctypes.c_int
+            lib.oracle_repair_back.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
             lib.oracle_split_once.restype = ctypes.c_int
             lib.oracle_split_once.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32,
                                               ctypes.c_uint64, ctypes.c_uint, ctypes.c_void_p]
@@ -117,6 +119,18 @@ def pbit_sort(keys, next_, head: int, key_bits: int, K: int = 4, descending: boo
         raise OracleError(rc)
     res = (int(oh.value), out[:n])
     return res + (c.as_dict(),) if with_counters else res
+
+
+def repair_back(next_, head: int):
+    """The doubly-linked "reverse connection" repair after sorting:
+    returns back[] with back[v] = the node right behind v (NULL for the head)."""
+    nxt = np.ascontiguousarray(next_, dtype=np.uint32)
+    back = np.empty(max(nxt.shape[0], 1), np.uint32)
+    rc = _load().oracle_repair_back(nxt.ctypes.data if nxt.size else None, head & 0xFFFFFFFF, nxt.shape[0],
+                                    back.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return back[:nxt.shape[0]]
 
 
 def split_once(keys, next_, head: int, key_bits: int, K: int = 4):

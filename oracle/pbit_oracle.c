@@ -286,6 +286,20 @@ int oracle_pbit_sort_kind(const void *keys, int key_bits, const uint32_t *next, 
     return ORACLE_OK;
 }
 
+/* The "reverse connection" repair of a doubly-linked list after Pbit:
+ * "going through its elements it should set up pointer `back' in such a way as to show
+ * the element right behind".  back[head] = NULL.  The list must be valid (Q10). */
+int oracle_repair_back(const uint32_t *next, uint32_t head, uint64_t n, uint32_t *back) {
+    int rc = oracle_validate_list(next, head, n);
+    if (rc) return rc;
+    uint32_t behind = ORACLE_NULL;
+    for (uint32_t v = head; v != ORACLE_NULL; v = next[v]) {
+        back[v] = behind;
+        behind = v;
+    }
+    return ORACLE_OK;
+}
+
 /* First split only (P:351-353 at the top level, M -= K once): fills tab[Omega] with
  * the bucket heads and relinks next[] in place.  Exposed so tests can pin the
  * worked example's first-level groups. */

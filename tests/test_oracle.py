@@ -392,3 +392,32 @@ def test_literal_signed_split_is_reverse_stable():
     assert seq == [3, 1, 4, 2, 0]  # equal keys reversed: not stable
     h, out = oracle.pbit_sort(keys, nxt, head, 32, 4, kind="signed")
     assert walk(out, h) == [1, 3, 0, 2, 4]  # the oracle's reading: stable
+
+
+# ---------------------------------------------------------------- doubly-linked repair (NEXT row N2)
+def test_repair_back_examples():
+    """repair([a->b->c]) -> back(c)=b, back(b)=a, back(a)=NULL; a single
+    node gets NULL; the empty list stays empty."""
+    nxt = np.array([2, NULL, 1], np.uint32)  # a=0 -> c=2 -> b=1
+    back = oracle.repair_back(nxt, 0)
+    assert back[2] == 0 and back[1] == 2 and back[0] == NULL
+    assert list(oracle.repair_back(np.array([NULL], np.uint32), 0)) == [NULL]
+    assert oracle.repair_back(np.zeros(0, np.uint32), NULL).size == 0
+    with pytest.raises(oracle.OracleError):
+        oracle.repair_back(np.array([1, 0], np.uint32), 0)  # cycle
+
+
+def test_repair_back_after_sort_is_the_reverse_chain():
+    """After a sort, back[] must satisfy back[next[x]] = x for every node x with a
+    successor and back[head] = NULL: the plain definition w_{i+1} -> w_i."""
+    rng = np.random.default_rng(9)
+    n = 5003
+    keys = rng.integers(0, 50, n).astype(np.uint32)
+    order = rng.permutation(n)
+    nxt = np.full(n, NULL, np.uint32)
+    nxt[order[:-1]] = order[1:]
+    h, out = oracle.pbit_sort(keys, nxt, int(order[0]), 32, 4)
+    back = oracle.repair_back(out, h)
+    w = walk(out, h)
+    assert back[w[0]] == NULL
+    assert all(back[b] == a for a, b in zip(w, w[1:]))
