@@ -14,6 +14,7 @@ from .oracle import (  # noqa: F401
     build,
     memory_bound_T,
     pbit_sort,
+    repair_back,
     split_once,
     validate_list,
 )
