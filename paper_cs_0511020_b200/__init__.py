@@ -38,7 +38,7 @@ class _Opts(ctypes.Structure):
     _fields_ = [("digit_bits", ctypes.c_int), ("stream", ctypes.c_void_p), ("validate", ctypes.c_int),
                 ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("passes_run", ctypes.POINTER(ctypes.c_uint32)),
                 ("launches", ctypes.POINTER(ctypes.c_uint32)), ("key_kind", ctypes.c_int),
-                ("descending", ctypes.c_int)]
+                ("descending", ctypes.c_int), ("out_prev", ctypes.c_void_p)]
 
 
 KEY_KINDS = {"unsigned": 0, "signed": 1, "float": 2}  # pbit.h PBIT_KEY_*
@@ -119,14 +119,17 @@ def _stream_handle(stream, on_cuda: bool):
 
 
 def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: int = 0, out_next=None,
-              stream=None, timing: bool = False, key_kind: str = "unsigned", descending: bool = False):
+              stream=None, timing: bool = False, key_kind: str = "unsigned", descending: bool = False,
+              out_prev=None):
     """Stable sort of the list (head, next_) by keys; returns (head, out_next) (plus a
     dict of device ms per phase when timing=True).
 
     keys / next_ / out_next: CUDA tensors on the current device, or host arrays (torch
     CPU tensors or numpy) -- then the library stages them through device memory.
     next_ holds u32 ids (int32 view, NULL = -1 / 0xFFFFFFFF).  key_kind: "unsigned",
-    "signed" or "float" (how the key bits order, pbit.h PBIT_KEY_*); descending: order."""
+    "signed" or "float" (how the key bits order, pbit.h PBIT_KEY_*); descending: order.
+    out_prev (same kind as out_next): also filled with the predecessors of the sorted list
+    (doubly-linked lists, pbit.h pbit_opts.out_prev)."""
     if key_bits is None:
         key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
     n = int(next_.shape[0])
@@ -143,6 +146,8 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
     launches = ctypes.c_uint32(0)
     o = _opts(digit_bits, _stream_handle(stream, on_cuda), pm, ctypes.pointer(passes), ctypes.pointer(launches),
               key_kind, descending)
+    if out_prev is not None and n:
+        o.out_prev = ctypes.c_void_p(_ptr(out_prev))
     rc = lib.pbit_sort_list(_ptr(keys) if n else None, _ptr(next_) if n else None, head & 0xFFFFFFFF, n, key_bits,
                             ctypes.byref(oh), _ptr(out_next) if n else None, ctypes.byref(o))
     if rc:

@@ -794,7 +794,7 @@ template <bool FROM_IDS>
 __global__ void __launch_bounds__(PART_THREADS, PART_CTAS_PER_SM)
 k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, uint2* __restrict__ pout,
               uint32_t n, uint32_t v_off, int shift, int bits, uint32_t* __restrict__ cursor,
-              const int* __restrict__ err) {
+              const int* __restrict__ err, int dir) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
   if (*err) return;
@@ -806,10 +806,11 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[buf]);
     uint32_t bytes;
     const void* src;
-    if constexpr (FROM_IDS) {  // the tile's ids plus the next tile's first (the last succ)
-      const uint32_t c = min((uint32_t)PART_TILE + 4u, n - base);
+    if constexpr (FROM_IDS) {  // the tile's ids plus 4 look-ahead (dir +1) or look-behind (-1)
+      const uint32_t lo = dir > 0 ? base : (base >= 4u ? base - 4u : 0u);
+      const uint32_t c = min(base + (uint32_t)PART_TILE + 4u, n) - lo;
       bytes = ((c + 3u) & ~3u) * 4u;
-      src = ids + base;
+      src = ids + lo;
     } else {
       const uint32_t c = min((uint32_t)PART_TILE, n - base);
       bytes = ((c + 1u) & ~1u) * 8u;
@@ -846,13 +847,16 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
     uint2 x[PART_IPT];
     uint32_t r[PART_IPT];
     const uint32_t* in_ids = reinterpret_cast<const uint32_t*>(&sm.in[buf][0]);
+    const uint32_t off = (FROM_IDS && dir < 0) ? (base >= 4u ? 4u : 0u) : 0u;  // look-behind shift
 #pragma unroll
     for (int i = 0; i < PART_IPT; ++i) {
       const uint32_t j = i * PART_THREADS + t;
       if (j < cnt) {
         if constexpr (FROM_IDS) {
-          x[i].x = in_ids[j];
-          x[i].y = base + j + 1 < n ? in_ids[j + 1] : PBIT_NULL32;
+          // dir +1: (ids[p], ids[p+1]) -> out_next; dir -1: (ids[p], ids[p-1]) -> out_prev
+          x[i].x = in_ids[off + j];
+          if (dir > 0) x[i].y = base + j + 1 < n ? in_ids[j + 1] : PBIT_NULL32;
+          else x[i].y = base + j > 0 ? in_ids[off + j - 1] : PBIT_NULL32;
         } else {
           x[i] = sm.in[buf][j];
           x[i].x -= v_off;
@@ -908,17 +912,19 @@ static __global__ void k_relink_head(const uint32_t* __restrict__ ids, uint32_t*
 
 // Last step: one CTA per fine bin: scatter into a 64 KB smem window, write it coalesced.
 // FROM_IDS: n <= 2^14, one window, the pairs come straight from the sorted ids.
+// `out_next` is the output array: out_next (dir +1) or out_prev (dir -1, N2).
 template <bool FROM_IDS>
 __global__ void __launch_bounds__(512)
 k_relink_apply(const uint32_t* __restrict__ ids, const uint2* __restrict__ pairs, uint32_t n, uint32_t v_off,
-               uint32_t* __restrict__ out_next, const int* __restrict__ err) {
+               uint32_t* __restrict__ out_next, const int* __restrict__ err, int dir) {
   extern __shared__ __align__(16) uint32_t s_win[];
   if (*err) return;
   const uint32_t f0 = blockIdx.x << RELINK_FINE_SHIFT;
   const uint32_t cnt = min((uint32_t)(1u << RELINK_FINE_SHIFT), n - f0);
   for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
     if constexpr (FROM_IDS) {
-      s_win[ids[i]] = i + 1 < n ? ids[i + 1] : PBIT_NULL32;
+      if (dir > 0) s_win[ids[i]] = i + 1 < n ? ids[i + 1] : PBIT_NULL32;
+      else s_win[ids[i]] = i > 0 ? ids[i - 1] : PBIT_NULL32;
     } else {
       const uint2 p = __ldcs(pairs + f0 + i);
       s_win[p.x - v_off - f0] = p.y;

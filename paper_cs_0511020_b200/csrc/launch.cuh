@@ -70,9 +70,11 @@ static inline size_t relink_cursor_words(uint32_t n) {
 // formed on the fly) or pairs (`pairs`, v - v_off = local id).  pbuf[2]: n pairs each;
 // when the source is pairs it must not be pbuf[0] (level 0 writes pbuf[0]).
 // Returns the number of kernels launched.
+// dir = -1 (ids source only): out_next receives the predecessors instead (out_prev, the
+// doubly-linked repair of P:1179-1181).
 static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t v_off, uint32_t n, uint2* pbuf0,
                               uint2* pbuf1, uint32_t* cursors, uint32_t* out_next, const int* err, cudaStream_t st,
-                              int sms) {
+                              int sms, int dir = 1) {
   static bool attr = false;  // benign race: idempotent
   if (!attr) {
     cudaFuncSetAttribute(k_relink_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
@@ -85,8 +87,8 @@ static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t 
   RelinkLevels lv(n);
   const uint32_t nfine = (n + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
   if (lv.L == 0) {
-    if (ids) k_relink_apply<true><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(ids, nullptr, n, 0, out_next, err);
-    else k_relink_apply<false><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, pairs, n, v_off, out_next, err);
+    if (ids) k_relink_apply<true><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(ids, nullptr, n, 0, out_next, err, dir);
+    else k_relink_apply<false><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, pairs, n, v_off, out_next, err, 1);
     return 1;
   }
   const uint32_t ntiles = (n + PART_TILE - 1) / PART_TILE;
@@ -98,14 +100,14 @@ static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t 
     uint2* out = buf[l & 1];
     if (l == 0 && ids)
       k_relink_part<true><<<grid, PART_THREADS, psm, st>>>(ids, nullptr, out, n, 0, lv.shift[l], lv.bits[l], cursors,
-                                                           err);
+                                                           err, dir);
     else
       k_relink_part<false><<<grid, PART_THREADS, psm, st>>>(nullptr, in, out, n, l == 0 ? v_off : 0u, lv.shift[l],
-                                                            lv.bits[l], cursors, err);
+                                                            lv.bits[l], cursors, err, 1);
     cursors += RelinkLevels::cursors(n, lv.shift[l]);
     in = out;
   }
-  k_relink_apply<false><<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, in, n, 0, out_next, err);
+  k_relink_apply<false><<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, in, n, 0, out_next, err, 1);
   return (uint32_t)lv.L + 1;
 }
 

@@ -497,6 +497,7 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
   int K = opts && opts->digit_bits ? opts->digit_bits : 8;
   if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
   if (n_global > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+  if (opts && opts->out_prev) return PBIT_ERR_UNSUPPORTED;  // N2 is single-GPU only (pbit.h)
   const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
   if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
   cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;

@@ -183,8 +183,8 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
 // ----------------------------------------------------------------------------- the device path
 template <int KB>
 static int run_device(const void* keys, const uint32_t* next, uint32_t head, const SortPlan& p, uint32_t* out_next,
-                      uint32_t* out_head, cudaStream_t st, int sms, float* phase_ms, uint32_t* passes_run,
-                      uint32_t* launches_out) {
+                      uint32_t* out_prev, uint32_t* out_head, cudaStream_t st, int sms, float* phase_ms,
+                      uint32_t* passes_run, uint32_t* launches_out) {
   using RT = typename Rec<KB>::T;
   Ws w;
   const size_t bytes = carve(p, nullptr, &w);
@@ -315,6 +315,10 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     k_relink_head<<<1, 1, 0, st>>>(fin, w.d_head, w.err);
     ++launches;
     launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_next, w.err, st, sms);
+    if (out_prev) {  // N2: the same binned relink of the pairs (ids[p], ids[p-1])
+      cudaMemsetAsync(w.cursors, 0, relink_cursor_words(n) * 4, st);
+      launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_prev, w.err, st, sms, -1);
+    }
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
 
@@ -360,8 +364,8 @@ bool key_kind_ok(int key_kind, int key_bits) {
 }
 
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
-                int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, cudaStream_t st,
-                float* phase_ms, uint32_t* passes_run, uint32_t* launches) {
+                int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
+                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches) {
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
   int sms = 0;
@@ -371,10 +375,10 @@ int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t 
   p.key_kind = key_kind;
   p.descending = descending ? 1 : 0;
   switch (key_bits) {
-    case 8: return run_device<1>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
-    case 16: return run_device<2>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
-    case 32: return run_device<4>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
-    default: return run_device<8>(keys, next, head, p, out_next, out_head, st, sms, phase_ms, passes_run, launches);
+    case 8: return run_device<1>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
+    case 16: return run_device<2>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
+    case 32: return run_device<4>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
+    default: return run_device<8>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
   }
 }
 
@@ -419,6 +423,8 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   const int key_kind = opts ? opts->key_kind : PBIT_KEY_UNSIGNED;
   const int descending = opts ? opts->descending : 0;
   if (!key_kind_ok(key_kind, key_bits)) return PBIT_ERR_INVALID_ARG;
+  uint32_t* out_prev = opts ? opts->out_prev : nullptr;
+  if (out_prev && out_prev == out_next) return PBIT_ERR_INVALID_ARG;
   cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
   float* phase_ms = opts ? opts->phase_ms : nullptr;
   uint32_t* passes_run = opts ? opts->passes_run : nullptr;
@@ -435,25 +441,28 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
   const int kk = pointer_kind(keys, dev), kn = pointer_kind(next, dev), ko = pointer_kind(out_next, dev);
-  if (kk < 0 || kn < 0 || ko < 0) return PBIT_ERR_INVALID_ARG;
-  if (kk == 1 && kn == 1 && ko == 1)
-    return sort_device(keys, next, head, n, key_bits, K, key_kind, descending, out_head, out_next, st, phase_ms,
-                       passes_run, launches);
-  if (kk != 0 || kn != 0 || ko != 0) return PBIT_ERR_INVALID_ARG;  // mixed host/device
+  const int kp = out_prev ? pointer_kind(out_prev, dev) : ko;
+  if (kk < 0 || kn < 0 || ko < 0 || kp < 0) return PBIT_ERR_INVALID_ARG;
+  if (kk == 1 && kn == 1 && ko == 1 && kp == 1)
+    return sort_device(keys, next, head, n, key_bits, K, key_kind, descending, out_head, out_next, out_prev, st,
+                       phase_ms, passes_run, launches);
+  if (kk != 0 || kn != 0 || ko != 0 || kp != 0) return PBIT_ERR_INVALID_ARG;  // mixed host/device
 
   // host buffers: stage through device memory inside the call
   const size_t kbytes = n * (size_t)(key_bits / 8), nbytes = n * 4;
   char* d = nullptr;
   const size_t a = align_up(kbytes), b = align_up(nbytes);
-  if (cudaMallocAsync((void**)&d, a + 2 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (cudaMallocAsync((void**)&d, a + 3 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  uint32_t* d_prev = out_prev ? (uint32_t*)(d + a + 2 * b) : nullptr;
   int rc = PBIT_OK;
   if (cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ||
       cudaMemcpyAsync(d + a, next, nbytes, cudaMemcpyHostToDevice, st))
     rc = PBIT_ERR_CUDA;
   if (!rc) rc = sort_device(d, (const uint32_t*)(d + a), head, n, key_bits, K, key_kind, descending, out_head,
-                            (uint32_t*)(d + a + b), st,
+                            (uint32_t*)(d + a + b), d_prev, st,
                             phase_ms, passes_run, launches);
   if (!rc && cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+  if (!rc && out_prev && cudaMemcpyAsync(out_prev, d_prev, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
   cudaFreeAsync(d, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = PBIT_ERR_CUDA;
   cudaGetLastError();

@@ -26,8 +26,8 @@ size_t sweep_tile(int key_bits);
 int rank_mode();                      // RANK_ATOMIC / RANK_BALLOT / RANK_MATCH for k_onesweep
 void init_rank_mode(cudaStream_t st); // runs the atomic-order self-test once
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
-                int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, cudaStream_t st,
-                float* phase_ms, uint32_t* passes_run, uint32_t* launches);
+                int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
+                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches);
 // key_kind / key_bits combination accepted by the ABI (PBIT_KEY_*, pbit.h)
 bool key_kind_ok(int key_kind, int key_bits);
 

@@ -85,3 +85,17 @@ def test_mg_key_kinds(mg, kind, desc):
                               descending=desc, kind=kind)
     assert h == oh
     assert np.array_equal(out.cpu().numpy().view(np.uint32), on)
+
+
+def test_mg_out_prev_unsupported(mg):
+    p, comm = mg
+    li = workloads.make_list(1000, 32, seed=3, device="cuda")
+    import ctypes
+    o = p._opts(0, 0, None, None, None)
+    prev = torch.empty_like(li.next)
+    o.out_prev = ctypes.c_void_p(prev.data_ptr())
+    out = torch.empty_like(li.next)
+    oh = ctypes.c_uint32(0)
+    rc = p.lib.pbit_sort_list_mg(li.keys.data_ptr(), li.next.data_ptr(), li.head, li.n, 0, li.n, 32,
+                                 ctypes.byref(oh), out.data_ptr(), ctypes.c_void_p(comm), ctypes.byref(o))
+    assert rc == 6  # PBIT_ERR_UNSUPPORTED

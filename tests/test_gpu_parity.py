@@ -282,3 +282,39 @@ def test_key_kind_invalid_args(pbit):
     with pytest.raises(pbit.PbitError) as e:  # no 8-bit IEEE format
         pbit.sort_list(k, nx, 0, key_kind="float")
     assert e.value.code == 1
+
+
+# ---------------------------------------------------------------- doubly-linked lists (NEXT row N2)
+@pytest.mark.parametrize("n,key_bits,keys,links", [
+    (1, 32, "uniform", "random"), (2, 8, "uniform", "random"), (3, 16, "equal", "push"),
+    (16384, 32, "uniform", "random"), (16385, 32, "zipf", "random"), (70001, 64, "uniform", "random"),
+    (1000003, 32, "zipf", "random"), (1 << 20, 16, "uniform", "identity")])
+def test_doubly_linked_out_prev(pbit, n, key_bits, keys, links):
+    """out_prev = the paper's reverse-connection repair of the sorted list,
+    computed by the oracle from its own sorted out_next."""
+    li = workloads.make_list(n, key_bits, seed=n + 5, keys=keys, links=links, device="cuda")
+    prev = torch.empty_like(li.next)
+    h, out = pbit.sort_list(li.keys, li.next, li.head, key_bits=key_bits, out_prev=prev)
+    torch.cuda.synchronize()
+    oh, on = _oracle(li)
+    _assert_same((h, out.cpu().numpy().view(np.uint32)), (oh, on), f"{li.name} next")
+    want_prev = oracle.repair_back(on, oh)
+    assert np.array_equal(prev.cpu().numpy().view(np.uint32), want_prev)
+
+
+def test_doubly_linked_host_buffers_and_args(pbit):
+    li = workloads.make_list(40001, 32, seed=8, keys="uniform", device="cpu")
+    prev = np.empty(li.n, np.uint32)
+    out = np.empty(li.n, np.uint32)
+    h, _ = pbit.sort_list(li.keys, li.next, li.head, out_next=out, out_prev=prev, descending=True,
+                          key_kind="signed")
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, 32, 4,
+                              descending=True, kind="signed")
+    assert h == oh and np.array_equal(out, on)
+    assert np.array_equal(prev, oracle.repair_back(on, oh))
+    k = li.keys.cuda()
+    nx = li.next.cuda()
+    o = torch.empty_like(nx)
+    with pytest.raises(pbit.PbitError) as e:  # out_prev aliasing out_next
+        pbit.sort_list(k, nx, li.head, out_next=o, out_prev=o)
+    assert e.value.code == 1
