@@ -66,11 +66,27 @@ struct KeyMap {
 // ============================================================================ a1/a2: pack
 // Reads key[v], next[v] (streaming, coalesced), writes the AoS record kn[v], and counts
 // every digit of every key into a per-CTA smem histogram (flushed once per CTA).
+// Four independent nodes per thread and iteration: 4x the loads in flight of one node
+// per thread, every access still lane-contiguous.
+template <int KB>
+__device__ __forceinline__ void pack_one(unsigned long long k, uint32_t nx, uint32_t v, uint32_t n_ids,
+                                         typename Rec<KB>::T* __restrict__ kn, uint32_t* s_hist, int radix,
+                                         uint32_t mask, int K, int D, const KeyMap& km, int& bad) {
+  bad |= (nx != PBIT_NULL32) & (nx >= n_ids);
+  if (!km.identity()) k = km(k, KB * 8);
+  if constexpr (KB == 8) kn[v] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), nx, 0u);
+  else kn[v] = make_uint2((uint32_t)k, nx);
+  for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
+}
+
 template <int KB>
 __global__ void __launch_bounds__(PACK_THREADS)
 k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_t n, uint32_t n_ids,
        typename Rec<KB>::T* __restrict__ kn, uint32_t* __restrict__ hist, int K, int D,
        int* __restrict__ err, KeyMap km) {
+  using KT = std::conditional_t<KB == 1, uint8_t, std::conditional_t<KB == 2, uint16_t,
+             std::conditional_t<KB == 4, uint32_t, unsigned long long>>>;
+  constexpr int U = 4;  // independent nodes per thread and iteration (all loads issued first)
   extern __shared__ uint32_t s_hist[];
   const int radix = 1 << K;
   const int nb = D * radix;
@@ -78,24 +94,23 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
   __syncthreads();
   const uint32_t mask = radix - 1;
   int bad = 0;
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    uint32_t nx = __ldcs(next + v);
-    bad |= (nx != PBIT_NULL32) & (nx >= n_ids);
-    if constexpr (KB == 8) {
-      unsigned long long k = __ldcs(reinterpret_cast<const unsigned long long*>(keys) + v);
-      if (!km.identity()) k = km(k, 64);
-      kn[v] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), nx, 0u);
-      for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
-    } else {
-      uint32_t k;
-      if constexpr (KB == 1) k = reinterpret_cast<const uint8_t*>(keys)[v];
-      else if constexpr (KB == 2) k = reinterpret_cast<const uint16_t*>(keys)[v];
-      else k = __ldcs(reinterpret_cast<const uint32_t*>(keys) + v);
-      if (!km.identity()) k = (uint32_t)km(k, KB * 8);
-      kn[v] = make_uint2(k, nx);
-      for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
+  const KT* __restrict__ kp = reinterpret_cast<const KT*>(keys);
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  uint32_t v = tid;
+  for (; (unsigned long long)v + (U - 1) * (unsigned long long)stride < n; v += U * stride) {
+    KT k[U];
+    uint32_t nx[U];
+#pragma unroll
+    for (int e = 0; e < U; ++e) {
+      k[e] = __ldcs(kp + v + e * stride);
+      nx[e] = __ldcs(next + v + e * stride);
     }
+#pragma unroll
+    for (int e = 0; e < U; ++e)
+      pack_one<KB>((unsigned long long)k[e], nx[e], v + e * stride, n_ids, kn, s_hist, radix, mask, K, D, km, bad);
   }
+  for (; v < n; v += stride)
+    pack_one<KB>((unsigned long long)kp[v], __ldcs(next + v), v, n_ids, kn, s_hist, radix, mask, K, D, km, bad);
   if (bad) atomicOr(err, E_BAD_INDEX);
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x)

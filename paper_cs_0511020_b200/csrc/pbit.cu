@@ -220,8 +220,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   {
     const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
     const size_t smem = (size_t)p.D * radix * 4;
-    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err,
-                                                   KeyMap{p.key_kind, p.descending});
+    const KeyMap km{p.key_kind, p.descending};
+    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
