@@ -882,6 +882,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
     __syncthreads();
     // exclusive scan of the tile's bin counts; claim the tile's space in every bin
     const uint32_t parent = FROM_IDS ? 0u : base >> (shift + bits);
+    uint32_t claim = 0;
     {
       const uint32_t c = t < nb ? sm.cnt[t] : 0u;
       uint32_t y = c;
@@ -896,8 +897,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
       for (uint32_t q = 0; q < w; ++q) add += sm.warp[q];
       if (t < nb) {
         sm.start[t] = y - c + add;
-        const uint32_t g = (parent << bits) | t;
-        sm.gofs[t] = c ? (g << shift) + atomicAdd(cursor + g, c) : 0u;
+        if (c) claim = atomicAdd(cursor + ((parent << bits) | t), c);  // round trip overlaps the staging
       }
     }
     __syncthreads();
@@ -906,6 +906,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
       const uint32_t j = i * PART_THREADS + t;
       if (j < cnt) sm.stage[sm.start[(x[i].x >> shift) & mask] + r[i]] = x[i];
     }
+    if (t < nb) sm.gofs[t] = (((parent << bits) | t) << shift) + claim;
     __syncthreads();
     // coalesced write-out: consecutive threads store consecutive staged pairs, which land
     // contiguously inside each bin's run
