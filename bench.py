@@ -394,6 +394,23 @@ def run_ours(args):
                  "frac_of_nominal_8tbs": round(dram / (ms / 1e3) / 1e9 / 8000.0, 4),
                  "source": tr.get("_source")}
 
+    # ---- the paper's tables-versus-lists comparison on this GPU: the same
+    # keys sorted as an ARRAY (pbit_sort_array: the radix passes without ranking/relink)
+    idx = torch.empty(n, dtype=torch.int32, device="cuda")
+    for _ in range(3):
+        pbit.sort_array(keys, key_bits=kb, digit_bits=K, out_index=idx)
+    torch.cuda.synchronize()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(st)
+    for _ in range(args.steps):
+        pbit.sort_array(keys, key_bits=kb, digit_bits=K, out_index=idx)
+    a1.record(st)
+    torch.cuda.synchronize()
+    arr_ms = a0.elapsed_time(a1) / args.steps
+    array_ctx = {"what": "same keys sorted as an array (pbit_sort_array -> sorted index), P:1118-1177",
+                 "ms": round(arr_ms, 4), "keys_per_s": n / (arr_ms / 1e3), "list_over_array_time": round(ms / arr_ms, 3)}
+    del idx
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         cpu = cpu_baseline(args.config, min(n, args.cpu_sample), args.cpu_reps)
@@ -409,7 +426,7 @@ def run_ours(args):
                            "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6
                            else "inputs smaller than L2"},
                 "hbm_gbs_method": round(method_bytes_per_node(kb) * n * ws / (ms_max / 1e3) / 1e9, 1),
-                "roofline": roofline, "whole_call_dram": whole, "cpu_baseline": cpu,
+                "roofline": roofline, "whole_call_dram": whole, "array_sort": array_ctx, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (kb // 8 + 4),
                         "d2h_bytes_per_step": n * 4 + 4},
                 "gpu_launches": launches * args.steps, "clocks": clocks}

@@ -131,6 +131,26 @@ int pbit_sort_list(const void *keys, const uint32_t *next, uint32_t head, uint64
                    int key_bits, uint32_t *out_head, uint32_t *out_next, const pbit_opts *opts);
 
 /*
+ * pbit_sort_array -- the "table" of the paper's tables-versus-lists comparison (section
+ * 12; NEXT row N3): a stable sort of an ARRAY of n keys by the same radix
+ * passes, with no list ranking and no relink.
+ *
+ *   keys      [in]  n keys, key_bits/8 bytes each (ordered per opts->key_kind /
+ *                   opts->descending, as pbit_sort_list).
+ *   n         [in]  0 <= n <= 2^32-2.
+ *   key_bits  [in]  M in {8, 16, 32, 64}.
+ *   out_index [out] optional: n u32, out_index[i] = position in `keys` of the i-th key
+ *                   of the sorted order (equal keys keep their array order).
+ *   out_keys  [out] optional: n keys, the sorted keys (the input bit patterns).
+ *   opts      [in]  may be NULL; out_prev is ignored.
+ * At least one output is required.  keys / out_index / out_keys are all device pointers
+ * on the current device or all host pointers (staged).  Errors as pbit_sort_list
+ * (no INVALID_LIST).
+ */
+int pbit_sort_array(const void *keys, uint64_t n, int key_bits, uint32_t *out_index, void *out_keys,
+                    const pbit_opts *opts);
+
+/*
  * pbit_sort_list_mg -- the same sort of ONE list whose nodes are sharded over the
  * G ranks of an NCCL communicator (one process per GPU).
  *

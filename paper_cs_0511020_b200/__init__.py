@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("PBIT_LIB_PATH") or os.path.join(_HERE, "libpbit.so") 
 PBIT_NULL = 0xFFFFFFFF
 NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
-SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
+SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_sort_array", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
            "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version", "pbit_last_error",
            "pbit_mg_slice", "pbit_mg_exchange_plan"]
 
@@ -53,6 +53,9 @@ def _load():
     lib.pbit_sort_list.restype = ctypes.c_int
     lib.pbit_sort_list.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int,
                                    u32p, ctypes.c_void_p, ctypes.POINTER(_Opts)]
+    lib.pbit_sort_array.restype = ctypes.c_int
+    lib.pbit_sort_array.argtypes = [ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p, ctypes.c_void_p,
+                                    ctypes.POINTER(_Opts)]
     lib.pbit_sort_list_mg.restype = ctypes.c_int
     lib.pbit_sort_list_mg.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64,
                                       ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int, u32p, ctypes.c_void_p,
@@ -158,6 +161,44 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
         ph["launches"] = int(launches.value)
         return int(oh.value), out_next, ph
     return int(oh.value), out_next
+
+
+def sort_array(keys, key_bits: int | None = None, digit_bits: int = 0, out_index=None, out_keys=None,
+               want_index: bool = True, want_keys: bool = False, key_kind: str = "unsigned",
+               descending: bool = False, stream=None, timing: bool = False):
+    """Stable sort of an ARRAY of keys (pbit.h pbit_sort_array, the paper's "table",
+    P:1118-1177).  Returns (out_index, out_keys) -- either may be None -- plus a dict of
+    device ms per phase when timing=True.  Tensors on the current CUDA device or host
+    arrays (torch CPU tensors or numpy)."""
+    if key_bits is None:
+        key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
+    n = int(keys.shape[0])
+    on_cuda = isinstance(keys, torch.Tensor) and keys.is_cuda
+    if want_index and out_index is None:
+        if isinstance(keys, torch.Tensor):
+            out_index = torch.empty(n, dtype=torch.int32, device=keys.device)
+        else:
+            import numpy as np
+            out_index = np.empty(n, np.uint32)
+    if want_keys and out_keys is None:
+        out_keys = keys.clone() if isinstance(keys, torch.Tensor) else keys.copy()
+    pm = (ctypes.c_float * NUM_PHASES)() if timing else None
+    passes = ctypes.c_uint32(0)
+    launches = ctypes.c_uint32(0)
+    o = _opts(digit_bits, _stream_handle(stream, on_cuda), pm, ctypes.pointer(passes), ctypes.pointer(launches),
+              key_kind, descending)
+    rc = lib.pbit_sort_array(_ptr(keys) if n else None, n, key_bits,
+                             _ptr(out_index) if (out_index is not None and n) else None,
+                             _ptr(out_keys) if (out_keys is not None and n) else None, ctypes.byref(o))
+    if rc:
+        raise PbitError(rc, _errtext(rc))
+    if timing:
+        ph = {name: float(pm[i]) for i, name in enumerate(PHASE_NAMES) if i in (0, 4) or pm[i] > 0}
+        ph = {("prep" if k == "pack" else "finish" if k == "relink" else k): v for k, v in ph.items()}
+        ph["passes_run"] = int(passes.value)
+        ph["launches"] = int(launches.value)
+        return out_index, out_keys, ph
+    return out_index, out_keys
 
 
 # ----------------------------------------------------------------------------- multi-GPU

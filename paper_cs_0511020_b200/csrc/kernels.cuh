@@ -61,6 +61,15 @@ struct KeyMap {
     return k;
   }
   __host__ __device__ __forceinline__ bool identity() const { return kind == 0 && !descending; }
+  // the key bits back from a sort key (pbit_sort_array's out_keys)
+  __host__ __device__ __forceinline__ unsigned long long inverse(unsigned long long k, int bits) const {
+    const unsigned long long all = bits == 64 ? ~0ull : ((1ull << bits) - 1);
+    const unsigned long long sign = 1ull << (bits - 1);
+    if (descending) k = ~k & all;
+    if (kind == 1) k ^= sign;
+    else if (kind == 2) k = (k & sign) ? (k & ~sign) : (~k & all);
+    return k;
+  }
 };
 
 // ============================================================================ a1/a2: pack
@@ -579,7 +588,11 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-template <typename KeyT, int RADIX_BITS, int IPT, int RANK, bool GATHER = false>
+// Where the first pass's tile comes from (k_onesweep SRC): TMA of keys and ids; the
+// walk's segment slots (list sort, pass 0); TMA of keys with ids = positions (array sort).
+enum : int { SRC_TMA = 0, SRC_GATHER = 1, SRC_IOTA = 2 };
+
+template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int SRC = SRC_TMA>
 __global__ void __launch_bounds__(SWEEP_THREADS, 2)
 k_onesweep(const __grid_constant__ SweepArgs a) {
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
@@ -619,15 +632,18 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 
   // ---- TMA bulk loads of the tile (sizes rounded up to 16 B; buffers padded to 256 B);
   // the first key pass gathers the tile from the segment slots instead
+  constexpr bool GATHER = SRC == SRC_GATHER;
   if (GATHER) gather_tile<KeyT, TILE>(a, tile, tile_base, tile_count, sm.k, sm.iin, w, lane);
   if (!GATHER && t == 0) {
     const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
-    const uint32_t ib = (tile_count * 4u + 15u) & ~15u;
+    const uint32_t ib = SRC == SRC_IOTA ? 0u : (tile_count * 4u + 15u) & ~15u;
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(kb + ib) : "memory");
     bulk_g2s(sm.k, kin + tile_base, kb, &sm.mbar);
-    bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
+    if (SRC != SRC_IOTA) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
   }
+  if (SRC == SRC_IOTA)
+    for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) sm.iin[j] = tile_base + j;
   for (uint32_t i = t; i < SWEEP_WARPS * RADIX * sizeof(WCnt) / 4; i += SWEEP_THREADS)
     reinterpret_cast<uint32_t*>(&sm.wcnt[0][0])[i] = 0;
   if (!GATHER) {
@@ -741,6 +757,53 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
       const uint32_t g = sm.goff[(uint32_t)sm.k[j]] + j;
       iout[g] = sm.iout[j];
     }
+  }
+}
+
+// ============================================================================ N3: array sort
+// pbit_sort_array -- the "table" of the paper's tables-vs-lists comparison:
+// the same stable passes over an array, with no ranking and no relink.
+// k_array_prep: user keys (any width) -> sort keys (KeyMap applied, widened to the pass
+// key type) + histograms of every digit (per-CTA smem).
+template <int KB>
+__global__ void __launch_bounds__(PACK_THREADS)
+k_array_prep(const void* __restrict__ keys, uint32_t n, typename KeyOf<KB>::T* __restrict__ kout,
+             uint32_t* __restrict__ hist, int K, int D, KeyMap km) {
+  using KT = std::conditional_t<KB == 1, uint8_t, std::conditional_t<KB == 2, uint16_t,
+             std::conditional_t<KB == 4, uint32_t, unsigned long long>>>;
+  extern __shared__ uint32_t s_hist[];
+  const int radix = 1 << K;
+  const int nb = D * radix;
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) s_hist[i] = 0;
+  __syncthreads();
+  const uint32_t mask = radix - 1;
+  const KT* __restrict__ kp = reinterpret_cast<const KT*>(keys);
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    unsigned long long k = __ldcs(kp + v);
+    if (!km.identity()) k = km(k, KB * 8);
+    kout[v] = (typename KeyOf<KB>::T)k;
+    for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nb; i += blockDim.x)
+    if (s_hist[i]) atomicAdd(&hist[i], s_hist[i]);
+}
+
+// out_keys[i] = the original bits of the i-th sorted key (inverse KeyMap, narrowed);
+// iota: out_index[i] = i (no pass ran: the input order is the sorted order).
+template <int KB>
+__global__ void __launch_bounds__(256)
+k_array_finish(const typename KeyOf<KB>::T* __restrict__ ksorted, uint32_t n, void* __restrict__ out_keys,
+               uint32_t* __restrict__ out_index, KeyMap km) {
+  using KT = std::conditional_t<KB == 1, uint8_t, std::conditional_t<KB == 2, uint16_t,
+             std::conditional_t<KB == 4, uint32_t, unsigned long long>>>;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (out_keys) {
+      unsigned long long k = ksorted[v];
+      if (!km.identity()) k = km.inverse(k, KB * 8);
+      reinterpret_cast<KT*>(out_keys)[v] = (KT)k;
+    }
+    if (out_index) out_index[v] = v;
   }
 }
 

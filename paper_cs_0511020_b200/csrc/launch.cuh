@@ -10,31 +10,32 @@
 namespace pbit {
 
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
-template <typename KeyT, int RB, int IPT, int RANK, bool GATHER>
+template <typename KeyT, int RB, int IPT, int RANK, int SRC>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
   static bool attr = false;  // benign race: idempotent
   if (!attr) {
-    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, GATHER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(S));
     attr = true;
   }
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  k_onesweep<KeyT, RB, IPT, RANK, GATHER><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
+  k_onesweep<KeyT, RB, IPT, RANK, SRC><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
 }
 
-template <typename KeyT, int RB, int IPT, bool GATHER = false>
+template <typename KeyT, int RB, int IPT, int SRC = SRC_TMA>
 static void launch_one(const SweepArgs& a, cudaStream_t st, int mode) {
-  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, GATHER>(a, st);
-  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, GATHER>(a, st);
-  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, GATHER>(a, st);
+  if (mode == RANK_ATOMIC) launch_one_m<KeyT, RB, IPT, RANK_ATOMIC, SRC>(a, st);
+  else if (mode == RANK_MATCH) launch_one_m<KeyT, RB, IPT, RANK_MATCH, SRC>(a, st);
+  else launch_one_m<KeyT, RB, IPT, RANK_BALLOT, SRC>(a, st);
 }
 
 // The key passes of a host-side plan: pass i sorts digit plan.digit[i] (slot i, its own
-// ticket counter and lookback epoch), reading buffer i & 1.
+// ticket counter and lookback epoch), reading buffer i & 1.  first_src: where pass 0's
+// tiles come from (SRC_*).  final_ids: if set, the last pass writes its ids there.
 template <int KB, int RB>
 static void launch_key_passes(SweepArgs a, const Plan& plan, bool keep_keys, cudaStream_t st, cudaEvent_t* ev,
-                              int ev_base, bool gather_first) {
+                              int ev_base, int first_src, uint32_t* final_ids = nullptr) {
   using KeyT = typename KeyOf<KB>::T;
   constexpr int IPT = (KB == 8) ? SWEEP_IPT64 : SWEEP_IPT32;
   for (uint32_t s = 0; s < plan.npasses; ++s) {
@@ -42,17 +43,20 @@ static void launch_key_passes(SweepArgs a, const Plan& plan, bool keep_keys, cud
     a.digit = (int)plan.digit[s];
     a.src = (int)(s & 1);
     a.last = (s + 1 == plan.npasses) && !keep_keys;
-    if (s == 0 && gather_first) launch_one<KeyT, RB, IPT, true>(a, st, rank_mode());
-    else launch_one<KeyT, RB, IPT, false>(a, st, rank_mode());
+    if (final_ids && s + 1 == plan.npasses) a.vout[a.src ^ 1] = final_ids;
+    const int src = s == 0 ? first_src : SRC_TMA;
+    if (src == SRC_GATHER) launch_one<KeyT, RB, IPT, SRC_GATHER>(a, st, rank_mode());
+    else if (src == SRC_IOTA) launch_one<KeyT, RB, IPT, SRC_IOTA>(a, st, rank_mode());
+    else launch_one<KeyT, RB, IPT, SRC_TMA>(a, st, rank_mode());
     if (ev) cudaEventRecord(ev[ev_base + s], st);
   }
 }
 
 template <int KB>
 static void launch_key_passes_k(int K, const SweepArgs& a, const Plan& plan, bool keep_keys, cudaStream_t st,
-                                cudaEvent_t* ev, int ev_base, bool gather_first) {
+                                cudaEvent_t* ev, int ev_base, int first_src, uint32_t* final_ids = nullptr) {
   switch (K) {
-#define PBIT_K(RB) case RB: launch_key_passes<KB, RB>(a, plan, keep_keys, st, ev, ev_base, gather_first); break;
+#define PBIT_K(RB) case RB: launch_key_passes<KB, RB>(a, plan, keep_keys, st, ev, ev_base, first_src, final_ids); break;
     PBIT_K(1) PBIT_K(2) PBIT_K(3) PBIT_K(4) PBIT_K(5) PBIT_K(6) PBIT_K(7) PBIT_K(8)
 #undef PBIT_K
   }

@@ -261,7 +261,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       Plan h_pp{};
       CUDACHK(cudaMemcpyAsync(&h_pp, plan_p, sizeof(Plan), cudaMemcpyDeviceToHost, st));
       CUDACHK(cudaStreamSynchronize(st));
-      if (m) { launch_key_passes_k<KB>(K, pa, h_pp, true, st, nullptr, 0, false); launches += h_pp.npasses; }
+      if (m) { launch_key_passes_k<KB>(K, pa, h_pp, true, st, nullptr, 0, SRC_TMA); launches += h_pp.npasses; }
       const int pa_par = (int)(h_pp.npasses & 1u);  // sorted chunk in kbuf/ibuf[pa_par]
       const KeyT* sk = kbuf[pa_par];
 
@@ -353,7 +353,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       la.kin[0] = kbuf[pb]; la.kin[1] = kbuf[pb ^ 1]; la.vin[0] = ibuf[pb]; la.vin[1] = ibuf[pb ^ 1];
       la.kout[0] = kbuf[pb]; la.kout[1] = kbuf[pb ^ 1]; la.vout[0] = ibuf[pb]; la.vout[1] = ibuf[pb ^ 1];
       la.bases = bases_l;
-      if (m) { launch_key_passes_k<KB>(K, la, h_pl, false, st, nullptr, 0, false); launches += h_pl.npasses; }
+      if (m) { launch_key_passes_k<KB>(K, la, h_pl, false, st, nullptr, 0, SRC_TMA); launches += h_pl.npasses; }
       fin[0] = ibuf[pb];
       fin[1] = ibuf[pb ^ 1];
     }

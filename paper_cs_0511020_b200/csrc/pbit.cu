@@ -302,7 +302,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   sa.tile_first = w.tile_first; sa.nseg = w.nseg;
   { const char* e = getenv("PBIT_DEBUG_NO_LOOKBACK"); sa.debug_no_lookback = e ? atoi(e) : 0; }
   if (ok) {
-    launch_key_passes_k<KB>(p.K, sa, hplan, false, st, timing ? ev : nullptr, PBIT_PHASE_PASS0, true);
+    launch_key_passes_k<KB>(p.K, sa, hplan, false, st, timing ? ev : nullptr, PBIT_PHASE_PASS0, SRC_GATHER);
     launches += hplan.npasses;
   }
   if (timing)
@@ -380,6 +380,104 @@ int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t 
     case 32: return run_device<4>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
     default: return run_device<8>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
   }
+}
+
+// ----------------------------------------------------------------------------- N3: arrays
+// pbit_sort_array on device pointers: prep (key map + histograms) -> plan -> passes (the
+// first generates the ids) -> the last pass writes out_index; out_keys by k_array_finish.
+template <int KB>
+static int run_array(const void* keys, uint32_t n, int key_bits, int K, KeyMap km, uint32_t* out_index,
+                     void* out_keys, cudaStream_t st, int sms, float* phase_ms, uint32_t* passes_run,
+                     uint32_t* launches_out) {
+  using KeyT = typename KeyOf<KB>::T;
+  const int radix = 1 << K, D = (key_bits + K - 1) / K;
+  const size_t tile = sweep_tile(key_bits), ntiles = (n + tile - 1) / tile;
+  const size_t kb = align_up((size_t)n * sizeof(KeyT) + 16), ib = align_up((size_t)n * 4 + 16);
+  const size_t status_bytes = ntiles * (radix > 256 ? radix : 256) * 8;
+  const size_t ctl_bytes = align_up((size_t)D * radix * 4) * 2 + align_up(sizeof(Plan)) + 256 + align_up(80 * 4);
+  char* base = nullptr;
+  if (cudaMallocAsync((void**)&base, 2 * kb + 2 * ib + align_up(status_bytes) + ctl_bytes, st) != cudaSuccess) {
+    cudaGetLastError();
+    return PBIT_ERR_OOM;
+  }
+  KeyT* kbuf[2] = {(KeyT*)base, (KeyT*)(base + kb)};
+  uint32_t* ibuf[2] = {(uint32_t*)(base + 2 * kb), (uint32_t*)(base + 2 * kb + ib)};
+  unsigned long long* status = (unsigned long long*)(base + 2 * kb + 2 * ib);
+  char* ctl = base + 2 * kb + 2 * ib + align_up(status_bytes);
+  uint32_t* hist = (uint32_t*)ctl;
+  uint32_t* bases = (uint32_t*)(ctl + align_up((size_t)D * radix * 4));
+  Plan* plan = (Plan*)(ctl + 2 * align_up((size_t)D * radix * 4));
+  int* err = (int*)((char*)plan + align_up(sizeof(Plan)));
+  uint32_t* tile_ctr = (uint32_t*)((char*)err + 256);
+
+  static thread_local cudaEvent_t ev_pool[64][PBIT_NUM_PHASES + 1];
+  static thread_local bool ev_ready[64] = {};
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  cudaEvent_t* ev = ev_pool[cur_dev & 63];
+  const bool timing = phase_ms != nullptr;
+  if (timing) {
+    if (!ev_ready[cur_dev & 63]) {
+      for (int i = 0; i <= PBIT_NUM_PHASES; ++i) cudaEventCreate(&ev[i]);
+      ev_ready[cur_dev & 63] = true;
+    }
+    cudaEventRecord(ev[PBIT_NUM_PHASES], st);
+  }
+  uint32_t launches = 0;
+  init_rank_mode(st);
+  cudaMemsetAsync(ctl, 0, ctl_bytes, st);
+  cudaMemsetAsync(status, 0, status_bytes, st);
+  {
+    const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
+    k_array_prep<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys, n, kbuf[0], hist, K, D, km);
+    k_plan<<<1, 256, 0, st>>>(hist, bases, plan, D, K, n, err);
+    launches += 2;
+  }
+  if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
+  Plan hplan{};
+  cudaMemcpyAsync(&hplan, plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
+  const bool synced = cudaStreamSynchronize(st) == cudaSuccess;
+  const int fblocks = std::max(1, std::min((int)((n + 255) / 256), sms * 8));
+  if (synced) {
+    if (hplan.npasses == 0) {  // one digit value everywhere: the input order is sorted
+      k_array_finish<KB><<<fblocks, 256, 0, st>>>(kbuf[0], n, out_keys, out_index, km);
+      ++launches;
+    } else {
+      SweepArgs sa{};
+      sa.kin[0] = kbuf[0]; sa.kin[1] = kbuf[1]; sa.vin[0] = ibuf[0]; sa.vin[1] = ibuf[1];
+      sa.kout[0] = kbuf[0]; sa.kout[1] = kbuf[1]; sa.vout[0] = ibuf[0]; sa.vout[1] = ibuf[1];
+      sa.bases = bases; sa.status = status; sa.tile_ctr = tile_ctr; sa.err = err; sa.n = n;
+      launch_key_passes_k<KB>(K, sa, hplan, out_keys != nullptr, st, timing ? ev : nullptr, PBIT_PHASE_PASS0,
+                              SRC_IOTA, out_index);
+      launches += hplan.npasses;
+      if (out_keys) {
+        k_array_finish<KB><<<fblocks, 256, 0, st>>>(kbuf[hplan.npasses & 1u], n, out_keys, nullptr, km);
+        ++launches;
+      }
+    }
+  }
+  if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
+  cudaFreeAsync(base, st);
+  const cudaError_t es = cudaStreamSynchronize(st);
+  const cudaError_t el = cudaGetLastError();
+  if (!synced || es || el) {
+    set_last_error("pbit_sort_array", cudaGetErrorString(es ? es : el));
+    return PBIT_ERR_CUDA;
+  }
+  if (timing) {
+    for (int i = 0; i < PBIT_NUM_PHASES; ++i) phase_ms[i] = 0.f;
+    auto el_ms = [&](cudaEvent_t a, cudaEvent_t b) { float ms = 0; cudaEventElapsedTime(&ms, a, b); return ms; };
+    phase_ms[PBIT_PHASE_PACK] = el_ms(ev[PBIT_NUM_PHASES], ev[PBIT_PHASE_PACK]);
+    cudaEvent_t a = ev[PBIT_PHASE_PACK];
+    for (uint32_t q = 0; q < hplan.npasses; ++q) {
+      phase_ms[PBIT_PHASE_PASS0 + q] = el_ms(a, ev[PBIT_PHASE_PASS0 + q]);
+      a = ev[PBIT_PHASE_PASS0 + q];
+    }
+    phase_ms[PBIT_PHASE_RELINK] = el_ms(a, ev[PBIT_PHASE_RELINK]);
+  }
+  if (passes_run) *passes_run = hplan.npasses;
+  if (launches_out) *launches_out = launches;
+  return PBIT_OK;
 }
 
 // pointer kind: 1 device (current device), 0 host (registered or pageable), -1 other device / error
@@ -463,6 +561,56 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
                             phase_ms, passes_run, launches);
   if (!rc && cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
   if (!rc && out_prev && cudaMemcpyAsync(out_prev, d_prev, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+  cudaFreeAsync(d, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = PBIT_ERR_CUDA;
+  cudaGetLastError();
+  return rc;
+}
+
+int pbit_sort_array(const void* keys, uint64_t n, int key_bits, uint32_t* out_index, void* out_keys,
+                    const pbit_opts* opts) {
+  if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
+  const int K = opts && opts->digit_bits ? opts->digit_bits : 8;
+  if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
+  if (n > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+  const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
+  if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
+  if (!out_index && !out_keys) return PBIT_ERR_INVALID_ARG;
+  cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
+  float* phase_ms = opts ? opts->phase_ms : nullptr;
+  uint32_t* passes_run = opts ? opts->passes_run : nullptr;
+  uint32_t* launches = opts ? opts->launches : nullptr;
+  if (passes_run) *passes_run = 0;
+  if (launches) *launches = 0;
+  if (n == 0) return PBIT_OK;
+  if (!keys) return PBIT_ERR_INVALID_ARG;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
+  int sms = 0;
+  if (int rc = device_info(dev, &sms)) return rc;
+  const int kk = pointer_kind(keys, dev);
+  const int ki = out_index ? pointer_kind(out_index, dev) : kk;
+  const int ko = out_keys ? pointer_kind(out_keys, dev) : kk;
+  if (kk < 0 || ki < 0 || ko < 0 || kk != ki || kk != ko) return PBIT_ERR_INVALID_ARG;
+  const uint32_t n32 = (uint32_t)n;
+  auto run = [&](const void* k, uint32_t* oi, void* ok) {
+    switch (key_bits) {
+      case 8: return run_array<1>(k, n32, 8, K, km, oi, ok, st, sms, phase_ms, passes_run, launches);
+      case 16: return run_array<2>(k, n32, 16, K, km, oi, ok, st, sms, phase_ms, passes_run, launches);
+      case 32: return run_array<4>(k, n32, 32, K, km, oi, ok, st, sms, phase_ms, passes_run, launches);
+      default: return run_array<8>(k, n32, 64, K, km, oi, ok, st, sms, phase_ms, passes_run, launches);
+    }
+  };
+  if (kk == 1) return run(keys, out_index, out_keys);
+  // host buffers: stage through device memory inside the call
+  const size_t kbytes = n * (size_t)(key_bits / 8), nbytes = n * 4;
+  char* d = nullptr;
+  const size_t a = align_up(kbytes), b = align_up(nbytes);
+  if (cudaMallocAsync((void**)&d, 2 * a + b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  int rc = cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ? PBIT_ERR_CUDA : PBIT_OK;
+  if (!rc) rc = run(d, out_index ? (uint32_t*)(d + 2 * a) : nullptr, out_keys ? d + a : nullptr);
+  if (!rc && out_index && cudaMemcpyAsync(out_index, d + 2 * a, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+  if (!rc && out_keys && cudaMemcpyAsync(out_keys, d + a, kbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
   cudaFreeAsync(d, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = PBIT_ERR_CUDA;
   cudaGetLastError();

@@ -318,3 +318,40 @@ def test_doubly_linked_host_buffers_and_args(pbit):
     with pytest.raises(pbit.PbitError) as e:  # out_prev aliasing out_next
         pbit.sort_list(k, nx, li.head, out_next=o, out_prev=o)
     assert e.value.code == 1
+
+
+# ---------------------------------------------------------------- arrays (NEXT row N3)
+def _array_oracle(keys_np, key_bits, kind="unsigned", desc=False):
+    """The oracle's Pbit on the array read as a list in array order (next[i] = i+1):
+    the sorted list order is the stable sorted order of the array."""
+    n = len(keys_np)
+    nxt = np.arange(1, n + 1, dtype=np.uint32)
+    if n:
+        nxt[-1] = NULL
+    h, out = oracle.pbit_sort(keys_np, nxt, 0 if n else NULL, key_bits, 4, descending=desc, kind=kind)
+    from tests.listcheck import walk
+    return np.array(walk(out, h), np.uint32)
+
+
+@pytest.mark.parametrize("n,key_bits,keys,kind,desc", [
+    (1, 32, "uniform", "unsigned", False), (7, 8, "uniform", "unsigned", True), (4097, 16, "uniform", "signed", False),
+    (100003, 32, "zipf", "unsigned", False), (100003, 32, "uniform", "float", True),
+    (70001, 64, "uniform", "signed", True), (70001, 64, "runs4096", "unsigned", False),
+    (65537, 32, "equal", "unsigned", False), (1000003, 32, "uniform", "unsigned", False)])
+def test_array_sort_vs_oracle(pbit, n, key_bits, keys, kind, desc):
+    li = workloads.make_list(n, key_bits, seed=n ^ 77, keys=keys, device="cuda")
+    idx, sk = pbit.sort_array(li.keys, key_bits=key_bits, want_keys=True, key_kind=kind, descending=desc)
+    torch.cuda.synchronize()
+    kn = workloads.keys_numpy(li)
+    want = _array_oracle(kn, key_bits, kind, desc)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), want)
+    assert np.array_equal(sk.cpu().numpy().view(kn.dtype), kn[want])
+
+
+@pytest.mark.parametrize("K", [1, 3, 4, 8])
+def test_array_digit_widths_and_host_buffers(pbit, K):
+    li = workloads.make_list(50001, 32, seed=3, keys="zipf", device="cpu")
+    kn = workloads.keys_numpy(li)
+    want = _array_oracle(kn, 32)
+    idx, _ = pbit.sort_array(kn, key_bits=32, digit_bits=K)  # numpy host buffers (staged)
+    assert np.array_equal(np.asarray(idx).view(np.uint32), want)
