@@ -181,7 +181,7 @@ def run_reference(args):
     value = sample_n / t
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "u32" if c["key_bits"] <= 32 else "u64",
+            "scaling": "strong", "vs_baseline": None, "dtype": "u32" if c["key_bits"] <= 32 else "u64",
             "data": "synthetic", "config": {"workload": args.config, "desc": c["desc"], "n": sample_n,
                                             "note": "bounded sample of the workload (oracle is single-threaded)"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
@@ -418,11 +418,11 @@ def run_ours(args):
     clocks = clk.summary()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u32" if kb <= 32 else "u64", "data": "synthetic",
                 "config": {"workload": args.config, "desc": c["desc"], "n_per_gpu": n, "key_bits": kb,
                            "digit_bits": K, "passes_run": passes_run,
-                           "parallelism": "independent lists per GPU" if ws > 1 else "single GPU",
+                           "parallelism": "single GPU (N > 1: one list over N ranks, pbit_sort_list_mg)",
                            "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6
                            else "inputs smaller than L2"},
                 "hbm_gbs_method": round(method_bytes_per_node(kb) * n * ws / (ms_max / 1e3) / 1e9, 1),
