@@ -201,6 +201,8 @@ def _run(G, n, key_bits, seed, keys_kind="uniform", links="random", K=8):
     (2, 2500, 32, "uniform", "random", 8),
     (2, 1000, 32, "equal", "random", 8),
     (3, 130, 8, "uniform", "identity", 4),
+    (4, 6007, 32, "zipf", "random", 8),
+    (4, 2048, 16, "equal", "push", 8),
 ])
 def test_mg_protocol_matches_oracle(G, n, key_bits, keys_kind, links, K):
     import oracle
