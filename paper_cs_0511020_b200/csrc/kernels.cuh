@@ -253,6 +253,39 @@ static __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, 
   }
 }
 
+// Small ruler lists (nsub <= RANK_SMALL): all pointer-jumping rounds in one CTA with the
+// arrays in shared memory (one launch instead of log2(nsub) + 1), then the check of
+// k_rank_check; results back in place (d, c, s).
+constexpr int RANK_SMALL = 6144;  // 2 x 6144 x 16 B = 192 KB of shared memory
+static __global__ void __launch_bounds__(1024)
+k_rank_jump_block(unsigned long long* __restrict__ d, uint32_t* __restrict__ c, uint32_t* __restrict__ s, uint32_t m,
+                  int rounds, uint32_t head_sub, uint32_t n, int* __restrict__ err) {
+  extern __shared__ __align__(16) unsigned char sraw[];
+  unsigned long long* sd = reinterpret_cast<unsigned long long*>(sraw);  // [2][RANK_SMALL]
+  uint32_t* sc = reinterpret_cast<uint32_t*>(sd + 2 * RANK_SMALL);      // [2][RANK_SMALL]
+  uint32_t* ss = sc + 2 * RANK_SMALL;                                   // [2][RANK_SMALL]
+  if (*err) return;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) { sd[i] = d[i]; sc[i] = c[i]; ss[i] = s[i]; }
+  __syncthreads();
+  int cur = 0;
+  for (int r = 0; r < rounds; ++r) {
+    const uint32_t a = cur * RANK_SMALL, b = (cur ^ 1) * RANK_SMALL;
+    for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const uint32_t nx = ss[a + i];
+      unsigned long long dd = sd[a + i];
+      uint32_t cc = sc[a + i], n2 = nx;
+      if (nx != PBIT_NULL32) { dd += sd[a + nx]; cc += sc[a + nx]; n2 = ss[a + nx]; }
+      sd[b + i] = dd; sc[b + i] = cc; ss[b + i] = n2;
+    }
+    cur ^= 1;
+    __syncthreads();
+  }
+  const uint32_t a = cur * RANK_SMALL;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) { d[i] = sd[a + i]; c[i] = sc[a + i]; s[i] = ss[a + i]; }
+  if (threadIdx.x == 0 && (ss[a + head_sub] != PBIT_NULL32 || sd[a + head_sub] != (unsigned long long)n))
+    atomicOr(err, E_CHAIN);
+}
+
 // Validation (reading Q10): the chain from the head must end (succ NULL) and hold exactly
 // n nodes; then every node lies on it.
 static __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const uint32_t* __restrict__ succ,

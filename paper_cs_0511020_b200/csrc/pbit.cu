@@ -57,17 +57,6 @@ int device_info(int dev, int* sms) {
   return PBIT_OK;
 }
 
-// L2 fetch granularity for the random-access phases (walk, relink): a random 8 B read
-// otherwise pulls a whole 128 B line from HBM (ncu: 4.2 DRAM sectors per node).
-static int l2_fetch_bytes() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("PBIT_L2_FETCH");
-    v = e ? atoi(e) : 32;
-  }
-  return v;
-}
-
 // ----------------------------------------------------------------------------- planning
 void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   p->n = (uint32_t)n;
@@ -79,7 +68,7 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   static int env_s = -2;
   if (env_s == -2) { const char* e = getenv("PBIT_RULER_LOG2"); env_s = e ? atoi(e) : -1; }
   int s_log2 = env_s > 0 ? env_s : 6;
-  while (s_log2 > 2 && (n >> s_log2) < (1u << 14)) --s_log2;
+  while (s_log2 > 2 && (n >> s_log2) < (1u << 13)) --s_log2;
   p->s_log2 = s_log2;
   p->cap = 4u << s_log2;
   p->R = (uint32_t)((n + (1ull << s_log2) - 1) >> s_log2);
@@ -212,7 +201,6 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   uint32_t launches = 0;
   init_rank_mode(st);
 
-  if (l2_fetch_bytes() > 0) cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)l2_fetch_bytes());
   cudaMemsetAsync(w.ctl, 0, w.ctl_bytes, st);
   cudaMemsetAsync(w.status, 0, w.status_bytes, st);
 
@@ -262,16 +250,28 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     while ((1ull << rounds) < nsub) ++rounds;
     rounds += 1;
     int cur = 0;
-    for (int i = 0; i < rounds; ++i) {
-      k_rank_jump<<<sblocks, 256, 0, st>>>(w.sdist[cur], w.scnt[cur], w.ssucc[cur], w.sdist[cur ^ 1],
-                                           w.scnt[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
-      cur ^= 1;
+    if (nsub <= (uint32_t)RANK_SMALL) {  // every round in one CTA (small lists: launch latency)
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(k_rank_jump_block, cudaFuncAttributeMaxDynamicSharedMemorySize, RANK_SMALL * 32);
+        attr = true;
+      }
+      k_rank_jump_block<<<1, 1024, RANK_SMALL * 32, st>>>(w.sdist[0], w.scnt[0], w.ssucc[0], nsub, rounds, head_sub,
+                                                          n, w.err);
+      launches += 1;
+    } else {
+      for (int i = 0; i < rounds; ++i) {
+        k_rank_jump<<<sblocks, 256, 0, st>>>(w.sdist[cur], w.scnt[cur], w.ssucc[cur], w.sdist[cur ^ 1],
+                                             w.scnt[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
+        cur ^= 1;
+      }
+      k_rank_check<<<1, 1, 0, st>>>(w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
+      launches += rounds + 1;
     }
-    k_rank_check<<<1, 1, 0, st>>>(w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
     k_rank_walk_b<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
                                            head_sub, w.sdist[cur], w.scnt[cur], w.dist, w.seg_ord, w.seg_pos,
                                            w.tile_first, (uint32_t)sweep_tile(p.key_bits), n, w.nseg, w.err);
-    launches += rounds + 3;
+    launches += 2;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
   }
   // a3: bucket bases + pass plan; the host reads {plan, error} once here, so every pass
