@@ -134,6 +134,17 @@ def dist_env():
     return ws, rank, local
 
 
+def bench_config(cfg: str, n: int, K: int, ws: int = 1) -> dict:
+    """The `config` object of the JSON line: identical for our arm and the reference arm."""
+    import workloads
+    c = workloads.CONFIGS[cfg]
+    kb = c["key_bits"]
+    return {"workload": cfg, "desc": c["desc"], "n_per_gpu": n, "key_bits": kb, "digit_bits": K,
+            "parallelism": "single GPU" if ws == 1 else f"one list, node ids sharded over {ws} ranks, "
+                                                         "key-range exchange (NCCL)",
+            "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6 else "inputs smaller than L2"}
+
+
 def cpu_baseline(cfg: str, sample_n: int, reps: int = 1):
     """The oracle as it stands (paper-literal Pbit, K=4, one thread) on a bounded
     sample of the workload."""
@@ -182,10 +193,12 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32" if c["key_bits"] <= 32 else "u64",
-            "data": "synthetic", "config": {"workload": args.config, "desc": c["desc"], "n": sample_n,
-                                            "note": "bounded sample of the workload (oracle is single-threaded)"},
+            "data": "synthetic",
+            "config": bench_config(args.config, c["n"] if args.n is None else args.n,
+                                   args.digit_bits or c["digit_bits"], args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": f"{args.config}-shaped list n={sample_n}, paper-literal Pbit K=4, "
+                             "sample": f"each step: a bounded sample of the workload, a {args.config}-shaped list "
+                                       f"of n={sample_n} sorted by the paper-literal Pbit (K=4) on one core; "
                                        f"{args.steps} timed steps"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -268,9 +281,7 @@ def run_mg(args):
         line = {"metric": METRIC, "value": n / (ms / 1e3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u32" if kb <= 32 else "u64", "data": "synthetic",
-                "config": {"workload": args.config, "desc": c["desc"], "n": n, "key_bits": kb, "digit_bits": K,
-                           "parallelism": f"one list, node ids sharded over {ws} ranks, key-range exchange (NCCL)",
-                           "l2": "inputs larger than L2 (no flush needed)"},
+                "config": bench_config(args.config, n, K, ws),
                 "roofline": {"bound": "hbm", "achieved": round(per_rank_gbs, 1), "peak": peak, "unit": "GB/s",
                              "frac": round(per_rank_gbs / peak, 4), "traffic": None,
                              "kernel": "pbit_sort_list_mg (whole call, method bytes per rank)",
@@ -420,11 +431,8 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "u32" if kb <= 32 else "u64", "data": "synthetic",
-                "config": {"workload": args.config, "desc": c["desc"], "n_per_gpu": n, "key_bits": kb,
-                           "digit_bits": K, "passes_run": passes_run,
-                           "parallelism": "single GPU (N > 1: one list over N ranks, pbit_sort_list_mg)",
-                           "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6
-                           else "inputs smaller than L2"},
+                "config": bench_config(args.config, n, K),
+                "passes_run": passes_run,
                 "hbm_gbs_method": round(method_bytes_per_node(kb) * n * ws / (ms_max / 1e3) / 1e9, 1),
                 "roofline": roofline, "whole_call_dram": whole, "array_sort": array_ctx, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (kb // 8 + 4),
