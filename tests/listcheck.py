@@ -97,7 +97,35 @@ def unsigned_order_key(keys, key_bits):
     return k ^ (-(1 << 63))
 
 
-def check_properties_torch(keys, key_bits, order, out_head, out_next):
+def order_key(keys, key_bits, kind="unsigned", descending=False):
+    """int64 tensor whose signed order is the requested order of the key bits:
+    unsigned; signed two's complement; IEEE 754 totalOrder for floats (sign-magnitude:
+    -NaN < -inf < .. < -0.0 < +0.0 < .. < +inf < +NaN, DESIGN.md reading Q18);
+    descending reverses it (bitwise not: no overflow)."""
+    import torch
+    u = unsigned_order_key(keys, key_bits)
+    if kind == "unsigned":
+        k = u
+    else:
+        b = keys.to(torch.int64)
+        if key_bits < 64:
+            b = b & ((1 << key_bits) - 1)
+            sign = 1 << (key_bits - 1)
+            if kind == "signed":
+                k = (b ^ sign) - sign
+            else:
+                mag = b & (sign - 1)
+                k = torch.where((b & sign) != 0, -mag - 1, mag)
+        else:
+            if kind == "signed":
+                k = b
+            else:
+                mag = b & ((1 << 63) - 1)
+                k = torch.where(b < 0, -mag - 1, mag)
+    return ~k if descending else k
+
+
+def check_properties_torch(keys, key_bits, order, out_head, out_next, kind="unsigned", descending=False):
     """Same proof as check_sorted_list_properties, with torch ops on the tensors'
     device (used for the full-size configs, up to 2^30 nodes)."""
     import torch
@@ -119,14 +147,14 @@ def check_properties_torch(keys, key_bits, order, out_head, out_next):
     assert int(cnt.max()) <= 1, "a node has two predecessors"
     assert 0 <= out_head < n and int(cnt[out_head]) == 0, "head has a predecessor"
     del cnt
-    k = unsigned_order_key(keys.to(dev), key_bits)
+    k = order_key(keys.to(dev), key_bits, kind, descending)
     kv, ks = k[v], k[s]
     ok = (kv < ks) | ((kv == ks) & (rank[v] < rank[s]))
     bad = int((~ok).sum())
     assert bad == 0, f"{bad} edges break (key, input-rank) order"
 
 
-def sampled_successors_torch(keys, key_bits, order, samples):
+def sampled_successors_torch(keys, key_bits, order, samples, kind="unsigned", descending=False):
     """The plain definition evaluated one output at a time: the successor of node v is
     the node with the smallest (key, input rank) above (key[v], rank[v])."""
     import torch
@@ -134,7 +162,7 @@ def sampled_successors_torch(keys, key_bits, order, samples):
     dev = keys.device
     rank = torch.empty(n, dtype=torch.int64, device=dev)
     rank[order.to(dev)] = torch.arange(n, device=dev)
-    k = unsigned_order_key(keys, key_bits)
+    k = order_key(keys, key_bits, kind, descending)
     out = []
     for v in samples:
         kv, rv = k[v], rank[v]

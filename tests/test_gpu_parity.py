@@ -355,3 +355,51 @@ def test_array_digit_widths_and_host_buffers(pbit, K):
     want = _array_oracle(kn, 32)
     idx, _ = pbit.sort_array(kn, key_bits=32, digit_bits=K)  # numpy host buffers (staged)
     assert np.array_equal(np.asarray(idx).view(np.uint32), want)
+
+
+# ---------------------------------------------------------------- N1-N3 at full BASELINE sizes (properties)
+@pytest.mark.parametrize("cfg,kind,desc", [("C3", "float", False), ("C4", "signed", True), ("C3", "unsigned", True)])
+def test_full_size_key_kinds(pbit, cfg, kind, desc):
+    c = workloads.CONFIGS[cfg]
+    li = workloads.make_config(cfg, device="cuda")
+    h, out = pbit.sort_list(li.keys, li.next, li.head, digit_bits=c["digit_bits"], key_kind=kind, descending=desc)
+    torch.cuda.synchronize()
+    check_properties_torch(li.keys, li.key_bits, li.order, h, out, kind=kind, descending=desc)
+    g = torch.Generator().manual_seed(2)
+    samples = torch.randint(0, li.n, (4,), generator=g).tolist() + [h]
+    want = sampled_successors_torch(li.keys, li.key_bits, li.order, samples, kind=kind, descending=desc)
+    assert [int(out[v]) & 0xFFFFFFFF for v in samples] == want
+    del li, out
+    torch.cuda.empty_cache()
+
+
+def test_full_size_doubly_linked_c3(pbit):
+    li = workloads.make_config("C3", device="cuda")
+    prev = torch.empty_like(li.next)
+    h, out = pbit.sort_list(li.keys, li.next, li.head, out_prev=prev)
+    torch.cuda.synchronize()
+    check_properties_torch(li.keys, li.key_bits, li.order, h, out)
+    on = out.to(torch.int64) & 0xFFFFFFFF
+    pv = prev.to(torch.int64) & 0xFFFFFFFF
+    has = on != NULL
+    v = torch.nonzero(has).squeeze(1)
+    assert bool((pv[on[v]] == v).all()), "prev[next[v]] != v"
+    assert int(pv[h]) == NULL and int((pv == NULL).sum()) == 1
+    del li, out, prev
+    torch.cuda.empty_cache()
+
+
+def test_full_size_array_c3(pbit):
+    li = workloads.make_config("C3", device="cuda")
+    idx, sk = pbit.sort_array(li.keys, want_keys=True)
+    torch.cuda.synchronize()
+    ix = idx.to(torch.int64) & 0xFFFFFFFF
+    n = li.n
+    assert int(torch.bincount(ix, minlength=n).max()) == 1, "index is not a permutation"
+    from tests.listcheck import order_key
+    k = order_key(li.keys, 32)[ix]
+    ok = (k[:-1] < k[1:]) | ((k[:-1] == k[1:]) & (ix[:-1] < ix[1:]))
+    assert bool(ok.all()), "array order not sorted/stable"
+    assert torch.equal(sk, li.keys[ix]), "sorted keys differ from keys[index]"
+    del li, idx, sk
+    torch.cuda.empty_cache()

@@ -421,3 +421,26 @@ def test_repair_back_after_sort_is_the_reverse_chain():
     w = walk(out, h)
     assert back[w[0]] == NULL
     assert all(back[b] == a for a, b in zip(w, w[1:]))
+
+
+def test_order_key_checker_matches_python_sort():
+    """The full-size checker's order key (tests/listcheck.order_key) against python's
+    sort of the values -- pins the checker used for N1 at full size."""
+    import torch
+    from tests.listcheck import order_key
+    rng = np.random.default_rng(12)
+    for bits, dt in ((16, np.float16), (32, np.float32), (64, np.float64)):
+        vals = np.concatenate([rng.normal(0, 10, 200), [0.0, -0.0, np.inf, -np.inf]]).astype(dt)
+        t = torch.from_numpy(vals.view({16: np.int16, 32: np.int32, 64: np.int64}[bits]).copy())
+        k = order_key(t, bits, "float").numpy()
+        want = sorted(range(len(vals)), key=lambda i: (float(vals[i]), 0 if np.signbit(vals[i]) else 1))
+        assert list(np.argsort(k, kind="stable")) == want
+        kd = order_key(t, bits, "float", descending=True).numpy()
+        assert list(np.argsort(kd, kind="stable")) == sorted(range(len(vals)), key=lambda i: (
+            -float(vals[i]), 0 if not np.signbit(vals[i]) else 1))
+    for bits, dt in ((8, np.int8), (32, np.int32), (64, np.int64)):
+        info = np.iinfo(dt)
+        vals = rng.integers(info.min, info.max, 300, dtype=dt, endpoint=True)
+        t = torch.from_numpy(vals.copy())
+        assert list(np.argsort(order_key(t, bits, "signed").numpy(), kind="stable")) == \
+            sorted(range(len(vals)), key=lambda i: int(vals[i]))
