@@ -104,8 +104,8 @@ typedef struct {
                         ids of the sorted list, out_prev[w_{i+1}] = w_i and
                         out_prev[w_0] = PBIT_NULL -- the paper's "reverse connection"
                         repair.  Same memory kind as out_next, must not
-                        alias it; pbit_sort_list only (the _mg call returns
-                        PBIT_ERR_UNSUPPORTED).  NULL = singly-linked.               */
+                        alias it; pbit_sort_list_mg: this rank's n_local predecessors
+                        (device).  NULL = singly-linked.                           */
 } pbit_opts;
 
 enum { PBIT_KEY_UNSIGNED = 0, PBIT_KEY_SIGNED = 1, PBIT_KEY_FLOAT = 2 };

@@ -248,7 +248,7 @@ def mg_exchange_plan(nranks: int, rank: int, n: int, slice_: int, lt, le):
 
 def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int, comm: int,
                  key_bits: int | None = None, digit_bits: int = 0, out_next_local=None, stream=None,
-                 key_kind: str = "unsigned", descending: bool = False):
+                 key_kind: str = "unsigned", descending: bool = False, out_prev_local=None):
     """Sort one list sharded over the ranks of `comm` (see include/pbit.h).  Returns
     (head, out_next_local)."""
     if key_bits is None:
@@ -259,6 +259,8 @@ def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int,
     oh = ctypes.c_uint32(0)
     launches = ctypes.c_uint32(0)
     o = _opts(digit_bits, _stream_handle(stream, True), None, None, ctypes.pointer(launches), key_kind, descending)
+    if out_prev_local is not None and n_local:
+        o.out_prev = ctypes.c_void_p(_ptr(out_prev_local))
     rc = lib.pbit_sort_list_mg(_ptr(keys_local) if n_local else None, _ptr(next_local) if n_local else None,
                                head & 0xFFFFFFFF, n_global, node_lo, n_local, key_bits, ctypes.byref(oh),
                                _ptr(out_next_local) if n_local else None, ctypes.c_void_p(comm), ctypes.byref(o))

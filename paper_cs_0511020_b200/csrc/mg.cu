@@ -67,8 +67,8 @@ struct Bump {
 
 template <int KB>
 int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint32_t n, uint32_t S,
-           uint32_t n_local, int K, KeyMap km, uint32_t* out_head, uint32_t* out_next_local, ncclComm_t comm,
-           int G, int r, cudaStream_t st, uint32_t* launches_out) {
+           uint32_t n_local, int K, KeyMap km, uint32_t* out_head, uint32_t* out_next_local,
+           uint32_t* out_prev_local, ncclComm_t comm, int G, int r, cudaStream_t st, uint32_t* launches_out) {
   using RT = typename Rec<KB>::T;
   uint32_t launches = 0;
   using KeyT = typename KeyOf<KB>::T;
@@ -119,7 +119,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   std::vector<uint32_t> h_counts, h_cntall;
   Plan h_plan{};
   int h_err = 0;
-  uint32_t h_firsts[65];
+  uint32_t h_firsts[130];  // first and last sorted id of every rank
   auto carve = [&]() {
     kn = b.take<RT>((size_t)G * S);
     seg = b.take<uint2>(Rmax);
@@ -147,7 +147,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     bases_l = b.take<uint32_t>((size_t)D * radix);
     cursors = b.take<uint32_t>(relink_cursor_words(S));
     cntmat = b.take<uint32_t>((size_t)G * radix);
-    firsts = b.take<uint32_t>(G + 1);
+    firsts = b.take<uint32_t>(2 * G + 2);
     cnt = b.take<uint32_t>(G);
     offs = b.take<uint32_t>(G);
     fill = b.take<uint32_t>(G);
@@ -358,34 +358,44 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       fin[1] = ibuf[pb ^ 1];
     }
 
-    // ---- 7. stitch and relink
+    // ---- 7. stitch and relink: every rank's first and last sorted id (all-gather), then
+    // (v, successor) -- and, for out_prev, (v, predecessor) -- routed to the owner of v
     ++launches;
-    k_first_id<<<1, 1, 0, st>>>(final_plan, fin[0], fin[1], m, firsts + G);
-    NCCLCHK(ncclAllGather(firsts + G, firsts, 1, ncclUint32, comm, st));
-    CUDACHK(cudaMemcpyAsync(h_firsts, firsts, 4ull * G, cudaMemcpyDeviceToHost, st));
+    k_first_last_id<<<1, 1, 0, st>>>(final_plan, fin[0], fin[1], m, firsts + 2 * G);
+    NCCLCHK(ncclAllGather(firsts + 2 * G, firsts, 2, ncclUint32, comm, st));
+    CUDACHK(cudaMemcpyAsync(h_firsts, firsts, 8ull * G, cudaMemcpyDeviceToHost, st));
     CUDACHK(cudaStreamSynchronize(st));
-    uint32_t next_rank = PBIT_NULL32;
-    for (int d = r + 1; d < G; ++d)
-      if (h_firsts[d] != PBIT_NULL32) { next_rank = d; break; }
-    const int pblocks = std::max(1, std::min((int)((m + 4095) / 4096), sms * 4));
-    if (m) {
-      ++launches;
-      k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, next_rank, firsts, S, G, cnt, nullptr,
-                                             nullptr, nullptr, 0, err);
-    }
-    NCCLCHK(ncclAllGather(cnt, cntall, G, ncclUint32, comm, st));
-    h_cntall.resize((size_t)G * G);
-    CUDACHK(cudaMemcpyAsync(h_cntall.data(), cntall, 4ull * G * G, cudaMemcpyDeviceToHost, st));
-    CUDACHK(cudaStreamSynchronize(st));
-    {
+    for (int dir = 1; dir >= -1; dir -= 2) {
+      uint32_t* out_local = dir > 0 ? out_next_local : out_prev_local;
+      if (!out_local) continue;
+      uint32_t edge = PBIT_NULL32;  // next rank's first id / previous rank's last id
+      if (dir > 0) {
+        for (int d = r + 1; d < G; ++d)
+          if (h_firsts[2 * d] != PBIT_NULL32) { edge = h_firsts[2 * d]; break; }
+      } else {
+        for (int d = r - 1; d >= 0; --d)
+          if (h_firsts[2 * d + 1] != PBIT_NULL32) { edge = h_firsts[2 * d + 1]; break; }
+      }
+      CUDACHK(cudaMemsetAsync(cnt, 0, 4ull * G, st));
+      CUDACHK(cudaMemsetAsync(fill, 0, 4ull * G, st));
+      const int pblocks = std::max(1, std::min((int)((m + 4095) / 4096), sms * 4));
+      if (m) {
+        ++launches;
+        k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, edge, dir, S, G, cnt, nullptr,
+                                               nullptr, nullptr, 0, err);
+      }
+      NCCLCHK(ncclAllGather(cnt, cntall, G, ncclUint32, comm, st));
+      h_cntall.resize((size_t)G * G);
+      CUDACHK(cudaMemcpyAsync(h_cntall.data(), cntall, 4ull * G * G, cudaMemcpyDeviceToHost, st));
+      CUDACHK(cudaStreamSynchronize(st));
       std::vector<uint32_t> h_offs(G);
       uint32_t acc = 0;
       for (int d = 0; d < G; ++d) { h_offs[d] = acc; acc += h_cntall[(size_t)r * G + d]; }
       CUDACHK(cudaMemcpyAsync(offs, h_offs.data(), 4ull * G, cudaMemcpyHostToDevice, st));
       if (m) {
         ++launches;
-        k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, next_rank, firsts, S, G, nullptr,
-                                               offs, fill, send_p, 1, err);
+        k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, edge, dir, S, G, nullptr, offs, fill,
+                                               send_p, 1, err);
       }
       uint32_t racc = 0;
       NCCLCHK(ncclGroupStart());
@@ -397,14 +407,17 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       }
       NCCLCHK(ncclGroupEnd());
       if (racc != n_local) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
-      // the received pairs (global v): out_next[v - lo] = succ for every own id v, in any order
-      if (n_local) launches += launch_relink(nullptr, pr[1], lo, n_local, pr[0], pr[1], cursors, out_next_local, err, st, sms);
+      // the received pairs (global v): out[v - lo] = w for every own id v, in any order
+      if (n_local) {
+        CUDACHK(cudaMemsetAsync(cursors, 0, relink_cursor_words(S) * 4, st));
+        launches += launch_relink(nullptr, pr[1], lo, n_local, pr[0], pr[1], cursors, out_local, err, st, sms);
+      }
     }
     CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
     CUDACHK(cudaStreamSynchronize(st));
     CUDACHK(cudaGetLastError());
     if (h_err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
-    *out_head = h_firsts[0];
+    *out_head = h_firsts[0];  // rank 0 always holds sorted position 0 (n > 0)
     if (launches_out) *launches_out = launches;
   }
 done:
@@ -497,7 +510,8 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
   int K = opts && opts->digit_bits ? opts->digit_bits : 8;
   if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
   if (n_global > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
-  if (opts && opts->out_prev) return PBIT_ERR_UNSUPPORTED;  // N2 is single-GPU only (pbit.h)
+  uint32_t* out_prev_local = opts ? opts->out_prev : nullptr;
+  if (out_prev_local && out_prev_local == out_next_local) return PBIT_ERR_INVALID_ARG;
   const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
   if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
   cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
@@ -520,20 +534,21 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
   if (n_local && (pointer_kind(keys_local, dev) != 1 || pointer_kind(next_local, dev) != 1 ||
-                  pointer_kind(out_next_local, dev) != 1))
+                  pointer_kind(out_next_local, dev) != 1 ||
+                  (out_prev_local && pointer_kind(out_prev_local, dev) != 1)))
     return PBIT_ERR_INVALID_ARG;
   switch (key_bits) {
     case 8: return run_mg<1>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                             out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                             out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
     case 16: return run_mg<2>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                              out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
     case 32: return run_mg<4>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                              out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
     default: return run_mg<8>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                              out_head, out_next_local, (ncclComm_t)nccl_comm, G, r, st,
+                              out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
                              opts ? opts->launches : nullptr);
   }
 }

@@ -142,18 +142,19 @@ __global__ void k_count_below(const KeyT* __restrict__ keys, uint32_t m, const u
   }
 }
 
-// (v, succ) pairs of this rank's sorted positions, counted (pass 0) or scattered (pass 1)
-// by the owner rank of v: owner = v / S.  succ of the last position = `next_first`.
+// (v, w) pairs of this rank's sorted positions, counted (pass 0) or scattered (pass 1) by
+// the owner rank of v: owner = v / S.  dir +1: w = the successor (`edge` = the next rank's
+// first id, or NULL, after the last position); dir -1: w = the predecessor (`edge` = the
+// previous rank's last id, or NULL, before the first position) -- out_prev (N2).
 static __global__ void __launch_bounds__(256)
 k_pairs_owner(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, const uint32_t* __restrict__ ids1,
-              uint32_t m, uint32_t next_first_dev_idx, const uint32_t* __restrict__ firsts, uint32_t S, int G,
-              uint32_t* __restrict__ counts, const uint32_t* __restrict__ offsets, uint32_t* __restrict__ fill,
-              uint2* __restrict__ send, int scatter, const int* __restrict__ err) {
+              uint32_t m, uint32_t edge, int dir, uint32_t S, int G, uint32_t* __restrict__ counts,
+              const uint32_t* __restrict__ offsets, uint32_t* __restrict__ fill, uint2* __restrict__ send, int scatter,
+              const int* __restrict__ err) {
   __shared__ uint32_t s_cnt[64];
   __shared__ uint32_t s_base[64];
   if (*err) return;
   const uint32_t* __restrict__ ids = (plan->npasses & 1) ? ids1 : ids0;
-  const uint32_t next_first = next_first_dev_idx == PBIT_NULL32 ? PBIT_NULL32 : firsts[next_first_dev_idx];
   for (int g = threadIdx.x; g < G; g += blockDim.x) s_cnt[g] = 0;
   __syncthreads();
   const uint32_t per = (m + gridDim.x - 1) / gridDim.x;
@@ -172,18 +173,21 @@ k_pairs_owner(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0, 
   __syncthreads();
   for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
     const uint32_t v = ids[p];
-    const uint32_t s = p + 1 < m ? ids[p + 1] : next_first;
+    const uint32_t w = dir > 0 ? (p + 1 < m ? ids[p + 1] : edge) : (p > 0 ? ids[p - 1] : edge);
     const uint32_t o = v / S;
     const uint32_t at = s_base[o] + atomicAdd(&s_cnt[o], 1u);
-    send[at] = make_uint2(v, s);
+    send[at] = make_uint2(v, w);
   }
 }
 
-// The first sorted id of this rank (or NULL when it holds no position), for the stitch.
-static __global__ void k_first_id(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
-                           const uint32_t* __restrict__ ids1, uint32_t m, uint32_t* __restrict__ out) {
+// The first and the last sorted id of this rank (NULL when it holds no position), for
+// the stitch: out[0] = first, out[1] = last.
+static __global__ void k_first_last_id(const Plan* __restrict__ plan, const uint32_t* __restrict__ ids0,
+                                       const uint32_t* __restrict__ ids1, uint32_t m, uint32_t* __restrict__ out) {
   const uint32_t* ids = (plan->npasses & 1) ? ids1 : ids0;
-  *out = m ? ids[0] : PBIT_NULL32;
+  out[0] = m ? ids[0] : PBIT_NULL32;
+  out[1] = m ? ids[m - 1] : PBIT_NULL32;
 }
+
 
 }  // namespace pbit

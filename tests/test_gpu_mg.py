@@ -87,15 +87,14 @@ def test_mg_key_kinds(mg, kind, desc):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), on)
 
 
-def test_mg_out_prev_unsupported(mg):
+@pytest.mark.parametrize("n,key_bits,keys", [(1, 32, "uniform"), (1000, 32, "zipf"), (200001, 64, "uniform")])
+def test_mg_out_prev(mg, n, key_bits, keys):
+    """N2 through the multi-GPU protocol (1 rank): out_prev = the oracle's repair walk."""
     p, comm = mg
-    li = workloads.make_list(1000, 32, seed=3, device="cuda")
-    import ctypes
-    o = p._opts(0, 0, None, None, None)
+    li = workloads.make_list(n, key_bits, seed=n + 9, keys=keys, device="cuda")
     prev = torch.empty_like(li.next)
-    o.out_prev = ctypes.c_void_p(prev.data_ptr())
-    out = torch.empty_like(li.next)
-    oh = ctypes.c_uint32(0)
-    rc = p.lib.pbit_sort_list_mg(li.keys.data_ptr(), li.next.data_ptr(), li.head, li.n, 0, li.n, 32,
-                                 ctypes.byref(oh), out.data_ptr(), ctypes.c_void_p(comm), ctypes.byref(o))
-    assert rc == 6  # PBIT_ERR_UNSUPPORTED
+    h, out = p.sort_list_mg(li.keys, li.next, li.head, n, 0, comm, out_prev_local=prev)
+    torch.cuda.synchronize()
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4)
+    assert h == oh and np.array_equal(out.cpu().numpy().view(np.uint32), on)
+    assert np.array_equal(prev.cpu().numpy().view(np.uint32), oracle.repair_back(on, oh))

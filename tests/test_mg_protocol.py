@@ -7,8 +7,9 @@ for the device kernels, and the product's own host-side exchange planner
   1 own id slice -> replica (all_gather)         4 chunk of own list positions
   5 top non-trivial digit: stable local pass, count matrix (all_gather), planner,
     point-to-point exchange, receive buffers concatenated in source-rank order
-  6 stable local sort                              7 stitch (all_gather of first ids),
-    (v, succ) routed to the owner of v, applied to the owner's out_next slice.
+  6 stable local sort                              7 stitch (all_gather of first and last ids),
+    (v, succ) and (v, pred) routed to the owner of v, applied to the owner's out_next /
+    out_prev slices.
 The assembled out_next must equal the paper-literal oracle bit for bit."""
 from __future__ import annotations
 
@@ -142,16 +143,23 @@ def _rank_main(rank, G, port, n, key_bits, seed, keys_kind, links, K, out_q):
             # 6. stable sort of the received runs (source order = position order for ties)
             perm = np.argsort(ck, kind="stable")
             ck, ids = ck[perm], ids[perm]
-        # ---- 7. stitch and route (v, succ) to the owner of v
-        first = torch.tensor([int(ids[0]) if len(ids) else NULL], dtype=torch.int64)
-        firsts = [torch.empty(1, dtype=torch.int64) for _ in range(G)]
-        dist.all_gather(firsts, first)
-        firsts = [int(f[0]) for f in firsts]
+        # ---- 7. stitch (all_gather of every rank's first and last sorted id) and route
+        # (v, succ) -- and (v, pred) for out_prev -- to the owner of v
+        fl = torch.tensor([int(ids[0]) if len(ids) else NULL, int(ids[-1]) if len(ids) else NULL],
+                          dtype=torch.int64)
+        fls = [torch.empty(2, dtype=torch.int64) for _ in range(G)]
+        dist.all_gather(fls, fl)
+        firsts = [int(f[0]) for f in fls]
+        lasts = [int(f[1]) for f in fls]
         nxt = next((firsts[d] for d in range(rank + 1, G) if firsts[d] != NULL), NULL)
+        prv = next((lasts[d] for d in range(rank - 1, -1, -1) if lasts[d] != NULL), NULL)
         succ = np.empty(len(ids), np.uint32)
+        pred = np.empty(len(ids), np.uint32)
         if len(ids):
             succ[:-1] = ids[1:]
             succ[-1] = nxt
+            pred[1:] = ids[:-1]
+            pred[0] = prv
         owner = (ids // S).astype(np.int64) if len(ids) else np.zeros(0, np.int64)
         cnt_out = np.bincount(owner, minlength=G)
         tc = torch.from_numpy(cnt_out.astype(np.int64))
@@ -159,17 +167,19 @@ def _rank_main(rank, G, port, n, key_bits, seed, keys_kind, links, K, out_q):
         dist.all_gather(allc, tc)
         cnt_in = np.array([int(allc[q][rank]) for q in range(G)])
         vv = [ids[owner == d].view(np.int32) for d in range(G)]
-        ss = [succ[owner == d].view(np.int32) for d in range(G)]
         rv = np.concatenate([x.view(np.uint32) for x in _exchange(vv, cnt_out, cnt_in, rank, G, torch.int32)])
-        rs = np.concatenate([x.view(np.uint32) for x in _exchange(ss, cnt_out, cnt_in, rank, G, torch.int32)])
         assert len(rv) == hi - lo
-        out_local = np.full(S, NULL, np.uint32)
-        out_local[rv - lo] = rs
-        outs = [torch.empty(S, dtype=torch.int32) for _ in range(G)]
-        dist.all_gather(outs, torch.from_numpy(out_local.view(np.int32)))
+        full = []
+        for w_ in (succ, pred):
+            ss = [w_[owner == d].view(np.int32) for d in range(G)]
+            rs = np.concatenate([x.view(np.uint32) for x in _exchange(ss, cnt_out, cnt_in, rank, G, torch.int32)])
+            out_local = np.full(S, NULL, np.uint32)
+            out_local[rv - lo] = rs
+            outs = [torch.empty(S, dtype=torch.int32) for _ in range(G)]
+            dist.all_gather(outs, torch.from_numpy(out_local.view(np.int32)))
+            full.append(np.concatenate([o.numpy().view(np.uint32) for o in outs])[:n])
         if rank == 0:
-            out_next = np.concatenate([o.numpy().view(np.uint32) for o in outs])[:n]
-            out_q.put(("ok", firsts[0], out_next))
+            out_q.put(("ok", firsts[0], (full[0], full[1])))
     except Exception as e:  # pragma: no cover - reported to the parent
         import traceback
         out_q.put(("error", traceback.format_exc(), None))
@@ -207,11 +217,12 @@ def _run(G, n, key_bits, seed, keys_kind="uniform", links="random", K=8):
 def test_mg_protocol_matches_oracle(G, n, key_bits, keys_kind, links, K):
     import oracle
     import workloads
-    head, out_next = _run(G, n, key_bits, seed=n + G, keys_kind=keys_kind, links=links, K=K)
+    head, (out_next, out_prev) = _run(G, n, key_bits, seed=n + G, keys_kind=keys_kind, links=links, K=K)
     li = workloads.make_list(n, key_bits, n + G, keys=keys_kind, links=links)
     oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4)
     assert head == oh
     assert np.array_equal(out_next, on)
+    assert np.array_equal(out_prev, oracle.repair_back(on, oh))  # N2 across ranks
 
 
 def test_exchange_plan_is_position_exact():
