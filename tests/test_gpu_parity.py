@@ -403,3 +403,25 @@ def test_full_size_array_c3(pbit):
     assert torch.equal(sk, li.keys[ix]), "sorted keys differ from keys[index]"
     del li, idx, sk
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- extreme digit plans
+@pytest.mark.parametrize("key_bits,K", [(64, 1), (64, 7), (32, 1), (16, 3), (8, 1), (64, 2)])
+def test_extreme_digit_plans(pbit, key_bits, K):
+    """Up to 64 passes (u64 keys, K = 1: the most the plan holds), narrow top digits."""
+    li = workloads.make_list(5003, key_bits, seed=key_bits * 10 + K, keys="uniform", device="cuda")
+    h, out, ph = pbit.sort_list(li.keys, li.next, li.head, digit_bits=K, timing=True)
+    torch.cuda.synchronize()
+    assert ph["passes_run"] == (key_bits + K - 1) // K
+    _assert_same((h, out.cpu().numpy().view(np.uint32)), _oracle(li), f"u{key_bits} K={K}")
+    idx, _ = pbit.sort_array(li.keys, key_bits=key_bits, digit_bits=K)
+    torch.cuda.synchronize()
+    kn = workloads.keys_numpy(li)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), np.argsort(kn, kind="stable").astype(np.uint32))
+
+
+def test_head_positions_and_tiny_lists(pbit):
+    """Every head position of small lists, n around the tile and window sizes."""
+    for n in (2, 3, 17, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385):
+        li = workloads.make_list(n, 32, seed=n, keys="zipf", links="random", device="cuda")
+        _assert_same(_gpu_sort(pbit, li), _oracle(li), f"n={n}")
