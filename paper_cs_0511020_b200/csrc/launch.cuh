@@ -3,22 +3,32 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 
 #include "kernels.cuh"
 #include "pbit_internal.h"
 
 namespace pbit {
 
+// cudaFuncSetAttribute is per device: true the first time a call site runs on the current
+// device (one bit per device), so multi-GPU processes set every kernel attribute everywhere.
+static inline bool first_use_on_device(std::atomic<unsigned long long>& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask.load(std::memory_order_relaxed) & bit) return false;
+  mask.fetch_or(bit);
+  return true;  // idempotent if two threads race here
+}
+
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
 template <typename KeyT, int RB, int IPT, int RANK, int SRC>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
-  static bool attr = false;  // benign race: idempotent
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_use_on_device(attr))
     cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(S));
-    attr = true;
-  }
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
   k_onesweep<KeyT, RB, IPT, RANK, SRC><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
 }
@@ -79,13 +89,12 @@ static inline size_t relink_cursor_words(uint32_t n) {
 static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t v_off, uint32_t n, uint2* pbuf0,
                               uint2* pbuf1, uint32_t* cursors, uint32_t* out_next, const int* err, cudaStream_t st,
                               int sms, int dir = 1) {
-  static bool attr = false;  // benign race: idempotent
-  if (!attr) {
+  static std::atomic<unsigned long long> attr{0};
+  if (first_use_on_device(attr)) {
     cudaFuncSetAttribute(k_relink_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
     cudaFuncSetAttribute(k_relink_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
     cudaFuncSetAttribute(k_relink_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
     cudaFuncSetAttribute(k_relink_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
-    attr = true;
   }
   if (n == 0) return 0;
   RelinkLevels lv(n);

@@ -251,11 +251,9 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     rounds += 1;
     int cur = 0;
     if (nsub <= (uint32_t)RANK_SMALL) {  // every round in one CTA (small lists: launch latency)
-      static bool attr = false;
-      if (!attr) {
+      static std::atomic<unsigned long long> attr{0};
+      if (first_use_on_device(attr))
         cudaFuncSetAttribute(k_rank_jump_block, cudaFuncAttributeMaxDynamicSharedMemorySize, RANK_SMALL * 32);
-        attr = true;
-      }
       k_rank_jump_block<<<1, 1024, RANK_SMALL * 32, st>>>(w.sdist[0], w.scnt[0], w.ssucc[0], nsub, rounds, head_sub,
                                                           n, w.err);
       launches += 1;
