@@ -610,10 +610,9 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
           const uint4* rec = reinterpret_cast<const uint4*>(a.slots) + (size_t)sr * a.cap + (x - sp);
           cp_async8(sk + (x - P), &rec->x);
           cp_async4(sv + (x - P), &rec->z);
-        } else {
+        } else {  // one 8 B copy of the whole record into the AoS tile (k_onesweep AOS)
           const uint2* rec = reinterpret_cast<const uint2*>(a.slots) + (size_t)sr * a.cap + (x - sp);
-          cp_async4(sk + (x - P), &rec->x);
-          cp_async4(sv + (x - P), &rec->y);
+          cp_async8(reinterpret_cast<uint2*>(sk) + (x - P), rec);
         }
       }
     }
@@ -689,12 +688,15 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   }
   __syncthreads();
 
-  // ---- stable in-warp ranking
+  // ---- stable in-warp ranking.  AOS (pass 0 with keys <= 32 bits): the gather copied
+  // whole (key, id) records into the k and iin buffers viewed as one uint2 array
+  constexpr bool AOS = GATHER && sizeof(KeyT) == 4;
+  const uint2* __restrict__ srec = reinterpret_cast<const uint2*>(sm.k);
   const uint32_t wofs = w * WARP_ITEMS;
   KeyT key[IPT];
   uint32_t rd[IPT];
 #pragma unroll
-  for (int i = 0; i < IPT; ++i) key[i] = sm.k[wofs + i * 32 + lane];
+  for (int i = 0; i < IPT; ++i) key[i] = AOS ? (KeyT)srec[wofs + i * 32 + lane].x : sm.k[wofs + i * 32 + lane];
   if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
   else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
   __syncthreads();
@@ -733,14 +735,34 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 
   // ---- stage in (digit, input order) order: keys from registers into sm.k (every warp
   // read its keys before the barriers above), values from sm.iin into sm.iout
+  if constexpr (AOS) {
+    // ids first (they live in the records the keys will overwrite), then the keys
 #pragma unroll
-  for (int i = 0; i < IPT; ++i) {
-    const uint32_t j = wofs + i * 32 + lane;
-    if (full_tile || j < tile_count) {
-      const uint32_t d = rd[i] >> 16;
-      const uint32_t lp = sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
-      sm.iout[lp] = sm.iin[j];
-      sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass needs only digits
+    for (int i = 0; i < IPT; ++i) {
+      const uint32_t j = wofs + i * 32 + lane;
+      if (full_tile || j < tile_count) {
+        const uint32_t d = rd[i] >> 16;
+        const uint32_t lp = sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
+        sm.iout[lp] = srec[j].y;
+        rd[i] = lp | (d << 16);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const uint32_t j = wofs + i * 32 + lane;
+      if (full_tile || j < tile_count) sm.k[rd[i] & 0xFFFFu] = last ? (KeyT)(rd[i] >> 16) : key[i];
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const uint32_t j = wofs + i * 32 + lane;
+      if (full_tile || j < tile_count) {
+        const uint32_t d = rd[i] >> 16;
+        const uint32_t lp = sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
+        sm.iout[lp] = sm.iin[j];
+        sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass needs only digits
+      }
     }
   }
 
