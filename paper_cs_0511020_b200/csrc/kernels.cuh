@@ -1,14 +1,20 @@
 // kernels.cuh -- the sm_100a kernels of the Pbit hot path.
 //
-//   k_pack      a1/a2  AoS (key,next) records + histograms of every digit (one sweep)
+//   k_pack      a1/a2  AoS (key,next) records + histograms of every digit (one sweep);
+//                      applies the key-order map (signed / float / descending, N1)
 //   k_walk      a1     ruling-set walk: every segment written in list order to its slot
-//   k_rank_*    a1     ruler-list ranking by pointer jumping; validates the chain
-//   k_gather    a1     segments -> list-order (key, id) arrays
+//   k_rank_*    a1     ruler-list ranking (second ruling set + pointer jumping);
+//                      validates the chain
+//   k_gather    a1     segments -> list-order (key, id) arrays (only when no pass runs;
+//                      otherwise pass 0 gathers its tiles itself)
 //   k_plan      a3     exclusive scans of the digit histograms -> bucket bases, pass plan
-//   k_onesweep  a3/a4  one stable LSD pass: TMA tile loads, warp-ballot ranking,
-//                      decoupled lookback, smem-staged coalesced scatter
-//   k_relink_*  a5     out_next from the sorted ids (the paper's merge),
-//                      binned so every write lands in an L2-resident window
+//   k_onesweep  a3/a4  one stable LSD pass: TMA tile loads, in-warp ranking (lane-ordered
+//                      shared atomics, or ballots), decoupled lookback, smem-staged
+//                      coalesced scatter
+//   k_relink_*  a5     out_next (and out_prev, N2) from the sorted ids (the paper's merge,
+//                      P:273-280): (v, succ) pairs binned by v in MSD partition levels,
+//                      applied in shared-memory windows
+//   k_array_*   N3     pbit_sort_array's prep (key map + histograms) and finish
 //
 // Paper anchors: the split loop is the stable scatter; the end-marker
 // recursion is the ascending order of the bucket bases; merge is relink.

@@ -1,10 +1,12 @@
 // pbit.cu -- host orchestrator + C-ABI entry of the single-GPU Pbit list sort.
 //
 // pbit_sort_list (include/pbit.h) runs, on the caller's stream:
-//   k_pack -> k_walk -> k_rank_init/k_rank_jump^r/k_rank_check -> k_gather -> k_plan
-//   -> k_onesweep x D (trivial digits exit at once) -> k_relink
-// then one small D2H of {head, error} and a stream sync.  No host round-trip sits
-// between kernels: the pass plan lives on the device.
+//   k_pack -> k_walk -> k_rank_walk_a, k_rank_jump^r (or k_rank_jump_block), k_rank_walk_b
+//   -> k_plan -> [host reads the pass plan: one small D2H + sync]
+//   -> k_onesweep per non-trivial digit (the first gathers from the walk's slots;
+//      k_gather only when no pass runs) -> k_relink_part per level -> k_relink_apply
+// then one small D2H of {head, error, passes} and a stream sync.  pbit_sort_array
+// (the "table" of P:1118-1177) runs k_array_prep -> k_plan -> the passes.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
