@@ -10,7 +10,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpbit.so")
 SOURCES = ["pbit.cu", "mg.cu"]
-HEADERS = ["common.cuh", "kernels.cuh", "pbit_internal.h", "launch.cuh", "mg_kernels.cuh"]
+HEADERS = ["common.cuh", "kernels.cuh", "pbit_internal.h", "launch.cuh", "mg_kernels.cuh", "small.cuh"]
 
 
 def nccl_dirs():

@@ -22,6 +22,7 @@
 #include "kernels.cuh"
 #include "pbit_internal.h"
 #include "launch.cuh"
+#include "small.cuh"
 
 namespace pbit {
 
@@ -80,6 +81,13 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
 static int debug_env(const char* name) {
   const char* e = getenv(name);
   return e ? atoi(e) : 0;
+}
+
+// PBIT_SMALL=0 sends small lists through the general path too (experiments, tests)
+static bool small_path_disabled() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("PBIT_SMALL"); v = (e && atoi(e) == 0) ? 1 : 0; }
+  return v != 0;
 }
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -363,6 +371,58 @@ bool key_kind_ok(int key_kind, int key_bits) {
   return key_kind == PBIT_KEY_FLOAT && key_bits >= 16;  // IEEE binary16/32/64
 }
 
+// Small lists (n <= SMALL_N): the whole sort in one cluster launch (small.cuh).  Digit
+// widths 4 (the paper's) and 8; phase_ms reports the kernel under PBIT_PHASE_WALK.
+template <int KB>
+static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint32_t n, int K, KeyMap km,
+                     uint32_t* out_next, uint32_t* out_prev, uint32_t* out_head, cudaStream_t st, float* phase_ms,
+                     uint32_t* passes_run, uint32_t* launches_out) {
+  using KeyT = typename KeyOf<KB>::T;
+  const size_t a4 = align_up((size_t)n * 4), ak = align_up((size_t)n * sizeof(KeyT));
+  const size_t bytes = 6 * a4 + 2 * ak + align_up(SMALL_CTAS * 256 * 4) + 256;  // dn: 2 x 2 x a4
+  char* base = nullptr;
+  if (cudaMallocAsync((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  SmallArgs sa{};
+  sa.keys = keys; sa.next = next; sa.head = head; sa.n = n; sa.out_next = out_next; sa.out_prev = out_prev;
+  sa.km = km;
+  char* q = base;
+  for (int i = 0; i < 2; ++i) { sa.dn[i] = (uint2*)q; q += 2 * a4; }
+  for (int i = 0; i < 2; ++i) { sa.lid[i] = (uint32_t*)q; q += a4; sa.lkey[i] = q; q += ak; }
+  sa.hist = (uint32_t*)q; q += align_up(SMALL_CTAS * 256 * 4);
+  sa.err = (int*)q; sa.d_head = (uint32_t*)(q + 4); sa.passes = (uint32_t*)(q + 8);
+  cudaMemsetAsync(q, 0, 16, st);
+  static thread_local cudaEvent_t ev[2];
+  static thread_local bool ev_ready = false;
+  if (phase_ms && !ev_ready) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); ev_ready = true; }
+  if (phase_ms) cudaEventRecord(ev[0], st);
+  static std::atomic<unsigned long long> attr{0};
+  if (first_use_on_device(attr) && SMALL_CTAS > 8) {
+    cudaFuncSetAttribute(k_small_sort<KB, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_small_sort<KB, 8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  }
+  if (K == 4) k_small_sort<KB, 4><<<SMALL_CTAS, SMALL_THREADS, 0, st>>>(sa);
+  else k_small_sort<KB, 8><<<SMALL_CTAS, SMALL_THREADS, 0, st>>>(sa);
+  if (phase_ms) cudaEventRecord(ev[1], st);
+  struct Res { int err; uint32_t head; uint32_t passes; } res{};
+  cudaMemcpyAsync(&res, q, sizeof res, cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(base, st);
+  const cudaError_t es = cudaStreamSynchronize(st);
+  const cudaError_t el = cudaGetLastError();
+  if (es || el) {
+    set_last_error("pbit_sort_list (small)", cudaGetErrorString(es ? es : el));
+    return PBIT_ERR_CUDA;
+  }
+  if (res.err) return PBIT_ERR_INVALID_LIST;
+  if (phase_ms) {
+    for (int i = 0; i < PBIT_NUM_PHASES; ++i) phase_ms[i] = 0.f;
+    cudaEventElapsedTime(&phase_ms[PBIT_PHASE_WALK], ev[0], ev[1]);
+  }
+  *out_head = res.head;
+  if (passes_run) *passes_run = res.passes;
+  if (launches_out) *launches_out = 1;
+  return PBIT_OK;
+}
+
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
                 int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
                 cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches) {
@@ -370,6 +430,17 @@ int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t 
   if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
   int sms = 0;
   if (int rc = device_info(dev, &sms)) return rc;
+  init_rank_mode(st);
+  if (n <= SMALL_N && (K == 4 || K == 8) && rank_mode() == RANK_ATOMIC && !small_path_disabled()) {
+    const KeyMap km{key_kind, descending ? 1 : 0};
+    const uint32_t n32 = (uint32_t)n;
+    switch (key_bits) {
+      case 8: return run_small<1>(keys, next, head, n32, K, km, out_next, out_prev, out_head, st, phase_ms, passes_run, launches);
+      case 16: return run_small<2>(keys, next, head, n32, K, km, out_next, out_prev, out_head, st, phase_ms, passes_run, launches);
+      case 32: return run_small<4>(keys, next, head, n32, K, km, out_next, out_prev, out_head, st, phase_ms, passes_run, launches);
+      default: return run_small<8>(keys, next, head, n32, K, km, out_next, out_prev, out_head, st, phase_ms, passes_run, launches);
+    }
+  }
   SortPlan p;
   make_plan(n, key_bits, K, &p);
   p.key_kind = key_kind;
