@@ -166,8 +166,7 @@ def test_side_stream_and_determinism(pbit):
 
 
 # ---------------------------------------------------------------- invalid lists
-def _bad_lists():
-    n = 50000
+def _bad_lists(n=50000):
     base = torch.arange(1, n + 1, dtype=torch.int32)
     base[-1] = -1
     cyc_head = base.clone(); cyc_head[-1] = 0                       # tail -> head
@@ -180,13 +179,15 @@ def _bad_lists():
             "index_ge_n": bad_idx, "two_predecessors": two_pred, "small_cycle": small_cycle}
 
 
+# (n, K): the single-cluster small-list path (n <= 2^16, K 4/8) and the general path
+@pytest.mark.parametrize("n,K", [(50000, 8), (50000, 3), (100003, 8)])
 @pytest.mark.parametrize("name", list(_bad_lists().keys()))
-def test_invalid_list_rejected_and_out_untouched(pbit, name):
-    nx = _bad_lists()[name].cuda()
+def test_invalid_list_rejected_and_out_untouched(pbit, name, n, K):
+    nx = _bad_lists(n)[name].cuda()
     keys = workloads.uniform_u32(nx.shape[0], 1, 1).to(torch.int32).cuda()
     out = torch.full_like(nx, 0x1234)
     with pytest.raises(pbit.PbitError) as e:
-        pbit.sort_list(keys, nx, 0, out_next=out)
+        pbit.sort_list(keys, nx, 0, out_next=out, digit_bits=K)
     assert e.value.code == 2
     torch.cuda.synchronize()
     assert bool((out == 0x1234).all()), "out_next modified on INVALID_LIST"
