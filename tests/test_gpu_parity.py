@@ -426,3 +426,25 @@ def test_head_positions_and_tiny_lists(pbit):
     for n in (2, 3, 17, 4095, 4096, 4097, 8191, 8192, 8193, 16383, 16384, 16385):
         li = workloads.make_list(n, 32, seed=n, keys="zipf", links="random", device="cuda")
         _assert_same(_gpu_sort(pbit, li), _oracle(li), f"n={n}")
+
+
+def test_small_path_in_place_host_and_stream(pbit):
+    """The single-cluster small-list path: in-place relink, host buffers, a side stream,
+    out_prev -- against the oracle."""
+    li = workloads.make_list(40009, 32, seed=21, keys="zipf", device="cuda")
+    want = _oracle(li)
+    nx = li.next.clone()
+    h, out = pbit.sort_list(li.keys, nx, li.head, out_next=nx)  # in place
+    torch.cuda.synchronize()
+    _assert_same((h, out.cpu().numpy().view(np.uint32)), want, "small in-place")
+    kh, nh = li.keys.cpu().numpy(), li.next.cpu().numpy()
+    oh = np.empty(li.n, np.uint32)
+    ph = np.empty(li.n, np.uint32)
+    h2, _ = pbit.sort_list(kh, nh, li.head, out_next=oh, out_prev=ph)  # host buffers
+    _assert_same((h2, oh), want, "small host")
+    assert np.array_equal(ph, oracle.repair_back(want[1], want[0]))
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        h3, o3 = pbit.sort_list(li.keys, li.next, li.head, stream=s)
+    s.synchronize()
+    _assert_same((h3, o3.cpu().numpy().view(np.uint32)), want, "small side stream")
