@@ -182,6 +182,10 @@ int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32
 int pbit_mg_get_unique_id(void *id_out /* PBIT_MG_UNIQUE_ID_BYTES host bytes */);
 int pbit_mg_comm_init(void **comm_out, int nranks, const void *id, int rank);
 int pbit_mg_comm_destroy(void *comm);
+/* After pbit_sort_list_mg returned PBIT_ERR_NCCL (an asynchronous NCCL error, or no
+ * progress for PBIT_MG_TIMEOUT_S seconds, default 300): abort the communicator, which also
+ * ends its pending collectives on the call's stream.  The communicator is then unusable. */
+int pbit_mg_comm_abort(void *comm);
 
 /* Node ids per rank for pbit_sort_list_mg: ceil(n_global / nranks) rounded up to 64. */
 uint64_t pbit_mg_slice(uint64_t n_global, int nranks);

@@ -21,7 +21,7 @@ PBIT_NULL = 0xFFFFFFFF
 NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
 SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_sort_array", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
-           "pbit_mg_comm_destroy", "pbit_status_string", "pbit_version", "pbit_last_error",
+           "pbit_mg_comm_destroy", "pbit_mg_comm_abort", "pbit_status_string", "pbit_version", "pbit_last_error",
            "pbit_mg_slice", "pbit_mg_exchange_plan"]
 
 STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
@@ -66,6 +66,8 @@ def _load():
     lib.pbit_mg_comm_init.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, ctypes.c_void_p, ctypes.c_int]
     lib.pbit_mg_comm_destroy.restype = ctypes.c_int
     lib.pbit_mg_comm_destroy.argtypes = [ctypes.c_void_p]
+    lib.pbit_mg_comm_abort.restype = ctypes.c_int
+    lib.pbit_mg_comm_abort.argtypes = [ctypes.c_void_p]
     lib.pbit_status_string.restype = ctypes.c_char_p
     lib.pbit_status_string.argtypes = [ctypes.c_int]
     lib.pbit_version.restype = ctypes.c_uint32
@@ -223,6 +225,11 @@ def mg_comm_init(nranks: int, uid: bytes, rank: int) -> int:
 
 def mg_comm_destroy(comm: int) -> None:
     lib.pbit_mg_comm_destroy(ctypes.c_void_p(comm))
+
+
+def mg_comm_abort(comm: int) -> None:
+    """Abort the communicator after sort_list_mg raised PBIT_ERR_NCCL (pbit.h)."""
+    lib.pbit_mg_comm_abort(ctypes.c_void_p(comm))
 
 
 def mg_slice(n_global: int, nranks: int) -> int:

@@ -21,6 +21,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "../../include/pbit.h"
@@ -63,6 +65,48 @@ struct Bump {
       rc = PBIT_ERR_CUDA;                                   \
       goto done;                                            \
     }                                                       \
+  } while (0)
+
+// Failure detection: wait for the stream while polling the communicator's
+// asynchronous error, with a timeout (PBIT_MG_TIMEOUT_S, default 300 s), instead of a
+// blocking synchronize that would hang forever if a peer died.  On an NCCL error or the
+// timeout the call returns PBIT_ERR_NCCL; the caller then aborts the communicator
+// (pbit_mg_comm_abort), which also releases the stream.
+static int mg_wait(cudaStream_t st, ncclComm_t comm) {
+  static double timeout_s = -1.0;
+  if (timeout_s < 0) {
+    const char* e = getenv("PBIT_MG_TIMEOUT_S");
+    timeout_s = e ? atof(e) : 300.0;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned spin = 0;; ++spin) {
+    const cudaError_t q = cudaStreamQuery(st);
+    if (q == cudaSuccess) return PBIT_OK;
+    if (q != cudaErrorNotReady) {
+      set_last_error("pbit_sort_list_mg", cudaGetErrorString(q));
+      return PBIT_ERR_CUDA;
+    }
+    ncclResult_t ar = ncclSuccess;
+    if (ncclCommGetAsyncError(comm, &ar) != ncclSuccess || (ar != ncclSuccess && ar != ncclInProgress)) {
+      set_last_error("pbit_sort_list_mg: NCCL asynchronous error", ncclGetErrorString(ar));
+      return PBIT_ERR_NCCL;
+    }
+    if ((spin & 255u) == 255u &&
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+      set_last_error("pbit_sort_list_mg", "timed out waiting for the collectives (PBIT_MG_TIMEOUT_S)");
+      return PBIT_ERR_NCCL;
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+}
+
+#define MGWAIT()                     \
+  do {                               \
+    const int rc_ = mg_wait(st, comm); \
+    if (rc_) {                       \
+      rc = rc_;                      \
+      goto done;                     \
+    }                                \
   } while (0)
 
 template <int KB>
@@ -228,7 +272,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     k_plan<<<1, 256, 0, st>>>(hist_g, bases_l, plan_g, D, K, n, err);
     CUDACHK(cudaMemcpyAsync(&h_plan, plan_g, sizeof(Plan), cudaMemcpyDeviceToHost, st));
     CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
-    CUDACHK(cudaStreamSynchronize(st));
+    MGWAIT();
     if (h_err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
 
     // ---- 4. emit the list-order chunk of positions [P0, P1)
@@ -260,7 +304,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       k_plan<<<1, 256, 0, st>>>(hist_a, bases_p, plan_p, D, K, m, err);
       Plan h_pp{};
       CUDACHK(cudaMemcpyAsync(&h_pp, plan_p, sizeof(Plan), cudaMemcpyDeviceToHost, st));
-      CUDACHK(cudaStreamSynchronize(st));
+      MGWAIT();
       if (m) { launch_key_passes_k<KB>(K, pa, h_pp, true, st, nullptr, 0, SRC_TMA); launches += h_pp.npasses; }
       const int pa_par = (int)(h_pp.npasses & 1u);  // sorted chunk in kbuf/ibuf[pa_par]
       const KeyT* sk = kbuf[pa_par];
@@ -284,7 +328,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         NCCLCHK(ncclAllReduce(mg_c, mg_c, (size_t)NS * nc, ncclUint32, ncclSum, comm, st));
         h_cnt.resize((size_t)NS * nc);
         CUDACHK(cudaMemcpyAsync(h_cnt.data(), mg_c, 4ull * NS * nc, cudaMemcpyDeviceToHost, st));
-        CUDACHK(cudaStreamSynchronize(st));
+        MGWAIT();
         for (int sp = 0; sp < NS; ++sp) {
           const uint64_t x = std::min<uint64_t>(n, (uint64_t)(sp + 1) * S);
           int pick = 0;  // the largest candidate with (global count below it) <= x
@@ -306,7 +350,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
           NCCLCHK(ncclAllGather(mg_c, mg_call, (size_t)2 * NS, ncclUint32, comm, st));
           h_cnt.resize((size_t)2 * NS * G);
           CUDACHK(cudaMemcpyAsync(h_cnt.data(), mg_call, 8ull * NS * G, cudaMemcpyDeviceToHost, st));
-          CUDACHK(cudaStreamSynchronize(st));
+          MGWAIT();
           for (int q = 0; q < G; ++q)
             for (int sp = 0; sp < NS; ++sp) {
               h_lt[(size_t)q * NS + sp] = h_cnt[(size_t)q * 2 * NS + sp];
@@ -348,7 +392,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       k_plan<<<1, 256, 0, st>>>(hist_b, bases_l, plan_l, D, K, m, err);
       Plan h_pl{};
       CUDACHK(cudaMemcpyAsync(&h_pl, plan_l, sizeof(Plan), cudaMemcpyDeviceToHost, st));
-      CUDACHK(cudaStreamSynchronize(st));
+      MGWAIT();
       SweepArgs la = pa;
       la.kin[0] = kbuf[pb]; la.kin[1] = kbuf[pb ^ 1]; la.vin[0] = ibuf[pb]; la.vin[1] = ibuf[pb ^ 1];
       la.kout[0] = kbuf[pb]; la.kout[1] = kbuf[pb ^ 1]; la.vout[0] = ibuf[pb]; la.vout[1] = ibuf[pb ^ 1];
@@ -364,7 +408,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     k_first_last_id<<<1, 1, 0, st>>>(final_plan, fin[0], fin[1], m, firsts + 2 * G);
     NCCLCHK(ncclAllGather(firsts + 2 * G, firsts, 2, ncclUint32, comm, st));
     CUDACHK(cudaMemcpyAsync(h_firsts, firsts, 8ull * G, cudaMemcpyDeviceToHost, st));
-    CUDACHK(cudaStreamSynchronize(st));
+    MGWAIT();
     for (int dir = 1; dir >= -1; dir -= 2) {
       uint32_t* out_local = dir > 0 ? out_next_local : out_prev_local;
       if (!out_local) continue;
@@ -387,7 +431,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       NCCLCHK(ncclAllGather(cnt, cntall, G, ncclUint32, comm, st));
       h_cntall.resize((size_t)G * G);
       CUDACHK(cudaMemcpyAsync(h_cntall.data(), cntall, 4ull * G * G, cudaMemcpyDeviceToHost, st));
-      CUDACHK(cudaStreamSynchronize(st));
+      MGWAIT();
       std::vector<uint32_t> h_offs(G);
       uint32_t acc = 0;
       for (int d = 0; d < G; ++d) { h_offs[d] = acc; acc += h_cntall[(size_t)r * G + d]; }
@@ -414,7 +458,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       }
     }
     CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
-    CUDACHK(cudaStreamSynchronize(st));
+    MGWAIT();
     CUDACHK(cudaGetLastError());
     if (h_err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
     *out_head = h_firsts[0];  // rank 0 always holds sorted position 0 (n > 0)
@@ -422,7 +466,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   }
 done:
   cudaFreeAsync(base, st);
-  cudaStreamSynchronize(st);
+  if (rc != PBIT_ERR_NCCL) cudaStreamSynchronize(st);  // a stuck collective is released by the caller's abort
   return rc;
 }
 
@@ -450,6 +494,11 @@ int pbit_mg_comm_init(void** comm_out, int nranks, const void* id, int rank) {
   if (ncclCommInitRank(&c, nranks, uid, rank) != ncclSuccess) return PBIT_ERR_NCCL;
   *comm_out = (void*)c;
   return PBIT_OK;
+}
+
+int pbit_mg_comm_abort(void* comm) {
+  if (!comm) return PBIT_ERR_INVALID_ARG;
+  return ncclCommAbort((ncclComm_t)comm) == ncclSuccess ? PBIT_OK : PBIT_ERR_NCCL;
 }
 
 int pbit_mg_comm_destroy(void* comm) {

@@ -216,6 +216,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
 
   // a1/a2: pack + histograms
   {
+    NvtxRange nv("pbit.pack");
     const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
     const size_t smem = (size_t)p.D * radix * 4;
     const KeyMap km{p.key_kind, p.descending};
@@ -226,6 +227,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
 
   // a1: walk
   RulerSel sel{n, (uint32_t)p.s_log2, p.R};
+  nvtxRangePushA("pbit.walk");
   const bool head_is_ruler = sel.is_ruler(head);
   const uint32_t R_static = p.R + (head_is_ruler ? 0u : 1u);
   const uint32_t head_ruler = head_is_ruler ? (head >> p.s_log2) : p.R;
@@ -245,9 +247,11 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_WALK], st);
+  nvtxRangePop();
 
   // a1: ruler ranking (second ruling set + pointer jumping over the sub-rulers)
   {
+    NvtxRange nv("pbit.rank");
     const uint32_t Rmax = R_static + p.dyn_cap;
     RulerSel sub{Rmax, (uint32_t)SUB_LOG2, (Rmax + (1u << SUB_LOG2) - 1) >> SUB_LOG2};
     const bool hs = sub.is_ruler(head_ruler);
@@ -302,6 +306,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (timing) cudaEventRecord(ev[PBIT_PHASE_GATHER], st);
 
   // a3/a4: passes
+  nvtxRangePushA("pbit.passes");
   SweepArgs sa{};
   sa.kin[0] = w.keys[0]; sa.kin[1] = w.keys[1]; sa.vin[0] = w.ids[0]; sa.vin[1] = w.ids[1];
   sa.kout[0] = w.keys[0]; sa.kout[1] = w.keys[1]; sa.vout[0] = w.ids[0]; sa.vout[1] = w.ids[1];
@@ -316,9 +321,11 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (timing)
     for (int s2 = ok ? (int)hplan.npasses : 0; s2 < p.D; ++s2) cudaEventRecord(ev[PBIT_PHASE_PASS0 + s2], st);
 
+  nvtxRangePop();
   // a5: relink: (v, succ) pairs grouped by v's fine bin (MSD partition levels), then
   // each 2^14-id bin applied in a shared-memory window
   if (ok && !sa.debug_no_lookback) {
+    NvtxRange nv("pbit.relink");
     const uint32_t* fin = w.ids[hplan.npasses & 1u];  // buffer holding the final ids
     k_relink_head<<<1, 1, 0, st>>>(fin, w.d_head, w.err);
     ++launches;
@@ -426,6 +433,7 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
                 int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
                 cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches) {
+  NvtxRange nv("pbit_sort_list");
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
   int sms = 0;

@@ -1,6 +1,7 @@
 // pbit_internal.h -- host-side interfaces shared by pbit.cu and mg.cu (not part of the ABI).
 #pragma once
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX3: a no-op unless a profiler is attached
 #include <stdint.h>
 
 namespace pbit {
@@ -16,6 +17,15 @@ struct SortPlan {
   uint32_t dyn_cap;
   int key_kind = 0;    // PBIT_KEY_* (key order map applied in the pack)
   int descending = 0;
+};
+
+// NVTX range around the launches of one phase (SURVEY §5 tracing): ncu --nvtx /
+// nsys attribute the phase's kernels to "pbit.<phase>".
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
 };
 
 void set_last_error(const char* what, const char* detail);
