@@ -4,21 +4,27 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 
 #include "kernels.cuh"
 #include "pbit_internal.h"
 
 namespace pbit {
 
-// cudaFuncSetAttribute is per device: true the first time a call site runs on the current
-// device (one bit per device), so multi-GPU processes set every kernel attribute everywhere.
-static inline bool first_use_on_device(std::atomic<unsigned long long>& mask) {
+// cudaFuncSetAttribute is per device: run `set` once per (call site, device) -- under a
+// lock, and marked done only after it ran, so a concurrent caller on another stream never
+// launches before the attributes are in place.
+template <typename F>
+static inline void once_per_device(std::atomic<unsigned long long>& done, F&& set) {
   int dev = 0;
   cudaGetDevice(&dev);
   const unsigned long long bit = 1ull << (dev & 63);
-  if (mask.load(std::memory_order_relaxed) & bit) return false;
-  mask.fetch_or(bit);
-  return true;  // idempotent if two threads race here
+  if (done.load(std::memory_order_acquire) & bit) return;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.load(std::memory_order_relaxed) & bit) return;
+  set();
+  done.fetch_or(bit, std::memory_order_release);
 }
 
 // One k_onesweep launch (sets the dynamic-smem attribute once per instantiation).
@@ -26,9 +32,10 @@ template <typename KeyT, int RB, int IPT, int RANK, int SRC>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
   static std::atomic<unsigned long long> attr{0};
-  if (first_use_on_device(attr))
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sizeof(S));
+  });
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
   k_onesweep<KeyT, RB, IPT, RANK, SRC><<<ntiles, SWEEP_THREADS, sizeof(S), st>>>(a);
 }
@@ -90,12 +97,12 @@ static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t 
                               uint2* pbuf1, uint32_t* cursors, uint32_t* out_next, const int* err, cudaStream_t st,
                               int sms, int dir = 1) {
   static std::atomic<unsigned long long> attr{0};
-  if (first_use_on_device(attr)) {
+  once_per_device(attr, [] {
     cudaFuncSetAttribute(k_relink_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
     cudaFuncSetAttribute(k_relink_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
     cudaFuncSetAttribute(k_relink_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
     cudaFuncSetAttribute(k_relink_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
-  }
+  });
   if (n == 0) return 0;
   RelinkLevels lv(n);
   const uint32_t nfine = (n + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;

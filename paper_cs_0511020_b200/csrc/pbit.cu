@@ -266,8 +266,9 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     int cur = 0;
     if (nsub <= (uint32_t)RANK_SMALL) {  // every round in one CTA (small lists: launch latency)
       static std::atomic<unsigned long long> attr{0};
-      if (first_use_on_device(attr))
+      once_per_device(attr, [] {
         cudaFuncSetAttribute(k_rank_jump_block, cudaFuncAttributeMaxDynamicSharedMemorySize, RANK_SMALL * 32);
+      });
       k_rank_jump_block<<<1, 1024, RANK_SMALL * 32, st>>>(w.sdist[0], w.scnt[0], w.ssucc[0], nsub, rounds, head_sub,
                                                           n, w.err);
       launches += 1;
@@ -403,10 +404,12 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
   if (phase_ms && !ev_ready) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); ev_ready = true; }
   if (phase_ms) cudaEventRecord(ev[0], st);
   static std::atomic<unsigned long long> attr{0};
-  if (first_use_on_device(attr) && SMALL_CTAS > 8) {
-    cudaFuncSetAttribute(k_small_sort<KB, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(k_small_sort<KB, 8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-  }
+  once_per_device(attr, [] {
+    if (SMALL_CTAS > 8) {
+      cudaFuncSetAttribute(k_small_sort<KB, 4>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      cudaFuncSetAttribute(k_small_sort<KB, 8>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    }
+  });
   if (K == 4) k_small_sort<KB, 4><<<SMALL_CTAS, SMALL_THREADS, 0, st>>>(sa);
   else k_small_sort<KB, 8><<<SMALL_CTAS, SMALL_THREADS, 0, st>>>(sa);
   if (phase_ms) cudaEventRecord(ev[1], st);

@@ -448,3 +448,35 @@ def test_small_path_in_place_host_and_stream(pbit):
         h3, o3 = pbit.sort_list(li.keys, li.next, li.head, stream=s)
     s.synchronize()
     _assert_same((h3, o3.cpu().numpy().view(np.uint32)), want, "small side stream")
+
+
+def test_concurrent_host_threads_on_own_streams(pbit):
+    """pbit.h: thread-safe across distinct streams -- 4 host threads (ctypes releases the
+    GIL), each sorting its own list on its own stream, small and general paths mixed."""
+    import threading
+    lists = [workloads.make_list(n, 32, seed=40 + i, keys="zipf", device="cuda")
+             for i, n in enumerate((30011, 150001, 60013, 250007))]
+    want = [_oracle(li) for li in lists]
+    got = [None] * len(lists)
+    errors = []
+
+    def work(i):
+        try:
+            s = torch.cuda.Stream()
+            li = lists[i]
+            with torch.cuda.stream(s):  # outputs allocated on (and used by) this stream
+                for _ in range(3):
+                    h, out = pbit.sort_list(li.keys, li.next, li.head)
+            s.synchronize()
+            got[i] = (h, out.cpu().numpy().view(np.uint32))
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(lists))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for i in range(len(lists)):
+        _assert_same(got[i], want[i], f"thread {i}")
