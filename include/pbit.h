@@ -78,9 +78,12 @@ enum {
 };
 
 typedef struct {
-    int digit_bits;  /* K, the bit-pattern length.  0 = auto (8).  1..8.
-                        The paper's default is K = 4.  Every K gives the
-                        same bytes.                                                 */
+    int digit_bits;  /* K, the bit-pattern length.  0 = auto (8).  1..16
+                        (SPEC's range); K need not divide key_bits (the top pattern
+                        is narrower).  The paper's default is K = 4.
+                        Every K gives the same bytes.  K <= 8 runs K-bit passes; a
+                        wider pattern is sorted as stable 8-bit sub-passes,
+                        so K = 9..16 runs the passes of K = 8.                       */
     void *stream;    /* cudaStream_t for every launch; NULL = legacy default stream */
     int validate;    /* reserved: validation always runs (it is fused into ranking) */
     float *phase_ms; /* optional host array of PBIT_NUM_PHASES floats: device ms per

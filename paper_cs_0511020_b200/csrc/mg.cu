@@ -556,8 +556,8 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
                       uint32_t* out_next_local, void* nccl_comm, const pbit_opts* opts) {
   if (!nccl_comm || !out_head) return PBIT_ERR_INVALID_ARG;
   if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
-  int K = opts && opts->digit_bits ? opts->digit_bits : 8;
-  if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
+  const int K = pass_bits(opts && opts->digit_bits ? opts->digit_bits : 8);
+  if (!K) return PBIT_ERR_INVALID_ARG;
   if (n_global > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
   uint32_t* out_prev_local = opts ? opts->out_prev : nullptr;
   if (out_prev_local && out_prev_local == out_next_local) return PBIT_ERR_INVALID_ARG;

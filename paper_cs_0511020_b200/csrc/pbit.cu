@@ -597,8 +597,8 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
                    uint32_t* out_head, uint32_t* out_next, const pbit_opts* opts) {
   if (!out_head) return PBIT_ERR_INVALID_ARG;
   if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
-  int K = opts && opts->digit_bits ? opts->digit_bits : 8;
-  if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
+  const int K = pass_bits(opts && opts->digit_bits ? opts->digit_bits : 8);
+  if (!K) return PBIT_ERR_INVALID_ARG;
   if (n > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
   const int key_kind = opts ? opts->key_kind : PBIT_KEY_UNSIGNED;
   const int descending = opts ? opts->descending : 0;
@@ -652,8 +652,8 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
 int pbit_sort_array(const void* keys, uint64_t n, int key_bits, uint32_t* out_index, void* out_keys,
                     const pbit_opts* opts) {
   if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
-  const int K = opts && opts->digit_bits ? opts->digit_bits : 8;
-  if (K < 1 || K > 8) return PBIT_ERR_INVALID_ARG;
+  const int K = pass_bits(opts && opts->digit_bits ? opts->digit_bits : 8);
+  if (!K) return PBIT_ERR_INVALID_ARG;
   if (n > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
   const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
   if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;

@@ -41,4 +41,11 @@ int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t 
 // key_kind / key_bits combination accepted by the ABI (PBIT_KEY_*, pbit.h)
 bool key_kind_ok(int key_kind, int key_bits);
 
+// Digit width of the GPU passes for the user's pattern length K (1..16, SPEC S:127's
+// range).  K <= 8 runs K-bit passes.  A K-bit pattern with K > 8 is sorted as stable 8-bit
+// sub-passes, least significant first: the composition of stable passes is the same sort
+// (P:1190), so the bytes are those of K (reading Q7); 2^K > 256 warp-private
+// counters per pass would not fit two pass CTAs per SM.  Returns 0 for an invalid K.
+inline int pass_bits(int K) { return K < 1 || K > 16 ? 0 : (K > 8 ? 8 : K); }
+
 }  // namespace pbit

@@ -56,8 +56,10 @@ def test_argument_checks_without_device(pbit):
     # key width not in {8,16,32,64}
     assert lib.pbit_sort_list(p, p, 0, 4, 24, ctypes.byref(oh), p, None) == 1
     # digit_bits out of range
-    o = pbit._opts(9, 0, None, None)
-    assert lib.pbit_sort_list(p, p, 0, 4, 32, ctypes.byref(oh), p, ctypes.byref(o)) == 1
+    for K in (17, -1):
+        o = pbit._opts(K, 0, None, None)
+        assert lib.pbit_sort_list(p, p, 0, 4, 32, ctypes.byref(oh), p, ctypes.byref(o)) == 1
+        assert lib.pbit_sort_array(p, 4, 32, p, None, ctypes.byref(o)) == 1
     # empty list: head must be NULL
     assert lib.pbit_sort_list(None, None, 0xFFFFFFFF, 0, 32, ctypes.byref(oh), None, None) == 0
     assert oh.value == 0xFFFFFFFF

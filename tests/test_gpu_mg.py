@@ -43,7 +43,7 @@ def test_mg_single_rank_vs_oracle(mg, n, key_bits, keys, links):
     assert np.array_equal(out.cpu().numpy().view(np.uint32), on)
 
 
-@pytest.mark.parametrize("K", [4, 8])
+@pytest.mark.parametrize("K", [4, 8, 12])
 def test_mg_digit_widths(mg, K):
     p, comm = mg
     li = workloads.make_list(250001, 32, seed=5, keys="zipf", device="cuda")

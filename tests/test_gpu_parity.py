@@ -83,6 +83,20 @@ def test_digit_width_sweep_zipf(pbit, K):
     _assert_same(_gpu_sort(pbit, li, K=K), _oracle(li), f"K={K}")
 
 
+@pytest.mark.parametrize("K", [9, 11, 12, 16])
+def test_wide_patterns_vs_oracle_K16(pbit, K):
+    """K = 9..16 (SPEC S:127's range): 8-bit sub-passes per pattern (reading Q7); the bytes
+    are the oracle's, which sorts with 16-bit patterns literally (tab[65536])."""
+    li = workloads.make_list(300007, 32, seed=79, keys="zipf", device="cuda")
+    h, out, ph = pbit.sort_list(li.keys, li.next, li.head, digit_bits=K, timing=True)
+    torch.cuda.synchronize()
+    assert ph["passes_run"] <= 4
+    _assert_same((h, out.cpu().numpy().view(np.uint32)), _oracle(li, K=16), f"K={K}")
+    idx, _ = pbit.sort_array(li.keys, key_bits=32, digit_bits=K)
+    kn = li.keys.cpu().numpy().view(np.uint32)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), np.argsort(kn, kind="stable").astype(np.uint32))
+
+
 @pytest.mark.parametrize("K", [3, 5, 8])
 def test_digit_width_sweep_u64_narrow_top_digit(pbit, K):
     li = workloads.make_list(70001, 64, seed=78, keys="uniform", device="cuda")
