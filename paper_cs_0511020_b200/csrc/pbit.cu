@@ -28,6 +28,36 @@ namespace pbit {
 
 // Text of the last CUDA/NCCL failure seen by this host thread (pbit_last_error()).
 static thread_local char g_last_err[256] = "";
+
+// The small host-visible results of a call (the pass plan mid-call; head, error word and
+// pass count at the end) land in pinned memory: into a pageable destination each small
+// cudaMemcpyAsync is a staged copy that blocks the host.  One box per host thread (calls
+// are synchronous, so a thread has at most one call in flight).
+struct HostBox {
+  Plan plan;
+  int err;
+  uint32_t head, npasses;
+  uint32_t small[4];  // run_small: {err, head, passes}
+};
+static HostBox* host_box() {
+  struct Holder {
+    HostBox* pinned = nullptr;
+    HostBox pageable{};
+    bool tried = false;
+    ~Holder() { if (pinned) cudaFreeHost(pinned); }
+  };
+  static thread_local Holder h;
+#ifndef PBIT_PAGEABLE_RESULTS
+  if (!h.tried) {
+    h.tried = true;
+    if (cudaHostAlloc((void**)&h.pinned, sizeof(HostBox), cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      h.pinned = nullptr;
+    }
+  }
+#endif
+  return h.pinned ? h.pinned : &h.pageable;
+}
 void set_last_error(const char* what, const char* detail) {
   snprintf(g_last_err, sizeof g_last_err, "%s: %s", what, detail ? detail : "");
 }
@@ -66,11 +96,15 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   p->key_bits = key_bits;
   p->K = K;
   p->D = (key_bits + K - 1) / K;
-  // ruler spacing: ~64 nodes per segment on large lists, more rulers on small ones so the
-  // walk still has enough independent walkers (and short tails)
+  // ruler spacing 2^s_log2 nodes per segment, by list size (measured): the
+  // walk wants enough segments per resident walker that the longest chains do not set
+  // its time (shorter segments on mid-size lists), ranking and pass 0's gather want fewer,
+  // longer segments (longer ones on the largest lists, where the ruler list's ranking
+  // leaves the L2)
   static int env_s = -2;
   if (env_s == -2) { const char* e = getenv("PBIT_RULER_LOG2"); env_s = e ? atoi(e) : -1; }
-  int s_log2 = env_s > 0 ? env_s : 6;
+  int s_log2 = n >= (1ull << 30) ? 7 : n >= (1ull << 26) ? 6 : n >= (1ull << 24) ? 5 : n >= (1ull << 22) ? 4 : 5;
+  if (env_s > 0) s_log2 = env_s;
   while (s_log2 > 2 && (n >> s_log2) < (1u << 13)) --s_log2;
   p->s_log2 = s_log2;
   p->cap = 4u << s_log2;
@@ -291,11 +325,11 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   // gets its digit and parity as kernel parameters and trivial digits are not launched
   k_plan<<<1, 256, 0, st>>>(w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
   ++launches;
-  Plan hplan{};
-  int herr = 0;
-  cudaMemcpyAsync(&hplan, w.plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(&herr, w.err, 4, cudaMemcpyDeviceToHost, st);
-  if (cudaStreamSynchronize(st) != cudaSuccess) herr = -1;
+  HostBox* hb = host_box();
+  cudaMemcpyAsync(&hb->plan, w.plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(&hb->err, w.err, 4, cudaMemcpyDeviceToHost, st);
+  int herr = cudaStreamSynchronize(st) != cudaSuccess ? -1 : hb->err;
+  const Plan hplan = hb->plan;
   const bool ok = herr == 0;
   if (ok && hplan.npasses == 0) {  // a1: gather to list order -- only when no pass can fuse it
     const uint32_t Rmax = R_static + p.dyn_cap;
@@ -339,7 +373,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
 
   // results: {head, err, npasses}
-  struct Res { uint32_t head; int err; uint32_t npasses; } res{};
+  HostBox& res = *hb;
   cudaError_t e1 = cudaMemcpyAsync(&res.head, w.d_head, 4, cudaMemcpyDeviceToHost, st);
   cudaError_t e2 = cudaMemcpyAsync(&res.err, w.err, 4, cudaMemcpyDeviceToHost, st);
   cudaError_t e3 = cudaMemcpyAsync(&res.npasses, &w.plan->npasses, 4, cudaMemcpyDeviceToHost, st);
@@ -398,7 +432,6 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
   for (int i = 0; i < 2; ++i) { sa.lid[i] = (uint32_t*)q; q += a4; sa.lkey[i] = q; q += ak; }
   sa.hist = (uint32_t*)q; q += align_up(SMALL_CTAS * 256 * 4);
   sa.err = (int*)q; sa.d_head = (uint32_t*)(q + 4); sa.passes = (uint32_t*)(q + 8);
-  cudaMemsetAsync(q, 0, 16, st);
   static thread_local cudaEvent_t ev[2];
   static thread_local bool ev_ready = false;
   if (phase_ms && !ev_ready) { cudaEventCreate(&ev[0]); cudaEventCreate(&ev[1]); ev_ready = true; }
@@ -413,8 +446,8 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
   if (K == 4) k_small_sort<KB, 4><<<SMALL_CTAS, SMALL_THREADS, 0, st>>>(sa);
   else k_small_sort<KB, 8><<<SMALL_CTAS, SMALL_THREADS, 0, st>>>(sa);
   if (phase_ms) cudaEventRecord(ev[1], st);
-  struct Res { int err; uint32_t head; uint32_t passes; } res{};
-  cudaMemcpyAsync(&res, q, sizeof res, cudaMemcpyDeviceToHost, st);
+  uint32_t* res_words = host_box()->small;
+  cudaMemcpyAsync(res_words, q, 12, cudaMemcpyDeviceToHost, st);
   cudaFreeAsync(base, st);
   const cudaError_t es = cudaStreamSynchronize(st);
   const cudaError_t el = cudaGetLastError();
@@ -422,13 +455,13 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
     set_last_error("pbit_sort_list (small)", cudaGetErrorString(es ? es : el));
     return PBIT_ERR_CUDA;
   }
-  if (res.err) return PBIT_ERR_INVALID_LIST;
+  if (res_words[0]) return PBIT_ERR_INVALID_LIST;
   if (phase_ms) {
     for (int i = 0; i < PBIT_NUM_PHASES; ++i) phase_ms[i] = 0.f;
     cudaEventElapsedTime(&phase_ms[PBIT_PHASE_WALK], ev[0], ev[1]);
   }
-  *out_head = res.head;
-  if (passes_run) *passes_run = res.passes;
+  *out_head = res_words[1];
+  if (passes_run) *passes_run = res_words[2];
   if (launches_out) *launches_out = 1;
   return PBIT_OK;
 }
@@ -516,9 +549,10 @@ static int run_array(const void* keys, uint32_t n, int key_bits, int K, KeyMap k
     launches += 2;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
-  Plan hplan{};
-  cudaMemcpyAsync(&hplan, plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
+  HostBox* hb = host_box();
+  cudaMemcpyAsync(&hb->plan, plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
   const bool synced = cudaStreamSynchronize(st) == cudaSuccess;
+  const Plan hplan = hb->plan;
   const int fblocks = std::max(1, std::min((int)((n + 255) / 256), sms * 8));
   if (synced) {
     if (hplan.npasses == 0) {  // one digit value everywhere: the input order is sorted

@@ -61,16 +61,20 @@ k_small_sort(const __grid_constant__ SmallArgs a) {
   __shared__ WCnt wcnt[SMALL_WARPS][RADIX];
   __shared__ uint32_t s_base[RADIX], s_scan[SMALL_WARPS];
   __shared__ int s_trivial;
+  __shared__ int s_err;  // this CTA's error bits; combined over the cluster via DSMEM
+  __shared__ int s_bad;
 
   const uint32_t n = a.n;
   const uint32_t c = cooperative_groups::this_cluster().block_rank();
   const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t gt = c * SMALL_THREADS + t, GT = SMALL_CTAS * SMALL_THREADS;
 
+  if (t == 0) s_err = 0;
+  __syncthreads();
   // ---- 1. ranking: dist = 1, nx = next; then rounds of dist += dist[nx], nx = nx[nx]
   for (uint32_t v = gt; v < n; v += GT) {
     const uint32_t x = a.next[v];
-    if (x != PBIT_NULL32 && x >= n) atomicOr(a.err, E_BAD_INDEX);
+    if (x != PBIT_NULL32 && x >= n) atomicOr(&s_err, E_BAD_INDEX);
     a.dn[0][v] = make_uint2(1u, x >= n ? PBIT_NULL32 : x);
   }
   small_sync();
@@ -96,10 +100,24 @@ k_small_sort(const __grid_constant__ SmallArgs a) {
   }
   // valid iff every pointer reached NULL and the head's chain holds all n nodes
   for (uint32_t v = gt; v < n; v += GT)
-    if (a.dn[cur][v].y != PBIT_NULL32) atomicOr(a.err, E_CHAIN);
-  if (gt == 0 && a.dn[cur][a.head].x != n) atomicOr(a.err, E_CHAIN);
+    if (a.dn[cur][v].y != PBIT_NULL32) atomicOr(&s_err, E_CHAIN);
+  if (gt == 0 && a.dn[cur][a.head].x != n) atomicOr(&s_err, E_CHAIN);
   small_sync();
-  if (*a.err) return;  // uniform: every write to err precedes the barrier
+  {  // every CTA ORs the cluster's error bits (DSMEM reads after the barrier), so the
+     // decision is uniform; the error word needs no memset before the launch
+    auto cl = cooperative_groups::this_cluster();
+    int e = 0;
+    if (t < SMALL_CTAS) e = *cl.map_shared_rank(&s_err, t);
+    e = __reduce_or_sync(0xffffffffu, w == 0 ? e : 0);
+    if (t == 0) s_bad = e;
+    __syncthreads();
+    const int bad = s_bad;
+    if (c == 0 && t == 0) *a.err = bad;
+    if (bad) {
+      cl.sync();  // no CTA exits while another may still read its s_err
+      return;
+    }
+  }
 
   // ---- 2. list order: position of v = n - dist[v]
   for (uint32_t v = gt; v < n; v += GT) {
