@@ -101,13 +101,15 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
   // its time (shorter segments on mid-size lists), ranking and pass 0's gather want fewer,
   // longer segments (longer ones on the largest lists, where the ruler list's ranking
   // leaves the L2)
-  static int env_s = -2;
-  if (env_s == -2) { const char* e = getenv("PBIT_RULER_LOG2"); env_s = e ? atoi(e) : -1; }
+  static const int env_s = [] { const char* e = getenv("PBIT_RULER_LOG2"); return e ? atoi(e) : -1; }();
   int s_log2 = n >= (1ull << 30) ? 7 : n >= (1ull << 26) ? 6 : n >= (1ull << 24) ? 5 : n >= (1ull << 22) ? 4 : 5;
   if (env_s > 0) s_log2 = env_s;
   while (s_log2 > 2 && (n >> s_log2) < (1u << 13)) --s_log2;
   p->s_log2 = s_log2;
-  p->cap = 4u << s_log2;
+#ifndef PBIT_CAP_SHIFT
+#define PBIT_CAP_SHIFT 2
+#endif
+  p->cap = (1u << PBIT_CAP_SHIFT) << s_log2;
   p->R = (uint32_t)((n + (1ull << s_log2) - 1) >> s_log2);
   p->dyn_cap = (uint32_t)(n / p->cap + 1);
 }
@@ -119,9 +121,8 @@ static int debug_env(const char* name) {
 
 // PBIT_SMALL=0 sends small lists through the general path too (experiments, tests)
 static bool small_path_disabled() {
-  static int v = -1;
-  if (v < 0) { const char* e = getenv("PBIT_SMALL"); v = (e && atoi(e) == 0) ? 1 : 0; }
-  return v != 0;
+  static const bool v = [] { const char* e = getenv("PBIT_SMALL"); return e && atoi(e) == 0; }();
+  return v;
 }
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -266,13 +267,14 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   const uint32_t R_static = p.R + (head_is_ruler ? 0u : 1u);
   const uint32_t head_ruler = head_is_ruler ? (head >> p.s_log2) : p.R;
   {
-    static int walk_occ[9] = {0};  // resident walk CTAs per SM, by key bytes
-    if (!walk_occ[KB]) {
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&walk_occ[KB], k_walk<KB>, WALK_THREADS, 0);
-      if (walk_occ[KB] < 1) walk_occ[KB] = 1;
-      if (int cap_occ = debug_env("PBIT_WALK_OCC")) walk_occ[KB] = std::min(walk_occ[KB], cap_occ);  // experiments
-    }
-    int blocks = sms * walk_occ[KB];  // one wave: the rulers are split statically over the CTAs
+    static const int walk_occ = [] {  // resident walk CTAs per SM (one arch per process)
+      int occ = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KB>, WALK_THREADS, 0);
+      occ = std::max(occ, 1);
+      if (int cap_occ = debug_env("PBIT_WALK_OCC")) occ = std::min(occ, cap_occ);  // experiments
+      return occ;
+    }();
+    int blocks = sms * walk_occ;  // one wave: the rulers are split statically over the CTAs
     const uint32_t min_per = 4;
     if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
