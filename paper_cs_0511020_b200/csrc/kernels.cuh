@@ -1006,7 +1006,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
     __syncthreads();
     // exclusive scan of the tile's bin counts; claim the tile's space in every bin
     const uint32_t parent = FROM_IDS ? 0u : base >> (shift + bits);
-    uint32_t claim = 0;
+    uint32_t claim = 0, my_start = 0;
     {
       const uint32_t c = t < nb ? sm.cnt[t] : 0u;
       uint32_t y = c;
@@ -1020,7 +1020,8 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
       uint32_t add = 0;
       for (uint32_t q = 0; q < w; ++q) add += sm.warp[q];
       if (t < nb) {
-        sm.start[t] = y - c + add;
+        my_start = y - c + add;
+        sm.start[t] = my_start;
         if (c) claim = atomicAdd(cursor + ((parent << bits) | t), c);  // round trip overlaps the staging
       }
     }
@@ -1030,7 +1031,9 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
       const uint32_t j = i * PART_THREADS + t;
       if (j < cnt) sm.stage[sm.start[(x[i].x >> shift) & mask] + r[i]] = x[i];
     }
-    if (t < nb) sm.gofs[t] = (((parent << bits) | t) << shift) + claim;
+    // gofs[b] = where the bin's claimed run starts minus where it starts in the stage
+    // (mod 2^32), so a staged pair j goes to gofs[b] + j: one table lookup per pair
+    if (t < nb) sm.gofs[t] = (((parent << bits) | t) << shift) + claim - my_start;
     __syncthreads();
     // coalesced write-out: consecutive threads store consecutive staged pairs, which land
     // contiguously inside each bin's run
@@ -1038,7 +1041,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
     for (uint32_t j = t; j < cnt; j += PART_THREADS) {
       const uint2 p = sm.stage[j];
       const uint32_t b = (p.x >> shift) & mask;
-      __stcs(pout + sm.gofs[b] + (j - sm.start[b]), p);
+      __stcs(pout + (sm.gofs[b] + j), p);
     }
     __syncthreads();  // stage, start and gofs are rewritten by the next tile
   }

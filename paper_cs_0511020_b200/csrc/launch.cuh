@@ -80,6 +80,23 @@ static void launch_key_passes_k(int K, const SweepArgs& a, const Plan& plan, boo
 }
 
 // Cursor words launch_relink needs (zeroed by the caller before the call).
+// Grid of a grid-stride kernel: at most one full wave (every CTA resident at once).  A
+// grid of sms x 8 CTAs for a kernel that fits 6 per SM runs a second, one-third-full wave
+// after the first, with every CTA holding an equal share of the work.
+template <typename Kern>
+static inline int full_wave(Kern kernel, int threads, size_t smem, int sms, uint64_t want_blocks) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    occ = 1;
+  }
+#ifdef PBIT_FIXED_GRID  // A/B experiments: the old fixed grid
+  occ = 8;
+#endif
+  const uint64_t cap = (uint64_t)sms * (uint64_t)std::max(occ, 1);
+  return (int)std::max<uint64_t>(1, std::min(want_blocks, cap));
+}
+
 static inline size_t relink_cursor_words(uint32_t n) {
   RelinkLevels lv(n);
   size_t c = 0;

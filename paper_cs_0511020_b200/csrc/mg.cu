@@ -222,7 +222,8 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
     // ---- 1. pack the own slice into its place of the replica; local histograms
     if (n_local) {
-      const int blocks = std::max(1, std::min((int)((n_local + 255) / 256), sms * 8));
+      const int blocks = full_wave(k_pack<KB>, PACK_THREADS, (size_t)D * radix * 4, sms,
+                                   (n_local + PACK_THREADS - 1) / PACK_THREADS);
       ++launches;
       k_pack<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys_local, next_local, n_local, n,
                                                                        kn + lo, hist_l, K, D, err, km);
@@ -248,7 +249,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
     // ---- 3. rank the ruler list (identical on every rank)
     {
-      const int sblocks = std::max(1, std::min((int)((nsub + 255) / 256), sms * 8));
+      const int sblocks = full_wave(k_rank_walk_a, 256, 0, sms, (nsub + 255) / 256);
       ++launches;
       k_rank_walk_a<<<sblocks, 256, 0, st>>>(seg, sub, Rmax, zero, 0, head_ruler, nsub, sdist[0], scnt[0], ssucc[0],
                                              err);

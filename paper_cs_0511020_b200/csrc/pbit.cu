@@ -252,8 +252,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   // a1/a2: pack + histograms
   {
     NvtxRange nv("pbit.pack");
-    const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
     const size_t smem = (size_t)p.D * radix * 4;
+    const int blocks = full_wave(k_pack<KB>, PACK_THREADS, smem, sms, (n + PACK_THREADS - 1) / PACK_THREADS);
     const KeyMap km{p.key_kind, p.descending};
     k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
     ++launches;
@@ -293,7 +293,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const bool hs = sub.is_ruler(head_ruler);
     const uint32_t nsub = sub.R + (hs ? 0u : 1u);
     const uint32_t head_sub = hs ? (head_ruler >> SUB_LOG2) : sub.R;
-    const int sblocks = std::max(1, std::min((int)((nsub + 255) / 256), sms * 8));
+    const int sblocks = full_wave(k_rank_walk_a, 256, 0, sms, (nsub + 255) / 256);
     k_rank_walk_a<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
                                            w.sdist[0], w.scnt[0], w.ssucc[0], w.err);
     int rounds = 1;
@@ -335,7 +335,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   const bool ok = herr == 0;
   if (ok && hplan.npasses == 0) {  // a1: gather to list order -- only when no pass can fuse it
     const uint32_t Rmax = R_static + p.dyn_cap;
-    const int gblocks = std::max(1, std::min((int)((Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS)), sms * 8));
+    const int gblocks = full_wave(k_gather<KB>, 256, 0, sms, (Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS));
     k_gather<KB><<<gblocks, 256, 0, st>>>((const RT*)w.slots, p.cap, w.seg, w.dist, w.seg_ord, w.nseg, n,
                                           (typename KeyOf<KB>::T*)w.keys[0], w.ids[0], w.plan, w.err);
     ++launches;
@@ -545,7 +545,8 @@ static int run_array(const void* keys, uint32_t n, int key_bits, int K, KeyMap k
   cudaMemsetAsync(ctl, 0, ctl_bytes, st);
   cudaMemsetAsync(status, 0, status_bytes, st);
   {
-    const int blocks = std::max(1, std::min((int)((n + PACK_THREADS - 1) / PACK_THREADS), sms * 8));
+    const int blocks = full_wave(k_array_prep<KB>, PACK_THREADS, (size_t)D * radix * 4, sms,
+                                 (n + PACK_THREADS - 1) / PACK_THREADS);
     k_array_prep<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys, n, kbuf[0], hist, K, D, km);
     k_plan<<<1, 256, 0, st>>>(hist, bases, plan, D, K, n, err);
     launches += 2;
@@ -555,7 +556,7 @@ static int run_array(const void* keys, uint32_t n, int key_bits, int K, KeyMap k
   cudaMemcpyAsync(&hb->plan, plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
   const bool synced = cudaStreamSynchronize(st) == cudaSuccess;
   const Plan hplan = hb->plan;
-  const int fblocks = std::max(1, std::min((int)((n + 255) / 256), sms * 8));
+  const int fblocks = full_wave(k_array_finish<KB>, 256, 0, sms, (n + 255) / 256);
   if (synced) {
     if (hplan.npasses == 0) {  // one digit value everywhere: the input order is sorted
       k_array_finish<KB><<<fblocks, 256, 0, st>>>(kbuf[0], n, out_keys, out_index, km);
