@@ -111,6 +111,11 @@ void make_plan(uint64_t n, int key_bits, int K, SortPlan* p) {
 #endif
   p->cap = (1u << PBIT_CAP_SHIFT) << s_log2;
   p->R = (uint32_t)((n + (1ull << s_log2) - 1) >> s_log2);
+  // one sub-ruler per 8 rulers on ruler lists below 2^20 (their sub-segment walks are the
+  // latency-bound part), per 16 above (where the pointer jumping over the sub-rulers is);
+  // measured, DESIGN.md §7
+  static const int env_sub = [] { const char* e = getenv("PBIT_SUB_LOG2"); return e ? atoi(e) : -1; }();
+  p->sub_log2 = env_sub > 0 ? env_sub : (p->R < (1u << 20) ? 3 : 4);
   p->dyn_cap = (uint32_t)(n / p->cap + 1);
 }
 
@@ -126,7 +131,6 @@ static bool small_path_disabled() {
 }
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
-static constexpr int SUB_LOG2 = 4;  // one sub-ruler per 16 rulers
 
 // ----------------------------------------------------------------------------- dispatch
 // In-warp ranking mode for the stable key passes: RANK_ATOMIC unless the load-time
@@ -187,7 +191,7 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
     w->pairs[i] = base ? (uint2*)w->slots + i * align_up(n) : nullptr;
   w->seg = (uint2*)take(Rmax * 8);
   w->dist = (uint32_t*)take(Rmax * 4);
-  const size_t nsub = (Rmax >> SUB_LOG2) + 2;
+  const size_t nsub = (Rmax >> p.sub_log2) + 2;
   for (int i = 0; i < 2; ++i) {
     w->sdist[i] = (unsigned long long*)take(nsub * 8);
     w->scnt[i] = (uint32_t*)take(nsub * 4);
@@ -289,6 +293,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   {
     NvtxRange nv("pbit.rank");
     const uint32_t Rmax = R_static + p.dyn_cap;
+    const int SUB_LOG2 = p.sub_log2;
     RulerSel sub{Rmax, (uint32_t)SUB_LOG2, (Rmax + (1u << SUB_LOG2) - 1) >> SUB_LOG2};
     const bool hs = sub.is_ruler(head_ruler);
     const uint32_t nsub = sub.R + (hs ? 0u : 1u);

@@ -12,6 +12,7 @@ struct SortPlan {
   int K;        // digit bits
   int D;        // digits = ceil(key_bits / K)
   int s_log2;   // ruler spacing exponent
+  int sub_log2; // rulers per sub-ruler exponent (second ruling-set level of the ranking)
   uint32_t cap; // slot capacity per segment
   uint32_t R;   // static rulers (id blocks)
   uint32_t dyn_cap;
