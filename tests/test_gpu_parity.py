@@ -68,6 +68,10 @@ CASES = [
     (100003, 32, "equal", "random"), (100003, 32, "max", "random"), (100003, 64, "equal", "identity"),
     (100003, 32, "sorted", "random"), (100003, 32, "reverse", "random"), (250001, 64, "runs4096", "random"),
     (1000003, 32, "zipf", "random"), (1000003, 64, "uniform", "push"), (1 << 20, 32, "uniform", "identity"),
+    # the plan's size classes: 16-node segments and 8-ruler sub-segments (2^22..2^24),
+    # 32-node segments (2^24..2^26)
+    ((1 << 22) + 19, 32, "zipf", "random"), ((1 << 23) + 5, 64, "uniform", "random"),
+    ((1 << 24) + 1, 16, "uniform", "random"),
 ]
 
 
