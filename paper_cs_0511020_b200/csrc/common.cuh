@@ -67,6 +67,7 @@ struct RulerSel {
 struct Plan {
   uint32_t npasses;
   uint32_t digit[64];
+  uint32_t skewed[2];  // bit d: some value of digit d holds more than n/16 of the keys
 };
 
 // ----------------------------------------------------------------------------- loads

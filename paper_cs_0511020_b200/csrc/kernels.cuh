@@ -398,12 +398,14 @@ k_plan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases, Plan* __
   __shared__ uint32_t s_np;
   const int radix = 1 << K;
   const int t = threadIdx.x, lane = t & 31, w = t >> 5;
-  if (t == 0) s_np = 0;
+  if (t == 0) { s_np = 0; plan->skewed[0] = plan->skewed[1] = 0u; }
   __syncthreads();
   for (int d = 0; d < D; ++d) {
     // radix <= 256 == blockDim
     const uint32_t c = t < radix ? hist[d * radix + t] : 0u;
     const int trivial = __syncthreads_or(c == n);
+    const int skewed = __syncthreads_or(c > n / 16u);
+    if (t == 0 && skewed) plan->skewed[d >> 5] |= 1u << (d & 31);
     uint32_t x = c;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -513,6 +515,7 @@ struct SweepArgs {
   int digit;      // digit index
   int last;       // the last pass of the sort (write ids only)
   int src;        // input buffer index
+  int combine;    // ranking: lanes sharing lane 0's digit take one atomic (skewed digits)
   // first key pass (GATHER): the tile is read from the walk's segment slots, in list order
   const void* slots;
   uint32_t cap;
@@ -532,8 +535,36 @@ enum : int { RANK_BALLOT = 0, RANK_MATCH = 1, RANK_ATOMIC = 2 };
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK, bool FULL>
 __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd)[IPT], int shift,
                                            WCnt* __restrict__ wrow, uint32_t wofs, uint32_t lane,
-                                           uint32_t tile_count) {
+                                           uint32_t tile_count, bool combine = false) {
   constexpr int RADIX = 1 << RADIX_BITS;
+  if (RANK == RANK_ATOMIC && combine) {
+    // Skewed digits after the first pass: the input is sorted by the lower digits, so a
+    // heavy key fills long input stretches that a few other keys interrupt.  The lanes
+    // sharing lane 0's digit (eq) take ONE atomic, issued by lane 0 (the lowest lane, so
+    // the lane order of the remaining conflicting atomics is unchanged); the other lanes
+    // add 1 each as usual.
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) {
+      const bool valid = FULL || (wofs + i * 32 + lane < tile_count);
+      const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
+      const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+      const uint32_t eq = __ballot_sync(0xffffffffu, valid && d == d0);  // valid lanes: a prefix
+      const bool in_eq = (eq >> lane) & 1u;
+      const uint32_t add = lane == 0 ? (uint32_t)__popc(eq) : (valid && !in_eq ? 1u : 0u);
+      uint32_t r = 0;
+      if constexpr (sizeof(WCnt) == 4) {
+        if (add) r = atomicAdd(reinterpret_cast<uint32_t*>(wrow + d), add);
+      } else {
+        const uint32_t sh = (d & 1u) << 4;
+        uint32_t* wc = reinterpret_cast<uint32_t*>(wrow) + (d >> 1);
+        if (add) r = (atomicAdd(wc, add << sh) >> sh) & 0xFFFFu;
+      }
+      const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0);
+      r = in_eq ? r0 + (uint32_t)__popc(eq & lanemask_lt()) : r;
+      rd[i] = r | (d << 16);
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
     const bool valid = FULL || (wofs + i * 32 + lane < tile_count);
@@ -703,8 +734,9 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   uint32_t rd[IPT];
 #pragma unroll
   for (int i = 0; i < IPT; ++i) key[i] = AOS ? (KeyT)srec[wofs + i * 32 + lane].x : sm.k[wofs + i * 32 + lane];
-  if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
-  else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count);
+  const bool combine = a.combine != 0;
+  if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
+  else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
   __syncthreads();
 
   // ---- per digit (thread t = digit t): exclusive over warps, tile total, aggregate

@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <atomic>
 #include <mutex>
@@ -55,11 +57,18 @@ static void launch_key_passes(SweepArgs a, const Plan& plan, bool keep_keys, cud
                               int ev_base, int first_src, uint32_t* final_ids = nullptr) {
   using KeyT = typename KeyOf<KB>::T;
   constexpr int IPT = (KB == 8) ? SWEEP_IPT64 : SWEEP_IPT32;
+  // PBIT_COMBINE (experiments, tests): 0 never combine, 2 on every pass
+  const char* ce = getenv("PBIT_COMBINE");
+  const int combine_env = ce ? atoi(ce) : 1;
   for (uint32_t s = 0; s < plan.npasses; ++s) {
     a.slot = (int)s;
     a.digit = (int)plan.digit[s];
     a.src = (int)(s & 1);
     a.last = (s + 1 == plan.npasses) && !keep_keys;
+    // lane-0 combining in the ranking: on a skewed digit whose input is sorted by the
+    // lower digits (not the first pass) and not yet grouped by key (not the last)
+    const bool skewed = (plan.skewed[a.digit >> 5] >> (a.digit & 31)) & 1u;
+    a.combine = combine_env == 2 || (combine_env == 1 && skewed && s > 0 && s + 1 < plan.npasses);
     if (final_ids && s + 1 == plan.npasses) a.vout[a.src ^ 1] = final_ids;
     const int src = s == 0 ? first_src : SRC_TMA;
     if (src == SRC_GATHER) launch_one<KeyT, RB, IPT, SRC_GATHER>(a, st, rank_mode());
@@ -79,7 +88,6 @@ static void launch_key_passes_k(int K, const SweepArgs& a, const Plan& plan, boo
   }
 }
 
-// Cursor words launch_relink needs (zeroed by the caller before the call).
 // Grid of a grid-stride kernel: at most one full wave (every CTA resident at once).  A
 // grid of sms x 8 CTAs for a kernel that fits 6 per SM runs a second, one-third-full wave
 // after the first, with every CTA holding an equal share of the work.
@@ -97,6 +105,7 @@ static inline int full_wave(Kern kernel, int threads, size_t smem, int sms, uint
   return (int)std::max<uint64_t>(1, std::min(want_blocks, cap));
 }
 
+// Cursor words launch_relink needs (zeroed by the caller before the call).
 static inline size_t relink_cursor_words(uint32_t n) {
   RelinkLevels lv(n);
   size_t c = 0;

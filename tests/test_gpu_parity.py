@@ -101,6 +101,19 @@ def test_wide_patterns_vs_oracle_K16(pbit, K):
     assert np.array_equal(idx.cpu().numpy().view(np.uint32), np.argsort(kn, kind="stable").astype(np.uint32))
 
 
+@pytest.mark.parametrize("n,key_bits,keys,K", [(300007, 32, "uniform", 8), (300007, 32, "zipf", 4),
+                                                 (100003, 64, "runs4096", 8), (8191, 16, "equal", 3)])
+def test_lane0_combining_on_every_pass(pbit, monkeypatch, n, key_bits, keys, K):
+    """The ranking's lane-0 combining (normally only on skewed middle passes) forced on
+    every pass, first and last included, on inputs of every shape."""
+    monkeypatch.setenv("PBIT_COMBINE", "2")
+    li = workloads.make_list(n, key_bits, seed=n + K, keys=keys, device="cuda")
+    _assert_same(_gpu_sort(pbit, li, K=K), _oracle(li), f"combine {li.name} K={K}")
+    idx, _ = pbit.sort_array(li.keys, key_bits=key_bits, digit_bits=K)
+    kn = workloads.keys_numpy(li)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), np.argsort(kn, kind="stable").astype(np.uint32))
+
+
 @pytest.mark.parametrize("K", [3, 5, 8])
 def test_digit_width_sweep_u64_narrow_top_digit(pbit, K):
     li = workloads.make_list(70001, 64, seed=78, keys="uniform", device="cuda")
