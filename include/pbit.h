@@ -169,7 +169,13 @@ int pbit_sort_array(const void *keys, uint64_t n, int key_bits, uint32_t *out_in
  *   out_next_local [out] device, n_local global successor ids for this rank's nodes.
  *   nccl_comm      [in]  ncclComm_t (see pbit_mg_comm_init) spanning the G ranks.
  *   opts           [in]  as above (stream used for every kernel and collective).
- * Collective: every rank must call it with the same head, n_global, key_bits, K.
+ * Collective: every rank must call it with the same head, n_global, key_bits, K,
+ * key_kind and descending, and the ranks that own nodes all with or all without
+ * opts->out_prev.  The ranks first agree on their arguments (one small all-reduce): if any
+ * rank's arguments are invalid, or the shared ones differ, EVERY rank returns the error
+ * (the largest status code any rank saw) before data moves.  A NULL nccl_comm or
+ * out_head returns PBIT_ERR_INVALID_ARG on that rank alone (the others then time out in
+ * the agreement with PBIT_ERR_NCCL after PBIT_MG_TIMEOUT_S).
  * Rank r returns the successors of its own nodes; the sorted positions it computed
  * internally are [r*S, r*S + S) (top-digit sharding, position-exact).
  */

@@ -19,31 +19,73 @@ def nccl_dirs():
     return os.path.join(base, "include"), os.path.join(base, "lib")
 
 
-def nvcc_cmd(out=LIB, extra=()):
+def nvcc_cmd(out=LIB, extra=(), link_nccl=True):
+    """link_nccl=False: NCCL headers only (the test build that links a stand-in)."""
     inc, lib = nccl_dirs()
+    link = [f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"] if link_nccl else []
     return ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
             "-Xcompiler", "-fPIC,-O2", "-shared", "-Xptxas", "-v" if os.environ.get("PBIT_PTXAS_V") else "-O3",
             f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}",
             *[os.path.join(CSRC, s) for s in SOURCES],
-            f"-L{lib}", "-l:libnccl.so.2", f"-Xlinker", f"-rpath={lib}", *extra, "-o", out]
+            *link, *extra, "-o", out]
+
+
+OBJDIR = os.path.join(ROOT, "build", "obj")
+
+
+def _common_flags():
+    inc, _ = nccl_dirs()
+    return ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+            "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v" if os.environ.get("PBIT_PTXAS_V") else "-O3",
+            f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}"]
+
+
+def _deps():
+    return [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "pbit.h"), __file__]
+
+
+def _newer(target, deps):
+    return not os.path.exists(target) or any(os.path.getmtime(d) > os.path.getmtime(target) for d in deps)
+
+
+def objects(force: bool = False, verbose: bool = False) -> list:
+    """Compile each source to build/obj/<name>.o, in parallel (the two sources take about
+    the same time); shared by libpbit.so and the tests' fake-NCCL build."""
+    os.makedirs(OBJDIR, exist_ok=True)
+    objs, procs = [], []
+    for src in SOURCES:
+        obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
+        objs.append(obj)
+        if force or _newer(obj, _deps()):
+            cmd = ["nvcc", *_common_flags(), "-c", os.path.join(CSRC, src), "-o", obj + f".tmp{os.getpid()}"]
+            if verbose:
+                print(" ".join(cmd), file=sys.stderr)
+            procs.append((obj, subprocess.Popen(cmd)))
+    bad = [o for o, p in procs if p.wait() != 0]
+    if bad:
+        raise RuntimeError(f"nvcc failed: {bad}")
+    for o, _ in procs:
+        os.replace(o + f".tmp{os.getpid()}", o)
+    return objs
+
+
+def link(out: str, objs: list, link_nccl: bool = True, extra=()) -> None:
+    _, lib = nccl_dirs()
+    nccl = [f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}"] if link_nccl else []
+    tmp = out + f".tmp{os.getpid()}"
+    subprocess.check_call(["nvcc", "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *objs, *nccl,
+                           *extra, "-o", tmp])
+    os.replace(tmp, out)
 
 
 def stale():
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(ROOT, "include", "pbit.h"), __file__]
-    return any(os.path.getmtime(d) > t for d in deps)
+    return _newer(LIB, _deps())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if force or stale():
-        tmp = LIB + f".tmp{os.getpid()}"
-        cmd = nvcc_cmd(tmp)
-        if verbose:
-            print(" ".join(cmd), file=sys.stderr)
-        subprocess.check_call(cmd)
-        os.replace(tmp, LIB)
+        objs = objects(force=force, verbose=verbose)
+        link(LIB, objs)
     return LIB
 
 

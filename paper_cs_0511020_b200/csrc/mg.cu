@@ -73,11 +73,7 @@ struct Bump {
 // timeout the call returns PBIT_ERR_NCCL; the caller then aborts the communicator
 // (pbit_mg_comm_abort), which also releases the stream.
 static int mg_wait(cudaStream_t st, ncclComm_t comm) {
-  static double timeout_s = -1.0;
-  if (timeout_s < 0) {
-    const char* e = getenv("PBIT_MG_TIMEOUT_S");
-    timeout_s = e ? atof(e) : 300.0;
-  }
+  static const double timeout_s = [] { const char* e = getenv("PBIT_MG_TIMEOUT_S"); return e ? atof(e) : 300.0; }();
   const auto t0 = std::chrono::steady_clock::now();
   for (unsigned spin = 0;; ++spin) {
     const cudaError_t q = cudaStreamQuery(st);
@@ -112,7 +108,8 @@ static int mg_wait(cudaStream_t st, ncclComm_t comm) {
 template <int KB>
 int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint32_t n, uint32_t S,
            uint32_t n_local, int K, KeyMap km, uint32_t* out_head, uint32_t* out_next_local,
-           uint32_t* out_prev_local, ncclComm_t comm, int G, int r, cudaStream_t st, uint32_t* launches_out) {
+           uint32_t* out_prev_local, bool with_prev, ncclComm_t comm, int G, int r, cudaStream_t st,
+           uint32_t* launches_out) {
   using RT = typename Rec<KB>::T;
   uint32_t launches = 0;
   using KeyT = typename KeyOf<KB>::T;
@@ -411,8 +408,10 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     CUDACHK(cudaMemcpyAsync(h_firsts, firsts, 8ull * G, cudaMemcpyDeviceToHost, st));
     MGWAIT();
     for (int dir = 1; dir >= -1; dir -= 2) {
+      // with_prev is the same on every rank (agreed before the first collective): a rank
+      // without own nodes still routes its share of the (v, pred) pairs
+      if (dir < 0 && !with_prev) continue;
       uint32_t* out_local = dir > 0 ? out_next_local : out_prev_local;
-      if (!out_local) continue;
       uint32_t edge = PBIT_NULL32;  // next rank's first id / previous rank's last id
       if (dir > 0) {
         for (int d = r + 1; d < G; ++d)
@@ -552,55 +551,99 @@ uint64_t pbit_mg_slice(uint64_t n_global, int nranks) {
   return (per + 63) / 64 * 64;
 }
 
+// Every rank's verdict on its arguments, and the arguments every rank must share, agreed
+// by one small all-reduce before any data moves: a bad argument on one rank then fails the
+// call on every rank, instead of leaving the others waiting in the first collective.
+// shared[0..ns): must be equal on all ranks (compared as max and ~max(~x) = min);
+// flags[0..nf): returned as the maximum over the ranks.  Returns the largest status any
+// rank reported, or INVALID_ARG if the shared values differ.
+static int mg_agree(int rc_local, const uint64_t* shared, int ns, uint64_t* flags, int nf, ncclComm_t comm,
+                    cudaStream_t st) {
+  std::vector<uint64_t> h(1 + 2 * (size_t)ns + nf);
+  h[0] = (uint64_t)rc_local;
+  for (int i = 0; i < ns; ++i) { h[1 + i] = shared[i]; h[1 + ns + i] = ~shared[i]; }
+  for (int i = 0; i < nf; ++i) h[1 + 2 * ns + i] = flags[i];
+  uint64_t* d = nullptr;
+  const size_t bytes = 8 * h.size();
+  if (cudaMallocAsync((void**)&d, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  int rc = PBIT_OK;
+  if (cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = PBIT_ERR_CUDA;
+  if (!rc && ncclAllReduce(d, d, h.size(), ncclUint64, ncclMax, comm, st) != ncclSuccess) rc = PBIT_ERR_NCCL;
+  if (!rc && cudaMemcpyAsync(h.data(), d, bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = PBIT_ERR_CUDA;
+  if (!rc) rc = mg_wait(st, comm);
+  cudaFreeAsync(d, st);
+  if (rc) return rc;
+  for (int i = 0; i < nf; ++i) flags[i] = h[1 + 2 * ns + i];
+  for (int i = 0; i < ns; ++i)
+    if (h[1 + i] != ~h[1 + ns + i]) {
+      set_last_error("pbit_sort_list_mg", "the ranks passed different shared arguments");
+      return std::max<int>((int)h[0], PBIT_ERR_INVALID_ARG);
+    }
+  return (int)h[0];
+}
+
 int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint64_t n_global,
                       uint64_t node_lo, uint64_t n_local, int key_bits, uint32_t* out_head,
                       uint32_t* out_next_local, void* nccl_comm, const pbit_opts* opts) {
-  if (!nccl_comm || !out_head) return PBIT_ERR_INVALID_ARG;
-  if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
-  const int K = pass_bits(opts && opts->digit_bits ? opts->digit_bits : 8);
-  if (!K) return PBIT_ERR_INVALID_ARG;
-  if (n_global > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
-  uint32_t* out_prev_local = opts ? opts->out_prev : nullptr;
-  if (out_prev_local && out_prev_local == out_next_local) return PBIT_ERR_INVALID_ARG;
-  const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
-  if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
-  cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
+  if (!nccl_comm || !out_head) return PBIT_ERR_INVALID_ARG;  // no communicator to agree over
+  ncclComm_t comm = (ncclComm_t)nccl_comm;
   int G = 0, r = 0;
-  if (ncclCommCount((ncclComm_t)nccl_comm, &G) != ncclSuccess) return PBIT_ERR_NCCL;
-  if (ncclCommUserRank((ncclComm_t)nccl_comm, &r) != ncclSuccess) return PBIT_ERR_NCCL;
-  if (G > 64) return PBIT_ERR_UNSUPPORTED;
+  if (ncclCommCount(comm, &G) != ncclSuccess) return PBIT_ERR_NCCL;
+  if (ncclCommUserRank(comm, &r) != ncclSuccess) return PBIT_ERR_NCCL;
+  cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
+  const int K = pass_bits(opts && opts->digit_bits ? opts->digit_bits : 8);
+  uint32_t* out_prev_local = opts ? opts->out_prev : nullptr;
+  const KeyMap km{opts ? opts->key_kind : PBIT_KEY_UNSIGNED, opts && opts->descending ? 1 : 0};
   const uint64_t S = pbit_mg_slice(n_global, G);
-  const uint64_t want_lo = (uint64_t)r * S;
-  const uint64_t want_n = n_global > want_lo ? std::min<uint64_t>(S, n_global - want_lo) : 0;
-  if (node_lo != want_lo || n_local != want_n) return PBIT_ERR_UNSUPPORTED;
-  if ((uint64_t)G * S > 0xFFFFFFFFull) return PBIT_ERR_UNSUPPORTED;
+  // this rank's own checks (status codes as in pbit.h)
+  const int rc_local = [&]() -> int {
+    if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return PBIT_ERR_INVALID_ARG;
+    if (!K) return PBIT_ERR_INVALID_ARG;
+    if (n_global > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+    if (out_prev_local && out_prev_local == out_next_local) return PBIT_ERR_INVALID_ARG;
+    if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
+    if (G > 64) return PBIT_ERR_UNSUPPORTED;
+    const uint64_t want_lo = (uint64_t)r * S;
+    const uint64_t want_n = n_global > want_lo ? std::min<uint64_t>(S, n_global - want_lo) : 0;
+    if (node_lo != want_lo || n_local != want_n) return PBIT_ERR_UNSUPPORTED;
+    if ((uint64_t)G * S > 0xFFFFFFFFull) return PBIT_ERR_UNSUPPORTED;
+    if (n_global && (uint64_t)head >= n_global) return PBIT_ERR_INVALID_ARG;
+    if (n_local && (!keys_local || !next_local || !out_next_local)) return PBIT_ERR_INVALID_ARG;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
+    if (n_local && (pointer_kind(keys_local, dev) != 1 || pointer_kind(next_local, dev) != 1 ||
+                    pointer_kind(out_next_local, dev) != 1 ||
+                    (out_prev_local && pointer_kind(out_prev_local, dev) != 1)))
+      return PBIT_ERR_INVALID_ARG;
+    return PBIT_OK;
+  }();
+  // shared by all ranks: the list, the key format, the digit width.  out_prev: the ranks
+  // that own nodes must all pass it or none (flags: some rank with / without it)
+  const uint64_t shared[6] = {n_global, head, (uint64_t)key_bits, (uint64_t)K, (uint64_t)km.kind,
+                              (uint64_t)km.descending};
+  uint64_t flags[2] = {n_local && out_prev_local ? 1ull : 0ull, n_local && !out_prev_local ? 1ull : 0ull};
+  int rc = mg_agree(rc_local, shared, 6, flags, 2, comm, st);
+  if (rc) return rc;
+  if (flags[0] && flags[1]) {
+    set_last_error("pbit_sort_list_mg", "out_prev passed on some ranks but not on others");
+    return PBIT_ERR_INVALID_ARG;
+  }
+  const bool with_prev = flags[0] != 0;
   if (n_global == 0) {
     if (head != PBIT_NULL) return PBIT_ERR_INVALID_LIST;
     *out_head = PBIT_NULL;
     return PBIT_OK;
   }
-  if ((uint64_t)head >= n_global) return PBIT_ERR_INVALID_ARG;
-  if (n_local && (!keys_local || !next_local || !out_next_local)) return PBIT_ERR_INVALID_ARG;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
-  if (n_local && (pointer_kind(keys_local, dev) != 1 || pointer_kind(next_local, dev) != 1 ||
-                  pointer_kind(out_next_local, dev) != 1 ||
-                  (out_prev_local && pointer_kind(out_prev_local, dev) != 1)))
-    return PBIT_ERR_INVALID_ARG;
+#define PBIT_RUN_MG(KB)                                                                                          \
+  run_mg<KB>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km, out_head,   \
+             out_next_local, out_prev_local, with_prev, comm, G, r, st, opts ? opts->launches : nullptr)
   switch (key_bits) {
-    case 8: return run_mg<1>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                             out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
-                             opts ? opts->launches : nullptr);
-    case 16: return run_mg<2>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                              out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
-                             opts ? opts->launches : nullptr);
-    case 32: return run_mg<4>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                              out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
-                             opts ? opts->launches : nullptr);
-    default: return run_mg<8>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km,
-                              out_head, out_next_local, out_prev_local, (ncclComm_t)nccl_comm, G, r, st,
-                             opts ? opts->launches : nullptr);
+    case 8: return PBIT_RUN_MG(1);
+    case 16: return PBIT_RUN_MG(2);
+    case 32: return PBIT_RUN_MG(4);
+    default: return PBIT_RUN_MG(8);
   }
+#undef PBIT_RUN_MG
 }
 
 }  // extern "C"

@@ -1,0 +1,160 @@
+"""TEST INFRASTRUCTURE: pbit_sort_list_mg with G ranks, as G host threads on ONE GPU.
+
+The library is the product's own objects linked with tests/fake_nccl/fake_nccl.cpp in
+place of NCCL (NCCL refuses two ranks on one device), so every step of mg.cu -- its
+kernels, its host planning, the exchanges -- runs for real at G > 1; only the transport
+is emulated (device-to-device copies between the ranks' buffers, host barriers).  Each
+case assembles the ranks' out_next (and out_prev) slices and compares them bit for bit
+with the paper-literal oracle.  Prints one line per case; exit status 1 on any mismatch.
+
+    python tests/fake_nccl/run_mg_threads.py            # the default case list
+"""
+from __future__ import annotations
+
+import os
+import sys
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, HERE)
+
+import build_fake  # noqa: E402
+
+os.environ["PBIT_LIB_PATH"] = build_fake.build()
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle  # noqa: E402
+import paper_cs_0511020_b200 as p  # noqa: E402
+import workloads  # noqa: E402
+
+assert p.LIB_PATH == os.environ["PBIT_LIB_PATH"], "the fake-NCCL library must be the one loaded"
+
+# (G, n, key_bits, keys, links, K, kind, descending, with_prev)
+CASES = [
+    (2, 100003, 32, "uniform", "random", 0, "unsigned", False, True),
+    (2, 4097, 32, "zipf", "random", 8, "unsigned", False, False),
+    (3, 250001, 32, "zipf", "random", 0, "unsigned", False, True),
+    (3, 77, 8, "uniform", "push", 4, "unsigned", False, False),       # a rank with no nodes
+    (4, 130, 32, "zipf", "random", 0, "unsigned", False, True),       # two, with out_prev
+    (4, 200001, 64, "runs4096", "random", 0, "unsigned", False, True),
+    (4, 300007, 32, "equal", "random", 0, "unsigned", False, False),  # one key value
+    (2, 123457, 32, "uniform", "random", 0, "float", True, False),
+    (3, 123457, 16, "uniform", "identity", 5, "signed", False, True),
+    (8, 1 << 20, 32, "uniform", "random", 0, "unsigned", False, True),
+    (5, 65536, 8, "uniform", "random", 4, "unsigned", False, False),
+]
+
+
+def run_case(G, n, key_bits, keys, links, K, kind, desc, with_prev, seed):
+    li = workloads.make_list(n, key_bits, seed=seed, keys=keys, links=links, device="cuda")
+    S = p.mg_slice(n, G)
+    uid = p.mg_unique_id()
+    res, errs = [None] * G, [None] * G
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            lo, hi = min(n, r * S), min(n, (r + 1) * S)
+            with torch.cuda.stream(st):
+                comm = p.mg_comm_init(G, uid, r)
+                prev = torch.empty(hi - lo, dtype=torch.int32, device="cuda") if with_prev else None
+                # node_lo = r * S even for a rank whose slice is empty (pbit.h)
+                h, out = p.sort_list_mg(li.keys[lo:hi], li.next[lo:hi], li.head, n, r * S, comm, key_bits=key_bits,
+                                        digit_bits=K, key_kind=kind, descending=desc, stream=st,
+                                        out_prev_local=prev)
+                st.synchronize()
+                res[r] = (h, out.cpu().numpy().view(np.uint32).copy(),
+                          prev.cpu().numpy().view(np.uint32).copy() if with_prev else None)
+                p.mg_comm_destroy(comm)
+        except Exception as e:  # noqa: BLE001  (reported by the main thread)
+            errs[r] = e
+
+    ts = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(G)]
+    for t in ts:
+        t.start()
+    import time
+    t0 = time.time()
+    while any(t.is_alive() for t in ts):
+        time.sleep(0.05)
+        # a rank that failed leaves the others waiting in a collective (as NCCL would)
+        if any(errs) and time.time() - t0 > 5 or time.time() - t0 > 120:
+            return False, (f"rank errors {[(r, repr(e)) for r, e in enumerate(errs) if e]}, "
+                           f"ranks still inside the call: {[r for r, t in enumerate(ts) if t.is_alive()]}"), True
+    if any(errs):
+        return False, f"rank errors: {[repr(e) for e in errs if e]}", False
+    heads = {r_[0] for r_ in res}
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4,
+                              descending=desc, kind=kind)
+    got = np.concatenate([r_[1] for r_ in res]) if n else np.zeros(0, np.uint32)
+    if heads != {oh}:
+        return False, f"heads {heads} != {oh}", False
+    if not np.array_equal(got, on):
+        bad = int(np.flatnonzero(got != on)[0])
+        return False, f"out_next differs first at node {bad}: {got[bad]} != {on[bad]}", False
+    if with_prev:
+        gp = np.concatenate([r_[2] for r_ in res])
+        if not np.array_equal(gp, oracle.repair_back(on, oh)):
+            return False, "out_prev differs from the oracle's repair walk", False
+    return True, "ok", False
+
+
+def run_mismatch(G=3):
+    """Rank 1 passes a different digit width: every rank must return INVALID_ARG from the
+    argument agreement (none may be left waiting in a collective)."""
+    n = 10007
+    li = workloads.make_list(n, 32, seed=3, keys="uniform", device="cuda")
+    S = p.mg_slice(n, G)
+    uid = p.mg_unique_id()
+    codes = [None] * G
+
+    def rank(r):
+        torch.cuda.set_device(0)
+        st = torch.cuda.Stream()
+        lo, hi = min(n, r * S), min(n, (r + 1) * S)
+        with torch.cuda.stream(st):
+            comm = p.mg_comm_init(G, uid, r)
+            try:
+                p.sort_list_mg(li.keys[lo:hi], li.next[lo:hi], li.head, n, r * S, comm, stream=st,
+                               digit_bits=4 if r == 1 else 8)
+                codes[r] = 0
+            except p.PbitError as e:
+                codes[r] = e.code
+            p.mg_comm_destroy(comm)
+
+    ts = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=60)
+    ok = not any(t.is_alive() for t in ts) and codes == [1] * G
+    print(f"G={G} mismatched digit_bits on rank 1: codes {codes}: {'ok' if ok else 'FAILED'}", flush=True)
+    return ok
+
+
+def main(argv):
+    cases = CASES
+    if argv:  # e.g. "3,250001,32,zipf,random,0,unsigned,0,1"
+        f = argv[0].split(",")
+        cases = [(int(f[0]), int(f[1]), int(f[2]), f[3], f[4], int(f[5]), f[6], bool(int(f[7])), bool(int(f[8])))]
+    fails = 0
+    for i, c in enumerate(cases):
+        ok, msg, stuck = run_case(*c, seed=1000 + i)
+        print(f"G={c[0]} n={c[1]} u{c[2]} {c[3]}/{c[4]} K={c[5]} {c[6]}{' desc' if c[7] else ''}"
+              f"{' +prev' if c[8] else ''}: {msg}", flush=True)
+        fails += not ok
+        if stuck:  # threads blocked in the fake transport cannot be joined: stop here
+            print(f"{i + 1 - fails}/{len(cases)} cases bit-exact (stopped)", flush=True)
+            os._exit(1)
+    print(f"{len(cases) - fails}/{len(cases)} cases bit-exact", flush=True)
+    if not argv and not run_mismatch():
+        fails += 1
+    return 1 if fails else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main(sys.argv[1:]))

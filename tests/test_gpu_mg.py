@@ -1,8 +1,9 @@
 """pbit_sort_list_mg through the C-ABI on the one GPU available: a 1-rank NCCL
 communicator runs every step of the multi-GPU protocol (pack + all-gather, count walk,
 segment-table exchange, ranking, emit walk, top-digit partition + exchange, local sort,
-stitch, owner routing, relink), compared bit-exactly with the oracle.  The G > 1
-exchange logic is covered on CPU by tests/test_mg_protocol.py (gloo, world_size 2-3)."""
+stitch, owner routing, relink), compared bit-exactly with the oracle.  G > 1: the real
+kernels at G = 2-8 in tests/test_gpu_mg_threads.py (stand-in transport, one GPU), and the
+protocol on CPU in tests/test_mg_protocol.py (gloo, world_size 2-4)."""
 from __future__ import annotations
 
 import numpy as np
