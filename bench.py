@@ -239,13 +239,14 @@ def run_mg(args):
     li = workloads.make_config(args.config, device="cuda", n=n)
     S = pbit.mg_slice(n, ws)
     lo, hi = min(n, rank * S), min(n, rank * S + S)
+    node_lo = rank * S  # pbit.h: node_lo = rank * S, also for a rank whose slice is empty
     keys, nxt, head, kb = li.keys[lo:hi].clone(), li.next[lo:hi].clone(), li.head, li.key_bits
     del li
     torch.cuda.empty_cache()
     out = torch.empty_like(nxt)
     st = torch.cuda.current_stream()
     for _ in range(max(args.warmup, 3)):
-        pbit.sort_list_mg(keys, nxt, head, n, lo, comm, digit_bits=K, out_next_local=out)
+        pbit.sort_list_mg(keys, nxt, head, n, node_lo, comm, digit_bits=K, out_next_local=out)
     torch.cuda.synchronize()
     dist.barrier()
     torch.cuda.synchronize()
@@ -253,7 +254,7 @@ def run_mg(args):
     with ClockSampler(local) as clk:
         e0.record(st)
         for _ in range(args.steps):
-            pbit.sort_list_mg(keys, nxt, head, n, lo, comm, digit_bits=K, out_next_local=out)
+            pbit.sort_list_mg(keys, nxt, head, n, node_lo, comm, digit_bits=K, out_next_local=out)
         e1.record(st)
         torch.cuda.synchronize()
     dist.barrier()
@@ -268,7 +269,7 @@ def run_mg(args):
     t0 = time.perf_counter()
     for _ in range(e_steps):
         kd, nd = kh.to("cuda", non_blocking=True), nh.to("cuda", non_blocking=True)
-        pbit.sort_list_mg(kd, nd, head, n, lo, comm, digit_bits=K, out_next_local=out)
+        pbit.sort_list_mg(kd, nd, head, n, node_lo, comm, digit_bits=K, out_next_local=out)
         oh.copy_(out, non_blocking=True)
         torch.cuda.synchronize()
     e2e_t = torch.tensor([(time.perf_counter() - t0) / e_steps], device="cuda")
