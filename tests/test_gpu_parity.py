@@ -128,6 +128,20 @@ def test_small_key_range_skips_trivial_digits(pbit):
     _assert_same((h, out.cpu().numpy().view(np.uint32)), _oracle(li), "C5-shaped")
 
 
+def test_largest_n_fails_cleanly_with_oom(pbit):
+    """n = 2^32 - 2, the largest the ABI accepts (u32 ids, PBIT_NULL reserved): the
+    workspace (~60 B/node) exceeds the 180 GB HBM, so the call must return PBIT_ERR_OOM
+    before any kernel runs, with no size arithmetic overflowing on the way."""
+    n = (1 << 32) - 2
+    keys = torch.empty(n, dtype=torch.uint8, device="cuda")
+    nx = torch.empty(n, dtype=torch.int32, device="cuda")
+    with pytest.raises(pbit.PbitError) as e:
+        pbit.sort_list(keys, nx, 0, key_bits=8, out_next=nx)  # in place: no third array
+    assert e.value.code == 3
+    del keys, nx
+    torch.cuda.empty_cache()
+
+
 def test_all_equal_keys_runs_no_pass(pbit):
     li = workloads.make_list(77777, 32, seed=6, keys="equal", device="cuda")
     h, out, ph = pbit.sort_list(li.keys, li.next, li.head, timing=True)
