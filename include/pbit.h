@@ -210,6 +210,14 @@ void pbit_mg_exchange_plan(int nranks, int rank, uint64_t n, uint64_t slice, con
                            const uint64_t *le, uint64_t *send_off, uint64_t *send_count,
                            uint64_t *recv_off, uint64_t *recv_count);
 
+/* Workspace.  Every call takes its workspace (about 60 B per node for 32-bit keys) from
+ * the library's own stream-ordered memory pool on the current device and returns it at
+ * the end of the call; the pool keeps up to half the device memory (PBIT_POOL_KEEP_GB
+ * overrides) mapped between calls, so repeated calls do not re-map memory.
+ * pbit_workspace_trim synchronizes the current device and releases cached workspace
+ * above keep_bytes (0 = all of it).  Returns PBIT_OK or PBIT_ERR_CUDA. */
+int pbit_workspace_trim(uint64_t keep_bytes);
+
 /* Text of the last CUDA or NCCL error seen by the calling host thread ("" if none). */
 const char *pbit_last_error(void);
 

@@ -22,7 +22,7 @@ NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
 SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_sort_array", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
            "pbit_mg_comm_destroy", "pbit_mg_comm_abort", "pbit_status_string", "pbit_version", "pbit_last_error",
-           "pbit_mg_slice", "pbit_mg_exchange_plan"]
+           "pbit_mg_slice", "pbit_mg_exchange_plan", "pbit_workspace_trim"]
 
 STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
           4: "PBIT_ERR_CUDA", 5: "PBIT_ERR_NCCL", 6: "PBIT_ERR_UNSUPPORTED"}
@@ -72,6 +72,8 @@ def _load():
     lib.pbit_status_string.argtypes = [ctypes.c_int]
     lib.pbit_version.restype = ctypes.c_uint32
     lib.pbit_last_error.restype = ctypes.c_char_p
+    lib.pbit_workspace_trim.restype = ctypes.c_int
+    lib.pbit_workspace_trim.argtypes = [ctypes.c_uint64]
     lib.pbit_mg_slice.restype = ctypes.c_uint64
     lib.pbit_mg_slice.argtypes = [ctypes.c_uint64, ctypes.c_int]
     u64p = ctypes.POINTER(ctypes.c_uint64)
@@ -205,6 +207,13 @@ def sort_array(keys, key_bits: int | None = None, digit_bits: int = 0, out_index
 
 # ----------------------------------------------------------------------------- multi-GPU
 last_mg_launches = 0  # kernels the last sort_list_mg call launched
+
+
+def workspace_trim(keep_bytes: int = 0) -> None:
+    """Release the library's cached workspace on the current device above keep_bytes."""
+    rc = lib.pbit_workspace_trim(ctypes.c_uint64(keep_bytes))
+    if rc:
+        raise PbitError(rc, _errtext(rc))
 
 
 def mg_unique_id() -> bytes:

@@ -208,7 +208,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   carve();
   const size_t bytes = b.off;
   char* base = nullptr;
-  if (cudaMallocAsync((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   b = Bump{base, 0};
   carve();
 
@@ -565,7 +565,7 @@ static int mg_agree(int rc_local, const uint64_t* shared, int ns, uint64_t* flag
   for (int i = 0; i < nf; ++i) h[1 + 2 * ns + i] = flags[i];
   uint64_t* d = nullptr;
   const size_t bytes = 8 * h.size();
-  if (cudaMallocAsync((void**)&d, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&d, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   int rc = PBIT_OK;
   if (cudaMemcpyAsync(d, h.data(), bytes, cudaMemcpyHostToDevice, st) != cudaSuccess) rc = PBIT_ERR_CUDA;
   if (!rc && ncclAllReduce(d, d, h.size(), ncclUint64, ncclMax, comm, st) != ncclSuccess) rc = PBIT_ERR_NCCL;

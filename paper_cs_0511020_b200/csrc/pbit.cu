@@ -63,9 +63,14 @@ void set_last_error(const char* what, const char* detail) {
 }
 
 // ----------------------------------------------------------------------------- device info
+// Per device: SM count, and the library's own stream-ordered memory pool for workspace.
+// The pool keeps freed workspace mapped between calls up to a release threshold (half the
+// device memory by default, PBIT_POOL_KEEP_GB overrides), so repeated calls do not re-map
+// memory; the device's default pool, which other code may use, is left alone.
+// pbit_workspace_trim() hands cached workspace back.
 struct DevInfo {
   int sms = 0;
-  bool pool_ready = false;
+  cudaMemPool_t pool = nullptr;
 };
 static std::mutex g_dev_mu;
 static DevInfo g_dev[64];
@@ -77,17 +82,35 @@ int device_info(int dev, int* sms) {
   if (!d.sms) {
     if (cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return PBIT_ERR_CUDA;
   }
-  if (!d.pool_ready) {
-    // keep freed workspace in the device pool between calls (stream-ordered allocator)
-    cudaMemPool_t pool;
-    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  if (!d.pool) {
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    if (cudaMemPoolCreate(&pool, &props) != cudaSuccess) {
+      cudaGetLastError();
+      return PBIT_ERR_CUDA;
     }
-    d.pool_ready = true;
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); total_b = 0; }
+    const char* e = getenv("PBIT_POOL_KEEP_GB");
+    uint64_t keep = e ? (uint64_t)(atof(e) * 1e9) : (uint64_t)total_b / 2;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    d.pool = pool;
   }
   *sms = d.sms;
   return PBIT_OK;
+}
+
+cudaError_t ws_alloc(void** ptr, size_t bytes, cudaStream_t st) {
+  int dev = 0, sms = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (device_info(dev, &sms) != PBIT_OK) return cudaErrorMemoryAllocation;
+  e = cudaMallocFromPoolAsync(ptr, bytes, g_dev[dev].pool, st);
+  if (e != cudaSuccess) cudaGetLastError();
+  return e;
 }
 
 // ----------------------------------------------------------------------------- planning
@@ -147,7 +170,7 @@ void init_rank_mode(cudaStream_t st) {
   } else {
     uint32_t* d_bad = nullptr;
     uint32_t bad = 1;
-    if (cudaMallocAsync((void**)&d_bad, 4, st) == cudaSuccess) {
+    if (ws_alloc((void**)&d_bad, 4, st) == cudaSuccess) {
       cudaMemsetAsync(d_bad, 0, 4, st);
       k_selftest_atomic_order<<<64, 256, 0, st>>>(4096, d_bad);
       cudaMemcpyAsync(&bad, d_bad, 4, cudaMemcpyDeviceToHost, st);
@@ -227,7 +250,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   Ws w;
   const size_t bytes = carve(p, nullptr, &w);
   char* base = nullptr;
-  if (cudaMallocAsync((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   carve(p, base, &w);
 
   // phase events come from a per-thread pool (created once), so timed calls carry no
@@ -430,7 +453,7 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
   const size_t a4 = align_up((size_t)n * 4), ak = align_up((size_t)n * sizeof(KeyT));
   const size_t bytes = 6 * a4 + 2 * ak + align_up(SMALL_CTAS * 256 * 4) + 256;  // dn: 2 x 2 x a4
   char* base = nullptr;
-  if (cudaMallocAsync((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   SmallArgs sa{};
   sa.keys = keys; sa.next = next; sa.head = head; sa.n = n; sa.out_next = out_next; sa.out_prev = out_prev;
   sa.km = km;
@@ -518,7 +541,7 @@ static int run_array(const void* keys, uint32_t n, int key_bits, int K, KeyMap k
   const size_t status_bytes = ntiles * (radix > 256 ? radix : 256) * 8;
   const size_t ctl_bytes = align_up((size_t)D * radix * 4) * 2 + align_up(sizeof(Plan)) + 256 + align_up(80 * 4);
   char* base = nullptr;
-  if (cudaMallocAsync((void**)&base, 2 * kb + 2 * ib + align_up(status_bytes) + ctl_bytes, st) != cudaSuccess) {
+  if (ws_alloc((void**)&base, 2 * kb + 2 * ib + align_up(status_bytes) + ctl_bytes, st) != cudaSuccess) {
     cudaGetLastError();
     return PBIT_ERR_OOM;
   }
@@ -635,6 +658,22 @@ const char* pbit_status_string(int s) {
   }
 }
 
+int pbit_workspace_trim(uint64_t keep_bytes) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) { cudaGetLastError(); return PBIT_ERR_CUDA; }
+  cudaMemPool_t pool;
+  {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    pool = g_dev[dev].pool;
+  }
+  if (!pool) return PBIT_OK;  // no call on this device yet: nothing cached
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemPoolTrimTo(pool, keep_bytes) != cudaSuccess) {
+    cudaGetLastError();
+    return PBIT_ERR_CUDA;
+  }
+  return PBIT_OK;
+}
+
 int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits,
                    uint32_t* out_head, uint32_t* out_next, const pbit_opts* opts) {
   if (!out_head) return PBIT_ERR_INVALID_ARG;
@@ -674,7 +713,7 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   const size_t kbytes = n * (size_t)(key_bits / 8), nbytes = n * 4;
   char* d = nullptr;
   const size_t a = align_up(kbytes), b = align_up(nbytes);
-  if (cudaMallocAsync((void**)&d, a + 3 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&d, a + 3 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   uint32_t* d_prev = out_prev ? (uint32_t*)(d + a + 2 * b) : nullptr;
   int rc = PBIT_OK;
   if (cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ||
@@ -730,7 +769,7 @@ int pbit_sort_array(const void* keys, uint64_t n, int key_bits, uint32_t* out_in
   const size_t kbytes = n * (size_t)(key_bits / 8), nbytes = n * 4;
   char* d = nullptr;
   const size_t a = align_up(kbytes), b = align_up(nbytes);
-  if (cudaMallocAsync((void**)&d, 2 * a + b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&d, 2 * a + b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   int rc = cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ? PBIT_ERR_CUDA : PBIT_OK;
   if (!rc) rc = run(d, out_index ? (uint32_t*)(d + 2 * a) : nullptr, out_keys ? d + a : nullptr);
   if (!rc && out_index && cudaMemcpyAsync(out_index, d + 2 * a, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;

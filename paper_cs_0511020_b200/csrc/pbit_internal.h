@@ -32,6 +32,8 @@ struct NvtxRange {
 void set_last_error(const char* what, const char* detail);
 void make_plan(uint64_t n, int key_bits, int K, SortPlan* p);
 int device_info(int dev, int* sms);
+// Stream-ordered workspace from the library's pool on the current device (pbit.cu).
+cudaError_t ws_alloc(void** ptr, size_t bytes, cudaStream_t st);
 int pointer_kind(const void* ptr, int dev);
 size_t sweep_tile(int key_bits);
 int rank_mode();                      // RANK_ATOMIC / RANK_BALLOT / RANK_MATCH for k_onesweep

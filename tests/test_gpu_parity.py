@@ -142,6 +142,18 @@ def test_largest_n_fails_cleanly_with_oom(pbit):
     torch.cuda.empty_cache()
 
 
+def test_workspace_pool_trim(pbit):
+    """Workspace comes from the library's own pool (not the device's default pool) and
+    pbit_workspace_trim hands it back; sorting afterwards still works."""
+    li = workloads.make_list(1 << 22, 32, seed=12, keys="uniform", device="cuda")
+    want = _oracle(li)
+    _assert_same(_gpu_sort(pbit, li), want, "before trim")
+    free0 = torch.cuda.mem_get_info()[0]
+    pbit.workspace_trim(0)
+    assert torch.cuda.mem_get_info()[0] >= free0 + (100 << 20)  # ~250 MB of workspace released
+    _assert_same(_gpu_sort(pbit, li), want, "after trim")
+
+
 def test_all_equal_keys_runs_no_pass(pbit):
     li = workloads.make_list(77777, 32, seed=6, keys="equal", device="cuda")
     h, out, ph = pbit.sort_list(li.keys, li.next, li.head, timing=True)
