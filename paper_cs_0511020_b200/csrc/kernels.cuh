@@ -615,16 +615,27 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
                "l"(gsrc) : "memory");
 }
 
+#ifndef PBIT_GATHER_UNROLL
+#define PBIT_GATHER_UNROLL 1
+#endif
+constexpr int GATHER_UNROLL = PBIT_GATHER_UNROLL;  // copy loop per segment: ~2 trips of 32 records
+
 // Fill the tile [P, P + count) of the list order straight from the walk's segment slots
 // (replaces a separate gather pass over n x 16 B).  Each warp fetches the metadata of 32
 // segments at once (one lane each), then copies the overlapping part of each with
 // cp.async (no registers, all copies in flight together).
+#ifndef PBIT_GATHER_BULK
+#define PBIT_GATHER_BULK 1
+#endif
 template <typename KeyT, int TILE>
 __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, uint32_t P, uint32_t count,
-                                            KeyT* sk, uint32_t* sv, uint32_t w, uint32_t lane) {
+                                            KeyT* sk, uint32_t* sv, uint32_t w, uint32_t lane,
+                                            unsigned long long* mbar) {
   constexpr bool WIDE = sizeof(KeyT) == 8;
   const uint32_t E = P + count;
   const uint32_t nseg = *a.nseg;
+  const uint32_t cap = a.cap;  // kernel parameters in registers: the loops below reload them otherwise
+  const unsigned char* __restrict__ slots = reinterpret_cast<const unsigned char*>(a.slots);
   // warp w takes segments first + w + SWEEP_WARPS * i: all warps share the copying
   for (uint32_t kb = a.tile_first[tile] + w;; kb += SWEEP_WARPS * 32) {
     const uint32_t k = kb + lane * SWEEP_WARPS;
@@ -642,19 +653,48 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
       const uint32_t sr = __shfl_sync(0xffffffffu, r, q);
       const uint32_t sl = __shfl_sync(0xffffffffu, len, q);
       const uint32_t lo = max(P, sp), hi = min(E, sp + sl);
+      if constexpr (!WIDE && PBIT_GATHER_BULK) {
+        // a segment starting at an even list position has its records at the same 16 B
+        // alignment in the slot and in the tile (slots and tiles start 16 B-aligned): one
+        // TMA bulk copy for its even-aligned middle, cp.async for the <= 2 edge records
+        if ((sp & 1u) == 0u && hi - lo >= 4u) {
+          const uint32_t a0 = (lo + 1u) & ~1u, a1 = hi & ~1u;
+          const uint2* src = reinterpret_cast<const uint2*>(slots) + (size_t)sr * cap;
+          uint2* dst = reinterpret_cast<uint2*>(sk);
+          if (lane == 0) {
+            const uint32_t bytes = (a1 - a0) * 8u;
+            const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+            asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+            bulk_g2s(dst + (a0 - P), src + (a0 - sp), bytes, mbar);
+          }
+          if (lane == 1 && lo < a0) cp_async8(dst + (lo - P), src + (lo - sp));
+          if (lane == 2 && a1 < hi) cp_async8(dst + (a1 - P), src + (a1 - sp));
+          continue;
+        }
+      }
+#pragma unroll (GATHER_UNROLL)
       for (uint32_t x = lo + lane; x < hi; x += 32) {
         if constexpr (WIDE) {
-          const uint4* rec = reinterpret_cast<const uint4*>(a.slots) + (size_t)sr * a.cap + (x - sp);
+          const uint4* rec = reinterpret_cast<const uint4*>(slots) + (size_t)sr * cap + (x - sp);
           cp_async8(sk + (x - P), &rec->x);
           cp_async4(sv + (x - P), &rec->z);
         } else {  // one 8 B copy of the whole record into the AoS tile (k_onesweep AOS)
-          const uint2* rec = reinterpret_cast<const uint2*>(a.slots) + (size_t)sr * a.cap + (x - sp);
+          const uint2* rec = reinterpret_cast<const uint2*>(slots) + (size_t)sr * cap + (x - sp);
           cp_async8(reinterpret_cast<uint2*>(sk) + (x - P), rec);
         }
       }
     }
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
+  if constexpr (!WIDE && PBIT_GATHER_BULK) {
+    __syncthreads();  // every expect_tx is registered before the barrier's one arrival
+    const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+    if (threadIdx.x == 0) asm volatile("mbarrier.arrive.shared.b64 _, [%0];" ::"r"(m) : "memory");
+    uint32_t done = 0;
+    while (!done)
+      asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], 0; selp.u32 %0, 1, 0, p; }"
+                   : "=r"(done) : "r"(m) : "memory");
+  }
 }
 
 // Where the first pass's tile comes from (k_onesweep SRC): TMA of keys and ids; the
@@ -702,7 +742,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   // ---- TMA bulk loads of the tile (sizes rounded up to 16 B; buffers padded to 256 B);
   // the first key pass gathers the tile from the segment slots instead
   constexpr bool GATHER = SRC == SRC_GATHER;
-  if (GATHER) gather_tile<KeyT, TILE>(a, tile, tile_base, tile_count, sm.k, sm.iin, w, lane);
+  if (GATHER) gather_tile<KeyT, TILE>(a, tile, tile_base, tile_count, sm.k, sm.iin, w, lane, &sm.mbar);
   if (!GATHER && t == 0) {
     const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
     const uint32_t ib = SRC == SRC_IOTA ? 0u : (tile_count * 4u + 15u) & ~15u;
