@@ -25,6 +25,15 @@
 
 namespace pbit {
 
+// Programmatic dependent launch (launch_pdl in launch.cuh): a kernel of the pipeline may be
+// launched while its predecessor is still finishing; it waits here for the predecessor's
+// completion and memory before touching anything, then lets its own successor launch.
+// Both are no-ops for a kernel launched without the attribute.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 constexpr int PACK_THREADS = 256;
 constexpr int WALK_THREADS = 256;
 #ifndef PBIT_WALK_FLUSH
@@ -99,6 +108,7 @@ __global__ void __launch_bounds__(PACK_THREADS)
 k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_t n, uint32_t n_ids,
        typename Rec<KB>::T* __restrict__ kn, uint32_t* __restrict__ hist, int K, int D,
        int* __restrict__ err, KeyMap km) {
+  pdl_enter();
   using KT = std::conditional_t<KB == 1, uint8_t, std::conditional_t<KB == 2, uint16_t,
              std::conditional_t<KB == 4, uint32_t, unsigned long long>>>;
   constexpr int U = 4;  // independent nodes per thread and iteration (all loads issued first)
@@ -145,6 +155,7 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
        typename Rec<KB>::T* __restrict__ slots, uint32_t cap, uint2* __restrict__ seg,
        uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t per_cta, int* __restrict__ err,
        int no_writes) {  // no_writes: timing experiments only
+  pdl_enter();
   using RT = typename Rec<KB>::T;
   // Records are staged in registers and stored in groups of WALK_FLUSH_BYTES, always as
   // whole 32 B sectors: a partial-sector store costs an HBM read-modify-write on B200.
@@ -221,6 +232,7 @@ static __global__ void k_rank_walk_a(const uint2* __restrict__ seg, RulerSel sub
                               const uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t head_ruler,
                               uint32_t nsub, unsigned long long* __restrict__ sdist, uint32_t* __restrict__ scnt,
                               uint32_t* __restrict__ ssucc, int* __restrict__ err) {
+  pdl_enter();
   if (*err) return;
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
   for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nsub; q += gridDim.x * blockDim.x) {
@@ -246,6 +258,7 @@ static __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, 
                             const uint32_t* __restrict__ s_in, unsigned long long* __restrict__ d_out,
                             uint32_t* __restrict__ c_out, uint32_t* __restrict__ s_out, uint32_t m,
                             const int* __restrict__ err) {
+  pdl_enter();
   if (*err) return;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < m; r += gridDim.x * blockDim.x) {
     const uint32_t s = s_in[r];
@@ -266,6 +279,7 @@ constexpr int RANK_SMALL = 6144;  // 2 x 6144 x 16 B = 192 KB of shared memory
 static __global__ void __launch_bounds__(1024)
 k_rank_jump_block(unsigned long long* __restrict__ d, uint32_t* __restrict__ c, uint32_t* __restrict__ s, uint32_t m,
                   int rounds, uint32_t head_sub, uint32_t n, int* __restrict__ err) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char sraw[];
   unsigned long long* sd = reinterpret_cast<unsigned long long*>(sraw);  // [2][RANK_SMALL]
   uint32_t* sc = reinterpret_cast<uint32_t*>(sd + 2 * RANK_SMALL);      // [2][RANK_SMALL]
@@ -296,6 +310,7 @@ k_rank_jump_block(unsigned long long* __restrict__ d, uint32_t* __restrict__ c, 
 // n nodes; then every node lies on it.
 static __global__ void k_rank_check(const unsigned long long* __restrict__ dist, const uint32_t* __restrict__ succ,
                              uint32_t head_sub, uint32_t n, int* __restrict__ err) {
+  pdl_enter();
   if (*err) return;
   if (succ[head_sub] != PBIT_NULL32 || dist[head_sub] != (unsigned long long)n) atomicOr(err, E_CHAIN);
 }
@@ -310,6 +325,7 @@ static __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub
                               uint32_t* __restrict__ seg_ord, uint32_t* __restrict__ seg_pos,
                               uint32_t* __restrict__ tile_first, uint32_t tile, uint32_t n,
                               uint32_t* __restrict__ nseg_out, const int* __restrict__ err) {
+  pdl_enter();
   if (*err) return;
   const uint32_t R = R_static + min(*dyn_count, dyn_cap);
   const uint32_t total = scnt[head_sub];  // segments on the chain (= R for a valid list)
@@ -348,6 +364,7 @@ k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
          const uint32_t* __restrict__ seg_ord, const uint32_t* __restrict__ nseg, uint32_t n,
          typename KeyOf<KB>::T* __restrict__ keys_lo, uint32_t* __restrict__ ids_lo,
          const Plan* __restrict__ plan, const int* __restrict__ err) {
+  pdl_enter();
   using RT = typename Rec<KB>::T;
   if (*err) return;
   if (plan->npasses != 0) return;  // the first pass gathers the segments itself
@@ -394,6 +411,7 @@ k_gather(const typename Rec<KB>::T* __restrict__ slots, uint32_t cap,
 static __global__ void __launch_bounds__(256)
 k_plan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases, Plan* __restrict__ plan,
        int D, int K, uint32_t n, const int* __restrict__ err) {
+  pdl_enter();
   __shared__ uint32_t s_warp[8];
   __shared__ uint32_t s_np;
   const int radix = 1 << K;
@@ -704,6 +722,7 @@ enum : int { SRC_TMA = 0, SRC_GATHER = 1, SRC_IOTA = 2 };
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int SRC = SRC_TMA>
 __global__ void __launch_bounds__(SWEEP_THREADS, 2)
 k_onesweep(const __grid_constant__ SweepArgs a) {
+  pdl_enter();
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
   constexpr int RADIX = S::RADIX;
   constexpr int TILE = S::TILE;
@@ -1006,6 +1025,7 @@ __global__ void __launch_bounds__(PART_THREADS, PART_CTAS_PER_SM)
 k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, uint2* __restrict__ pout,
               uint32_t n, uint32_t v_off, int shift, int bits, uint32_t* __restrict__ cursor,
               const int* __restrict__ err, int dir) {
+  pdl_enter();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
   if (*err) return;
@@ -1121,6 +1141,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
 
 static __global__ void k_relink_head(const uint32_t* __restrict__ ids, uint32_t* __restrict__ d_head,
                                      const int* __restrict__ err) {
+  pdl_enter();
   if (*err) return;
   *d_head = ids[0];
 }
@@ -1132,6 +1153,7 @@ template <bool FROM_IDS>
 __global__ void __launch_bounds__(512)
 k_relink_apply(const uint32_t* __restrict__ ids, const uint2* __restrict__ pairs, uint32_t n, uint32_t v_off,
                uint32_t* __restrict__ out_next, const int* __restrict__ err, int dir) {
+  pdl_enter();
   extern __shared__ __align__(16) uint32_t s_win[];
   if (*err) return;
   const uint32_t f0 = blockIdx.x << RELINK_FINE_SHIFT;

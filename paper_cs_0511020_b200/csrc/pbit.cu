@@ -282,7 +282,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const size_t smem = (size_t)p.D * radix * 4;
     const int blocks = full_wave(k_pack<KB>, PACK_THREADS, smem, sms, (n + PACK_THREADS - 1) / PACK_THREADS);
     const KeyMap km{p.key_kind, p.descending};
-    k_pack<KB><<<blocks, PACK_THREADS, smem, st>>>(keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
+    launch_pdl(k_pack<KB>, blocks, PACK_THREADS, smem, st, keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
@@ -305,8 +305,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t min_per = 4;
     if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
-    k_walk<KB><<<blocks, WALK_THREADS, 0, st>>>((const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap, w.seg,
-                                                w.dyn_count, p.dyn_cap, per_cta, w.err, debug_env("PBIT_DEBUG_WALK_NOWRITE"));
+    launch_pdl(k_walk<KB>, blocks, WALK_THREADS, 0, st, (const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap,
+               w.seg, w.dyn_count, p.dyn_cap, per_cta, w.err, debug_env("PBIT_DEBUG_WALK_NOWRITE"));
     ++launches;
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_WALK], st);
@@ -322,8 +322,8 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t nsub = sub.R + (hs ? 0u : 1u);
     const uint32_t head_sub = hs ? (head_ruler >> SUB_LOG2) : sub.R;
     const int sblocks = full_wave(k_rank_walk_a, 256, 0, sms, (nsub + 255) / 256);
-    k_rank_walk_a<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
-                                           w.sdist[0], w.scnt[0], w.ssucc[0], w.err);
+    launch_pdl(k_rank_walk_a, sblocks, 256, 0, st, w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
+               w.sdist[0], w.scnt[0], w.ssucc[0], w.err);
     int rounds = 1;
     while ((1ull << rounds) < nsub) ++rounds;
     rounds += 1;
@@ -333,27 +333,27 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
       once_per_device(attr, [] {
         cudaFuncSetAttribute(k_rank_jump_block, cudaFuncAttributeMaxDynamicSharedMemorySize, RANK_SMALL * 32);
       });
-      k_rank_jump_block<<<1, 1024, RANK_SMALL * 32, st>>>(w.sdist[0], w.scnt[0], w.ssucc[0], nsub, rounds, head_sub,
-                                                          n, w.err);
+      launch_pdl(k_rank_jump_block, 1, 1024, RANK_SMALL * 32, st, w.sdist[0], w.scnt[0], w.ssucc[0], nsub, rounds,
+                 head_sub, n, w.err);
       launches += 1;
     } else {
       for (int i = 0; i < rounds; ++i) {
-        k_rank_jump<<<sblocks, 256, 0, st>>>(w.sdist[cur], w.scnt[cur], w.ssucc[cur], w.sdist[cur ^ 1],
-                                             w.scnt[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
+        launch_pdl(k_rank_jump, sblocks, 256, 0, st, w.sdist[cur], w.scnt[cur], w.ssucc[cur], w.sdist[cur ^ 1],
+                   w.scnt[cur ^ 1], w.ssucc[cur ^ 1], nsub, w.err);
         cur ^= 1;
       }
-      k_rank_check<<<1, 1, 0, st>>>(w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
+      launch_pdl(k_rank_check, 1, 1, 0, st, w.sdist[cur], w.ssucc[cur], head_sub, n, w.err);
       launches += rounds + 1;
     }
-    k_rank_walk_b<<<sblocks, 256, 0, st>>>(w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
-                                           head_sub, w.sdist[cur], w.scnt[cur], w.dist, w.seg_ord, w.seg_pos,
-                                           w.tile_first, (uint32_t)sweep_tile(p.key_bits), n, w.nseg, w.err);
+    launch_pdl(k_rank_walk_b, sblocks, 256, 0, st, w.seg, sub, R_static, w.dyn_count, p.dyn_cap, head_ruler, nsub,
+               head_sub, w.sdist[cur], w.scnt[cur], w.dist, w.seg_ord, w.seg_pos, w.tile_first,
+               (uint32_t)sweep_tile(p.key_bits), n, w.nseg, w.err);
     launches += 2;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
   }
   // a3: bucket bases + pass plan; the host reads {plan, error} once here, so every pass
   // gets its digit and parity as kernel parameters and trivial digits are not launched
-  k_plan<<<1, 256, 0, st>>>(w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
+  launch_pdl(k_plan, 1, 256, 0, st, w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
   ++launches;
   HostBox* hb = host_box();
   cudaMemcpyAsync(&hb->plan, w.plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
@@ -392,7 +392,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   if (ok && !sa.debug_no_lookback) {
     NvtxRange nv("pbit.relink");
     const uint32_t* fin = w.ids[hplan.npasses & 1u];  // buffer holding the final ids
-    k_relink_head<<<1, 1, 0, st>>>(fin, w.d_head, w.err);
+    launch_pdl(k_relink_head, 1, 1, 0, st, fin, w.d_head, w.err);
     ++launches;
     launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_next, w.err, st, sms);
     if (out_prev) {  // N2: the same binned relink of the pairs (ids[p], ids[p-1])
