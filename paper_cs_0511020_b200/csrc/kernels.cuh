@@ -472,6 +472,7 @@ struct SweepSmem {
   uint32_t goff[RADIX];
   uint32_t scan[SWEEP_WARPS];
   uint32_t tile;
+  int bad;
   unsigned long long mbar;
 };
 
@@ -747,12 +748,14 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
 
   if (t == 0) {
+    sm.bad = *a.err;  // an invalid list (found after the pass was queued): no pass runs
     sm.tile = atomicAdd(a.tile_ctr + slot, 1u);
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar);
     asm volatile("mbarrier.init.shared.b64 [%0], 1;" ::"r"(m));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  if (sm.bad) return;  // uniform: every CTA read the same word (set before the pass)
   const uint32_t tile = sm.tile;
   const uint32_t tile_base = tile * (uint32_t)TILE;
   const uint32_t tile_count = min((uint32_t)TILE, n - tile_base);

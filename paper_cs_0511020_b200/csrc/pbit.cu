@@ -1,8 +1,8 @@
 // pbit.cu -- host orchestrator + C-ABI entry of the single-GPU Pbit list sort.
 //
 // pbit_sort_list (include/pbit.h) runs, on the caller's stream:
-//   k_pack -> k_walk -> k_rank_walk_a, k_rank_jump^r (or k_rank_jump_block), k_rank_walk_b
-//   -> k_plan -> [host reads the pass plan: one small D2H + sync]
+//   k_pack -> k_plan [its pass plan is copied to the host and read while the walk runs]
+//   -> k_walk -> k_rank_walk_a, k_rank_jump^r (or k_rank_jump_block), k_rank_walk_b
 //   -> k_onesweep per non-trivial digit (the first gathers from the walk's slots;
 //      k_gather only when no pass runs) -> k_relink_part per level -> k_relink_apply
 // then one small D2H of {head, error, passes} and a stream sync.  pbit_sort_array
@@ -155,6 +155,10 @@ static bool small_path_disabled() {
 
 static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 
+#ifndef PBIT_EARLY_PLAN
+#define PBIT_EARLY_PLAN 1
+#endif
+
 // ----------------------------------------------------------------------------- dispatch
 // In-warp ranking mode for the stable key passes: RANK_ATOMIC unless the load-time
 // self-test fails (or PBIT_RANK=ballot|match|atomic overrides, for experiments).
@@ -285,6 +289,21 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     launch_pdl(k_pack<KB>, blocks, PACK_THREADS, smem, st, keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
     ++launches;
   }
+#if PBIT_EARLY_PLAN
+  // a3, early: the bucket bases and the pass plan depend only on the histograms, complete
+  // after the pack.  The plan is copied to the host now and read while the walk runs, so
+  // the passes are queued behind the ranking with no host round trip in between; every
+  // later kernel checks the device error word itself (an invalid list found by the walk
+  // or the ranking stops them, and out_next stays untouched).
+  launch_pdl(k_plan, 1, 256, 0, st, w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
+  ++launches;
+  HostBox* hb = host_box();
+  cudaMemcpyAsync(&hb->plan, w.plan, sizeof(Plan), cudaMemcpyDeviceToHost, st);
+  static thread_local cudaEvent_t plan_ev[64] = {};
+  cudaEvent_t& pev = plan_ev[cur_dev & 63];
+  if (!pev) cudaEventCreateWithFlags(&pev, cudaEventDisableTiming);
+  cudaEventRecord(pev, st);
+#endif
   if (timing) cudaEventRecord(ev[PBIT_PHASE_PACK], st);
 
   // a1: walk
@@ -351,8 +370,12 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     launches += 2;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
   }
-  // a3: bucket bases + pass plan; the host reads {plan, error} once here, so every pass
-  // gets its digit and parity as kernel parameters and trivial digits are not launched
+  // the host reads the pass plan once, so every pass gets its digit and parity as kernel
+  // parameters and trivial digits are not launched
+#if PBIT_EARLY_PLAN
+  const bool ok = cudaEventSynchronize(pev) == cudaSuccess;  // long complete: the walk ran since
+  const Plan hplan = hb->plan;
+#else
   launch_pdl(k_plan, 1, 256, 0, st, w.hist, w.bases, w.plan, p.D, p.K, n, w.err);
   ++launches;
   HostBox* hb = host_box();
@@ -361,6 +384,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   int herr = cudaStreamSynchronize(st) != cudaSuccess ? -1 : hb->err;
   const Plan hplan = hb->plan;
   const bool ok = herr == 0;
+#endif
   if (ok && hplan.npasses == 0) {  // a1: gather to list order -- only when no pass can fuse it
     const uint32_t Rmax = R_static + p.dyn_cap;
     const int gblocks = full_wave(k_gather<KB>, 256, 0, sms, (Rmax + 8 * GATHER_SEGS - 1) / (8 * GATHER_SEGS));
