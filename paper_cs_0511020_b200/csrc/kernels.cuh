@@ -56,7 +56,10 @@ constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
 #define PBIT_WCNT32 0
 #endif
 constexpr int SWEEP_IPT32 = PBIT_SWEEP_IPT;                       // items per thread, keys <= 32 bits
-constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT == 16 ? 12 : PBIT_SWEEP_IPT * 3 / 4 + 1;  // 64-bit keys
+#ifndef PBIT_SWEEP_IPT64
+#define PBIT_SWEEP_IPT64 (PBIT_SWEEP_IPT == 16 ? 12 : PBIT_SWEEP_IPT * 3 / 4 + 1)
+#endif
+constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 // per-warp digit counters of the pass ranking: u32 (one word per digit: no two digits
 // share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
 using WCnt = std::conditional_t<PBIT_WCNT32 != 0, uint32_t, uint16_t>;
