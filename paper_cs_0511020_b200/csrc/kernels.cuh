@@ -452,15 +452,17 @@ k_plan(const uint32_t* __restrict__ hist, uint32_t* __restrict__ bases, Plan* __
 }
 
 // ============================================================================ a3/a4: onesweep
-// One stable counting-sort pass on digit plan->digit[slot] (single-pass scan with
-// decoupled lookback, Merrill & Garland).  Tile = 256 threads x IPT items, taken in
-// launch order from an atomic ticket so every predecessor tile is running or done.
+// One stable counting-sort pass on digit a.digit (single-pass scan with decoupled
+// lookback, Merrill & Garland).  Tile = SWEEP_THREADS (512) threads x IPT items, taken
+// in launch order from an atomic ticket so every predecessor tile is running or done.
 //
-//  1. TMA bulk copy (cp.async.bulk + mbarrier) of the tile's keys and ids into smem.
-//  2. Stable in-warp ranking: a warp ranks 32 consecutive items at a time, in input
-//     order; equal digits are grouped by K ballots (or match.any), the group leader
-//     bumps the warp's u16 counter for that digit (distinct digits per instruction,
-//     private row per warp: no atomics needed).
+//  1. TMA bulk copy (cp.async.bulk + mbarrier) of the tile's keys and ids into smem
+//     (pass 0 of the list sort: gathered from the walk's segment slots, gather_tile).
+//  2. Stable in-warp ranking (rank_items): a warp ranks 32 consecutive items at a time,
+//     in input order, on its private u16 digit counters -- one lane-ordered shared
+//     atomic per item (RANK_ATOMIC; lanes sharing lane 0's digit take one atomic on
+//     skewed middle passes), or peer masks from ballots / match.any with the group
+//     leader bumping the counter (RANK_BALLOT / RANK_MATCH).
 //  3. Per-digit warp offsets + tile totals; the aggregate is published at once.
 //  4. Stage the tile in smem in (digit, input order) order.
 //  5. Decoupled lookback, one thread per digit value.
