@@ -7,9 +7,12 @@
 //   2  count-walk own rulers                 ncclAllGather(segment table), ncclAllReduce(error)
 //   3  rank the ruler list (every rank, redundantly; validates the list)
 //   4  emit-walk the segments covering own positions [r*S, r*S+S) -> list-order chunk
-//   5  one stable pass on the top non-trivial digit; position-exact destinations
-//      (bucket b's elements from rank r occupy global ranks start(r,b) ..)  ncclSend/Recv
-//   6  full local sort of the received chunk (stable LSD, all non-trivial digits)
+//   0  the ranks agree on their arguments (one all-reduce; pbit.h)
+//   5  stable local sort of the chunk by the full key; exact splitters of the global
+//      (key, list position) order at ranks (s+1)*S by radix refinement (ncclAllReduce
+//      of candidate counts per digit); the host planner splits ties in rank order;
+//      the sorted ranges are exchanged                                   ncclSend/Recv
+//   6  full local sort of the received runs (stable LSD, all non-trivial digits)
 //   7  stitch (ncclAllGather of first ids) and route (v, succ) to the owner of v
 //                                           ncclSend/Recv; local windowed relink
 // Received streams are concatenated in source-rank order: elements with equal keys from
