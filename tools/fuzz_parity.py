@@ -3,7 +3,7 @@ compared bit-exactly with the oracle -- list sort (out_next, and out_prev on som
 array sort, every key kind and direction, digit widths 1..16, sizes 1 .. ~3M covering the
 single-cluster path and every size class of the general path.
 
-    python tools/fuzz_parity.py [seconds] [seed]
+    python tools/fuzz_parity.py [seconds] [seed] [max_n]
 """
 import os
 import sys
@@ -21,12 +21,13 @@ import workloads  # noqa: E402
 
 budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 2026)
+max_n = int(sys.argv[3]) if len(sys.argv) > 3 else 3_000_000
 KEYS = ["uniform", "zipf", "equal", "max", "sorted", "reverse", "runs4096"]
 LINKS = ["random", "identity", "push"]
 t0, cases, fails = time.time(), 0, 0
 while time.time() - t0 < budget:
     n = int(rng.choice([1, 2, 3, 31, 257, 4095, 65536, 65537]) if rng.random() < 0.3
-            else int(np.exp(rng.uniform(np.log(2), np.log(3_000_000)))))
+            else int(np.exp(rng.uniform(np.log(2), np.log(max_n)))))
     kb = int(rng.choice([8, 16, 32, 64]))
     keys = str(rng.choice(KEYS))
     links = str(rng.choice(LINKS))
