@@ -28,6 +28,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# The library returns its workspace to the device after every call by default (pbit.h);
+# a caller that sorts repeatedly keeps it mapped with PBIT_POOL_KEEP_GB (opt-in, stated
+# in the JSON line's config).  Set before libpbit.so creates its pool.
+os.environ.setdefault("PBIT_POOL_KEEP_GB", "96")
 
 METRIC = "sorted list nodes/sec at 1/2/4/8 B200; achieved HBM GB/s vs peak"
 UNIT = "nodes/s"
@@ -142,7 +146,8 @@ def bench_config(cfg: str, n: int, K: int, ws: int = 1) -> dict:
     return {"workload": cfg, "desc": c["desc"], "n_per_gpu": n, "key_bits": kb, "digit_bits": K,
             "parallelism": "single GPU" if ws == 1 else f"one list, node ids sharded over {ws} ranks, "
                                                          "key-range exchange (NCCL)",
-            "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6 else "inputs smaller than L2"}
+            "l2": "inputs larger than L2 (no flush needed)" if n * (kb // 8 + 4) > 126e6 else "inputs smaller than L2",
+            "workspace_pool_keep_gb": float(os.environ.get("PBIT_POOL_KEEP_GB", "0"))}
 
 
 def cpu_baseline(cfg: str, sample_n: int, reps: int = 1):

@@ -23,9 +23,11 @@
  * output.  pbit_opts.key_kind / .descending select signed or floating-point keys
  * and the descending order, also stable.
  *
- * Ownership.  The caller owns every array.  The library allocates stream-ordered
- * workspace (cudaMallocAsync on the call's stream; memory returns to the device
- * pool when the call ends) and never keeps pointers after returning.
+ * Ownership.  The caller owns every array.  The library takes stream-ordered workspace
+ * from its own memory pool on the current device (cudaMallocFromPoolAsync on the call's
+ * stream) and frees it before returning; by default the pool then hands the memory back
+ * to the device (release threshold 0; PBIT_POOL_KEEP_GB=x keeps up to x GB mapped between
+ * calls, see pbit_workspace_trim).  It never keeps pointers to caller arrays.
  *
  * Synchronisation.  Every call is synchronous: it returns after the work on
  * opts->stream has finished (out_head and the status are host values).  Calls on
@@ -34,8 +36,8 @@
  * Errors.  Functions return a pbit_status and never throw or abort.
  *   PBIT_ERR_INVALID_ARG  null pointer; key_bits not in {8,16,32,64}; digit_bits out
  *                         of range; key_kind not 0/1/2 or float keys of 8 bits;
- *                         head >= n (n > 0); n > 2^32-1; pointers that mix host and
- *                         device memory.
+ *                         head >= n (n > 0); n > 2^32-2 (PBIT_NULL is not a node id);
+ *                         pointers that mix host and device memory.
  *   PBIT_ERR_INVALID_LIST the input is not one NULL-terminated chain of exactly n
  *                         nodes starting at head (cycle, short chain, index >= n,
  *                         a node reached twice).  out_next is NOT modified (the check
@@ -85,7 +87,8 @@ typedef struct {
                         wider pattern is sorted as stable 8-bit sub-passes,
                         so K = 9..16 runs the passes of K = 8.                       */
     void *stream;    /* cudaStream_t for every launch; NULL = legacy default stream */
-    int validate;    /* reserved: validation always runs (it is fused into ranking) */
+    int validate;    /* ignored: validation always runs (it is fused into the ranking
+                        and costs one scalar check), whatever this field holds       */
     float *phase_ms; /* optional host array of PBIT_NUM_PHASES floats: device ms per
                         phase, filled after the call (adds CUDA events); else NULL  */
     uint32_t *passes_run; /* optional host out: number of radix passes executed (the
@@ -119,7 +122,7 @@ enum { PBIT_KEY_UNSIGNED = 0, PBIT_KEY_SIGNED = 1, PBIT_KEY_FLOAT = 2 };
  *   keys      [in]  n keys, key_bits/8 bytes each, node-indexed (u8/u16/u32/u64).
  *   next      [in]  n successor ids (u32), PBIT_NULL terminates.
  *   head      [in]  first node id (PBIT_NULL iff n == 0).
- *   n         [in]  number of nodes, 0 <= n <= 2^32-1.
+ *   n         [in]  number of nodes, 0 <= n <= 2^32-2.
  *   key_bits  [in]  M in {8, 16, 32, 64}.
  *   out_head  [out] HOST pointer: head of the sorted list.
  *   out_next  [out] n successor ids of the sorted list.  May alias `next`
@@ -177,7 +180,8 @@ int pbit_sort_array(const void *keys, uint64_t n, int key_bits, uint32_t *out_in
  * out_head returns PBIT_ERR_INVALID_ARG on that rank alone (the others then time out in
  * the agreement with PBIT_ERR_NCCL after PBIT_MG_TIMEOUT_S).
  * Rank r returns the successors of its own nodes; the sorted positions it computed
- * internally are [r*S, r*S + S) (top-digit sharding, position-exact).
+ * internally are [r*S, r*S + S) (key-range sharding: exact splitters of the global
+ * (key, list position) order, so the shards are equal in size even under heavy duplicates).
  */
 int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32_t head,
                       uint64_t n_global, uint64_t node_lo, uint64_t n_local, int key_bits,
@@ -212,11 +216,19 @@ void pbit_mg_exchange_plan(int nranks, int rank, uint64_t n, uint64_t slice, con
 
 /* Workspace.  Every call takes its workspace (about 60 B per node for 32-bit keys) from
  * the library's own stream-ordered memory pool on the current device and returns it at
- * the end of the call; the pool keeps up to half the device memory (PBIT_POOL_KEEP_GB
- * overrides) mapped between calls, so repeated calls do not re-map memory.
+ * the end of the call; the pool releases it to the device when the call's stream
+ * synchronizes (release threshold 0) unless PBIT_POOL_KEEP_GB=x asks it to keep up to x GB
+ * mapped between calls (repeated calls then skip the re-mapping).
  * pbit_workspace_trim synchronizes the current device and releases cached workspace
  * above keep_bytes (0 = all of it).  Returns PBIT_OK or PBIT_ERR_CUDA. */
 int pbit_workspace_trim(uint64_t keep_bytes);
+
+/* In-warp ranking of the radix passes on the current device, decided by a self-test of
+ * the lane order of conflicting shared-memory atomics that runs once per device before
+ * its first sort (the order is measured on sm_100a, not documented): 2 = lane-ordered
+ * atomics (the default), 0 = ballot peer masks (the fallback if the test ever fails),
+ * 1 = match.any; PBIT_RANK overrides.  -1 on a CUDA error. */
+int pbit_rank_mode(void);
 
 /* Text of the last CUDA or NCCL error seen by the calling host thread ("" if none). */
 const char *pbit_last_error(void);

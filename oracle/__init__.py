@@ -12,6 +12,7 @@ from .oracle import (  # noqa: F401
     OracleError,
     bits,
     build,
+    list_order,
     memory_bound_T,
     pbit_sort,
     repair_back,

@@ -70,6 +70,8 @@ def _load():
                                               ctypes.c_uint64, ctypes.c_uint, ctypes.c_void_p]
             lib.oracle_validate_list.restype = ctypes.c_int
             lib.oracle_validate_list.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_list_order.restype = ctypes.c_int
+            lib.oracle_list_order.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
             lib.oracle_bits.restype = ctypes.c_uint64
             lib.oracle_bits.argtypes = [ctypes.c_uint64, ctypes.c_uint, ctypes.c_uint]
             lib.oracle_memory_bound_T.restype = ctypes.c_uint64
@@ -150,6 +152,17 @@ def validate_list(next_, head: int) -> bool:
     nxt = np.ascontiguousarray(next_, dtype=np.uint32)
     return _load().oracle_validate_list(nxt.ctypes.data if nxt.size else None, head & 0xFFFFFFFF,
                                         nxt.shape[0]) == 0
+
+
+def list_order(next_, head: int):
+    """order[i] = the i-th node of the list (head, next_): the traversal L = L->next."""
+    nxt = np.ascontiguousarray(next_, dtype=np.uint32)
+    order = np.empty(max(nxt.shape[0], 1), np.uint32)
+    rc = _load().oracle_list_order(nxt.ctypes.data if nxt.size else None, head & 0xFFFFFFFF, nxt.shape[0],
+                                   order.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return order[:nxt.shape[0]]
 
 
 def bits(number: int, M: int, K: int = 4) -> int:

@@ -142,6 +142,18 @@ int oracle_validate_list(const uint32_t *next, uint32_t head, uint64_t n) {
     return steps == n ? ORACLE_OK : ORACLE_ERR_LIST;
 }
 
+/* The list order: order[i] = v_i with v_0 = head, v_{i+1} = next[v_i] -- the traversal
+ * `L = L->next` of the split loop down to the NULL of the last node (P:8).  Used
+ * by the checkers to read a sorted list (e.g. the payload sequence of C4, reading Q11).
+ * The list must be valid (oracle_validate_list), else ORACLE_ERR_LIST. */
+int oracle_list_order(const uint32_t *next, uint32_t head, uint64_t n, uint32_t *order) {
+    int rc = oracle_validate_list(next, head, n);
+    if (rc) return rc;
+    uint32_t v = head;
+    for (uint64_t i = 0; i < n; ++i) { order[i] = v; v = next[v]; }
+    return ORACLE_OK;
+}
+
 /* Sort the list (head, next[]) of n nodes by its M = key_bits unsigned keys with
  * pattern length K; the result goes to (*out_head, out_next[]).  out_next may
  * alias next.  Unsigned entry of the dispatcher P:444-466 (lines 14-15):

@@ -22,7 +22,7 @@ NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
 SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_sort_array", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
            "pbit_mg_comm_destroy", "pbit_mg_comm_abort", "pbit_status_string", "pbit_version", "pbit_last_error",
-           "pbit_mg_slice", "pbit_mg_exchange_plan", "pbit_workspace_trim"]
+           "pbit_mg_slice", "pbit_mg_exchange_plan", "pbit_workspace_trim", "pbit_rank_mode"]
 
 STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
           4: "PBIT_ERR_CUDA", 5: "PBIT_ERR_NCCL", 6: "PBIT_ERR_UNSUPPORTED"}
@@ -72,6 +72,8 @@ def _load():
     lib.pbit_status_string.argtypes = [ctypes.c_int]
     lib.pbit_version.restype = ctypes.c_uint32
     lib.pbit_last_error.restype = ctypes.c_char_p
+    lib.pbit_rank_mode.restype = ctypes.c_int
+    lib.pbit_rank_mode.argtypes = []
     lib.pbit_workspace_trim.restype = ctypes.c_int
     lib.pbit_workspace_trim.argtypes = [ctypes.c_uint64]
     lib.pbit_mg_slice.restype = ctypes.c_uint64
@@ -88,6 +90,32 @@ lib = _load()
 _KEY_BITS = {torch.uint8: 8, torch.int8: 8, torch.int16: 16, torch.uint16: 16, torch.int32: 32,
              torch.uint32: 32, torch.int64: 64, torch.uint64: 64, torch.float16: 16, torch.bfloat16: 16,
              torch.float32: 32, torch.float64: 64}
+
+
+_FLOAT_DTYPES = (torch.float16, torch.bfloat16, torch.float32, torch.float64)
+
+
+def _key_kind(keys, key_kind):
+    """key_kind=None: "float" for floating-point tensors / arrays, else "unsigned" (integer
+    tensors are read as raw unsigned bit patterns: torch's signed dtypes are the usual
+    holders of u16/u32/u64 keys -- pass key_kind="signed" for two's complement order).
+    An integer order asked for floating-point keys raises instead of sorting raw bits."""
+    dt = getattr(keys, "dtype", None)
+    is_float = dt in _FLOAT_DTYPES if isinstance(dt, torch.dtype) else getattr(dt, "kind", "") == "f"
+    if key_kind is None:
+        return "float" if is_float else "unsigned"
+    if key_kind not in KEY_KINDS:
+        raise ValueError(f"key_kind must be one of {sorted(KEY_KINDS)}")
+    if is_float and key_kind != "float":
+        raise ValueError(f"key_kind={key_kind!r} for floating-point keys ({dt}): pass key_kind='float' "
+                         "or a view of the bits as an integer dtype")
+    return key_kind
+
+
+def rank_mode() -> int:
+    """The in-warp ranking the radix passes use on the current device (pbit.h
+    pbit_rank_mode): 2 lane-ordered atomics, 0 ballots (self-test fallback)."""
+    return int(lib.pbit_rank_mode())
 
 
 def _errtext(rc: int) -> str:
@@ -126,7 +154,7 @@ def _stream_handle(stream, on_cuda: bool):
 
 
 def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: int = 0, out_next=None,
-              stream=None, timing: bool = False, key_kind: str = "unsigned", descending: bool = False,
+              stream=None, timing: bool = False, key_kind: str | None = None, descending: bool = False,
               out_prev=None):
     """Stable sort of the list (head, next_) by keys; returns (head, out_next) (plus a
     dict of device ms per phase when timing=True).
@@ -134,11 +162,13 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
     keys / next_ / out_next: CUDA tensors on the current device, or host arrays (torch
     CPU tensors or numpy) -- then the library stages them through device memory.
     next_ holds u32 ids (int32 view, NULL = -1 / 0xFFFFFFFF).  key_kind: "unsigned",
-    "signed" or "float" (how the key bits order, pbit.h PBIT_KEY_*); descending: order.
+    "signed" or "float" (how the key bits order, pbit.h PBIT_KEY_*; None: inferred, see
+    _key_kind); descending: order.
     out_prev (same kind as out_next): also filled with the predecessors of the sorted list
     (doubly-linked lists, pbit.h pbit_opts.out_prev)."""
     if key_bits is None:
         key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
+    key_kind = _key_kind(keys, key_kind)
     n = int(next_.shape[0])
     on_cuda = isinstance(next_, torch.Tensor) and next_.is_cuda
     if out_next is None:
@@ -168,7 +198,7 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
 
 
 def sort_array(keys, key_bits: int | None = None, digit_bits: int = 0, out_index=None, out_keys=None,
-               want_index: bool = True, want_keys: bool = False, key_kind: str = "unsigned",
+               want_index: bool = True, want_keys: bool = False, key_kind: str | None = None,
                descending: bool = False, stream=None, timing: bool = False):
     """Stable sort of an ARRAY of keys (pbit.h pbit_sort_array, the paper's "table",
     P:1118-1177).  Returns (out_index, out_keys) -- either may be None -- plus a dict of
@@ -176,6 +206,7 @@ def sort_array(keys, key_bits: int | None = None, digit_bits: int = 0, out_index
     arrays (torch CPU tensors or numpy)."""
     if key_bits is None:
         key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
+    key_kind = _key_kind(keys, key_kind)
     n = int(keys.shape[0])
     on_cuda = isinstance(keys, torch.Tensor) and keys.is_cuda
     if want_index and out_index is None:
@@ -264,11 +295,12 @@ def mg_exchange_plan(nranks: int, rank: int, n: int, slice_: int, lt, le):
 
 def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int, comm: int,
                  key_bits: int | None = None, digit_bits: int = 0, out_next_local=None, stream=None,
-                 key_kind: str = "unsigned", descending: bool = False, out_prev_local=None):
+                 key_kind: str | None = None, descending: bool = False, out_prev_local=None):
     """Sort one list sharded over the ranks of `comm` (see include/pbit.h).  Returns
     (head, out_next_local)."""
     if key_bits is None:
         key_bits = _KEY_BITS[keys_local.dtype]
+    key_kind = _key_kind(keys_local, key_kind)
     n_local = int(next_local.shape[0])
     if out_next_local is None:
         out_next_local = torch.empty_like(next_local)

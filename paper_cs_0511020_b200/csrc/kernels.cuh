@@ -351,9 +351,11 @@ static __global__ void k_rank_walk_b(const uint2* __restrict__ seg, RulerSel sub
       const uint2 x = seg[r];
       const uint32_t pos = n - D;  // list position of the segment's first node
       seg_pos[k] = pos;
-      // segments are shorter than a pass tile, so each holds at most one tile start
-      const uint32_t tb = (pos + tile - 1) / tile;
-      if (tb * tile < pos + x.x) tile_first[tb] = k;
+      // every tile (or, in the multi-GPU path, rank chunk) whose first position lies in
+      // this segment starts at it (single GPU: segments are shorter than a tile, so at
+      // most one; multi-GPU segments are not cut and may span several chunks)
+      for (uint32_t tb = (pos + tile - 1) / tile; (unsigned long long)tb * tile < (unsigned long long)pos + x.x; ++tb)
+        tile_first[tb] = k;
       seg_ord[k++] = r;
       D -= x.x;
       if (x.y == PBIT_NULL32 || sub.is_ruler(x.y)) break;

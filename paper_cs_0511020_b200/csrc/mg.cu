@@ -126,9 +126,19 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
   SortPlan p;
   make_plan(n, KB * 8, K, &p);
+  // a rank's id slice must be a whole number of ruler blocks: S is a multiple of 64
+  // (pbit_mg_slice), so the spacing is at most 64 here (make_plan picks 128 from 2^30)
+  if (p.s_log2 > 6) {
+    p.s_log2 = 6;
+    p.R = (uint32_t)(((uint64_t)n + 63) >> 6);
+  }
   const int radix = 1 << K;
   const uint32_t s = 1u << p.s_log2;
   const uint32_t bpr = S / s;                      // ruler blocks per rank
+  if ((uint64_t)G * bpr * s < (uint64_t)n || S % s) {
+    set_last_error("pbit_sort_list_mg", "ruler blocks do not tile the rank slices");
+    return PBIT_ERR_UNSUPPORTED;
+  }
   const uint32_t Gs = (uint32_t)G * bpr;           // segment-table entries (+1: head ruler)
   RulerSel sel{n, (uint32_t)p.s_log2, p.R};
   const bool head_is_ruler = sel.is_ruler(head);
@@ -170,7 +180,6 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     dist = b.take<uint32_t>(Rmax);
     seg_ord = b.take<uint32_t>(Rmax);
     seg_pos = b.take<uint32_t>(Rmax);
-    part_first = b.take<uint32_t>(G + 2);
     tile_first_unused = b.take<uint32_t>(1);
     for (int i = 0; i < 2; ++i) {
       sdist[i] = b.take<unsigned long long>(nsub + 1);
@@ -183,6 +192,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     status = b.take<unsigned long long>(ntiles * 256);
     send_p = b.take<uint2>(S);
     ctl_off = b.off;
+    part_first = b.take<uint32_t>(G + 2);  // zeroed with the control block
     hist_l = b.take<uint32_t>((size_t)D * radix);
     hist_g = b.take<uint32_t>((size_t)D * radix);
     hist_a = b.take<uint32_t>((size_t)D * radix);

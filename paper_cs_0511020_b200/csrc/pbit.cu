@@ -64,9 +64,8 @@ void set_last_error(const char* what, const char* detail) {
 
 // ----------------------------------------------------------------------------- device info
 // Per device: SM count, and the library's own stream-ordered memory pool for workspace.
-// The pool keeps freed workspace mapped between calls up to a release threshold (half the
-// device memory by default, PBIT_POOL_KEEP_GB overrides), so repeated calls do not re-map
-// memory; the device's default pool, which other code may use, is left alone.
+// The pool's release threshold is 0 by default (PBIT_POOL_KEEP_GB=x keeps x GB mapped
+// between calls); the device's default pool, which other code may use, is left alone.
 // pbit_workspace_trim() hands cached workspace back.
 struct DevInfo {
   int sms = 0;
@@ -92,10 +91,11 @@ int device_info(int dev, int* sms) {
       cudaGetLastError();
       return PBIT_ERR_CUDA;
     }
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) { cudaGetLastError(); total_b = 0; }
+    // default 0: workspace goes back to the device when a call ends (the paper's sort
+    // needs O(1) memory; this one O(n) only while it runs).  PBIT_POOL_KEEP_GB=x
+    // keeps up to x GB mapped between calls (repeated calls then skip the re-mapping)
     const char* e = getenv("PBIT_POOL_KEEP_GB");
-    uint64_t keep = e ? (uint64_t)(atof(e) * 1e9) : (uint64_t)total_b / 2;
+    uint64_t keep = e ? (uint64_t)(atof(e) * 1e9) : 0ull;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
     d.pool = pool;
   }
@@ -160,14 +160,25 @@ static inline size_t align_up(size_t x) { return (x + 255) & ~(size_t)255; }
 #endif
 
 // ----------------------------------------------------------------------------- dispatch
-// In-warp ranking mode for the stable key passes: RANK_ATOMIC unless the load-time
-// self-test fails (or PBIT_RANK=ballot|match|atomic overrides, for experiments).
-static std::atomic<int> g_rank_mode{-1};
+// In-warp ranking mode for the stable key passes, per device: RANK_ATOMIC unless that
+// device's self-test fails (or PBIT_RANK=ballot|match|atomic overrides, for experiments).
+// The lane order of conflicting shared atomics is measured, not documented, so it is
+// checked on every device before its first sort (pbit_rank_mode() reports the verdict).
+static std::atomic<int> g_rank_mode[64];
+static std::once_flag g_rank_init;
 
-int rank_mode() { return g_rank_mode.load(std::memory_order_relaxed); }
+static int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); dev = 0; }
+  return dev & 63;
+}
+
+int rank_mode() { return g_rank_mode[current_device()].load(std::memory_order_relaxed); }
 
 void init_rank_mode(cudaStream_t st) {
-  if (g_rank_mode.load() >= 0) return;
+  std::call_once(g_rank_init, [] { for (auto& m : g_rank_mode) m.store(-1); });
+  std::atomic<int>& slot = g_rank_mode[current_device()];
+  if (slot.load() >= 0) return;
   int mode = RANK_ATOMIC;
   if (const char* e = getenv("PBIT_RANK")) {
     mode = !strcmp(e, "ballot") ? RANK_BALLOT : !strcmp(e, "match") ? RANK_MATCH : RANK_ATOMIC;
@@ -184,7 +195,7 @@ void init_rank_mode(cudaStream_t st) {
     cudaGetLastError();
     if (bad) mode = RANK_BALLOT;
   }
-  g_rank_mode.store(mode);
+  slot.store(mode);
 }
 
 size_t sweep_tile(int key_bits) { return (size_t)SWEEP_THREADS * (key_bits == 64 ? SWEEP_IPT64 : SWEEP_IPT32); }
@@ -680,6 +691,15 @@ const char* pbit_status_string(int s) {
     case PBIT_ERR_UNSUPPORTED: return "unsupported";
     default: return "unknown status";
   }
+}
+
+int pbit_rank_mode(void) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return -1; }
+  int sms = 0;
+  if (device_info(dev, &sms) != PBIT_OK) return -1;
+  init_rank_mode((cudaStream_t)0);
+  return rank_mode();
 }
 
 int pbit_workspace_trim(uint64_t keep_bytes) {

@@ -86,3 +86,28 @@ def test_no_oracle_in_product_path():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"(^\s*(import|from)\s+oracle)|(#include\s*[<\"].*oracle)|liboracle|pbit_oracle",
                                      src, flags=re.M), f
+
+
+def test_key_kind_inferred_from_dtype(pbit):
+    """float keys without key_kind sort as floats; an integer order for float
+    keys raises instead of sorting raw bit patterns."""
+    import torch
+    assert pbit._key_kind(torch.zeros(2, dtype=torch.float32), None) == "float"
+    assert pbit._key_kind(torch.zeros(2, dtype=torch.bfloat16), None) == "float"
+    assert pbit._key_kind(np.zeros(2, np.float64), None) == "float"
+    assert pbit._key_kind(torch.zeros(2, dtype=torch.int32), None) == "unsigned"
+    assert pbit._key_kind(torch.zeros(2, dtype=torch.int32), "signed") == "signed"
+    with pytest.raises(ValueError):
+        pbit._key_kind(torch.zeros(2, dtype=torch.float32), "unsigned")
+    with pytest.raises(ValueError):
+        pbit._key_kind(torch.zeros(2, dtype=torch.int32), "bogus")
+
+
+def test_header_limits_match_the_checks(pbit):
+    """n <= 2^32-2: the header states the limit the library enforces."""
+    src = open(HEADER).read()
+    assert "2^32-1" not in src
+    lib = pbit.lib
+    oh = ctypes.c_uint32(7)
+    p = np.zeros(4, np.uint32).ctypes.data
+    assert lib.pbit_sort_list(p, p, 0, 0xFFFFFFFF, 32, ctypes.byref(oh), p, None) == 1

@@ -444,3 +444,17 @@ def test_order_key_checker_matches_python_sort():
         t = torch.from_numpy(vals.copy())
         assert list(np.argsort(order_key(t, bits, "signed").numpy(), kind="stable")) == \
             sorted(range(len(vals)), key=lambda i: int(vals[i]))
+
+
+@pytest.mark.parametrize("links", ["random", "identity", "push"])
+def test_list_order_is_the_generators_order(links):
+    # pinned to workloads' own construction of the list (next[order[p]] = order[p+1])
+    li = workloads.make_list(5003, 32, seed=11, links=links)
+    got = oracle.list_order(workloads.next_numpy(li), li.head)
+    assert np.array_equal(got.astype(np.int64), li.order.numpy())
+
+
+def test_list_order_rejects_invalid():
+    with pytest.raises(oracle.OracleError):
+        oracle.list_order(np.array([1, 0], np.uint32), 0)   # cycle
+    assert oracle.list_order(np.zeros(0, np.uint32), oracle.ORACLE_NULL).shape == (0,)

@@ -54,3 +54,28 @@ def test_runs4096_reading_q12():
     assert (np.diff(k[:4096].astype(np.float64)) >= 0).all()         # P-run ascending
     assert not (np.diff(k[4096:8192].astype(np.float64)) >= 0).all()  # R-run random
     assert li.payload is not None and li.payload.shape[0] == li.n
+
+
+def test_u64_kinds_use_every_bit():
+    # the u64 sorted / runs keys had bit 32 forced to 0
+    for kind in ("runs4096", "sorted", "reverse", "uniform"):
+        k = workloads.keys_numpy(workloads.make_list(1 << 14, 64, 5, keys=kind))
+        for bit in (0, 31, 32, 33, 63):
+            frac = float(((k >> np.uint64(bit)) & np.uint64(1)).mean())
+            assert 0.4 < frac < 0.6, (kind, bit, frac)
+
+
+def test_u64_runs_sorted_by_full_key():
+    li = workloads.make_list(4096 * 3, 64, seed=8, keys="runs4096")
+    k = workloads.keys_numpy(li)[li.order.numpy()]
+    assert np.all(k[1:4096] >= k[:4095]) and np.all(k[8193:12288] >= k[8192:12287])
+
+
+@pytest.mark.parametrize("kind,bits", [("runs4096", 64), ("zipf", 32), ("uniform", 8)])
+def test_chunking_does_not_change_values(kind, bits, monkeypatch):
+    ref = workloads.make_list(50001 if kind != "runs4096" else 4096 * 13 + 5, bits, 9, keys=kind)
+    monkeypatch.setattr(workloads, "CHUNK", 4096 * 3)
+    got = workloads.make_list(ref.n, bits, 9, keys=kind)
+    assert torch.equal(ref.keys, got.keys) and torch.equal(ref.next, got.next) and ref.head == got.head
+    if ref.payload is not None:
+        assert torch.equal(ref.payload, got.payload)

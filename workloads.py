@@ -71,19 +71,36 @@ def _bijection_bits(x: torch.Tensor, bits: int, seed: int) -> torch.Tensor:
     return x
 
 
-def permutation(n: int, seed: int, device="cpu") -> torch.Tensor:
-    """A seeded pseudo-random permutation of [0, n) (int64), by cycle-walking a keyed
-    bijection on the enclosing power of two.  Same result on every device."""
-    if n == 0:
-        return torch.zeros(0, dtype=torch.int64, device=device)
-    bits = max(1, math.ceil(math.log2(n))) if n > 1 else 1
-    x = torch.arange(n, dtype=torch.int64, device=device)
+CHUNK = 1 << 24  # elements per generator chunk: every draw is per element (or per 4096-run), so
+#                 chunking bounds the temporaries without changing a single value
+
+
+def _perm_values(x: torch.Tensor, n: int, bits: int, seed: int) -> torch.Tensor:
     y = _bijection_bits(x, bits, seed)
     bad = y >= n
     while bool(bad.any()):
         y[bad] = _bijection_bits(y[bad], bits, seed)
         bad = y >= n
     return y
+
+
+def _perm_bits(n: int) -> int:
+    return max(1, math.ceil(math.log2(n))) if n > 1 else 1
+
+
+def permutation_range(a: int, b: int, n: int, seed: int, device="cpu") -> torch.Tensor:
+    """Entries [a, b) of permutation(n, seed) (int64), computed on their own."""
+    return _perm_values(torch.arange(a, b, dtype=torch.int64, device=device), n, _perm_bits(n), seed)
+
+
+def permutation(n: int, seed: int, device="cpu") -> torch.Tensor:
+    """A seeded pseudo-random permutation of [0, n) (int64), by cycle-walking a keyed
+    bijection on the enclosing power of two.  Same result on every device."""
+    out = torch.empty(n, dtype=torch.int64, device=device)
+    for a in range(0, n, CHUNK):
+        b = min(n, a + CHUNK)
+        out[a:b] = permutation_range(a, b, n, seed, device)
+    return out
 
 
 def uniform_u32(n: int, seed: int, stream: int, device="cpu") -> torch.Tensor:
@@ -159,19 +176,23 @@ def zipf_thresholds(num_values: int, s: float) -> np.ndarray:
     return thr
 
 
-def make_list(n: int, key_bits: int, seed: int, keys: str = "uniform", links: str = "random",
-              device="cpu", key_range: int | None = None, zipf_s: float = 1.1,
-              zipf_values: int = 1 << 20) -> ListInput:
-    """General seeded list generator used by tests and bench.
+_I64_MIN = -(1 << 63)
 
-    keys: 'uniform' (full key_bits range, or [0, key_range)), 'zipf' (Zipf(zipf_s) rank
-    over zipf_values values, mapped to a 32-bit value by a keyed bijection -- DESIGN.md
-    reading Q17), 'equal' (all keys 0x5A..), 'max' (all ones), 'sorted'/'reverse'
-    (along the list), 'runs4096' (C4: alternating presorted / random runs of 4096 list
-    positions, reading Q12).
-    """
-    order = link_order(n, links, seed ^ 0x1111, device)
-    pos = torch.arange(n, dtype=torch.int64, device=device)
+
+def _ordered(lo: torch.Tensor, hi: torch.Tensor | None, key_bits: int) -> torch.Tensor:
+    """int64 whose signed order is the unsigned order of the key (lo, hi): the key itself
+    below 64 bits, the 64-bit pattern with its top bit flipped otherwise."""
+    return lo if key_bits < 64 else to_key_tensor(lo, 64, hi) ^ _I64_MIN
+
+
+def _from_ordered(c: torch.Tensor, key_bits: int) -> torch.Tensor:
+    return to_key_tensor(c, key_bits) if key_bits < 64 else c ^ _I64_MIN
+
+
+def _key_chunk(a: int, b: int, key_bits: int, seed: int, keys: str, key_range, thr, device) -> torch.Tensor:
+    """Keys of list positions [a, b), as the int64 `_ordered` form.  Per position, except
+    'runs4096' (per run of 4096 positions; a must be a multiple of 4096)."""
+    pos = torch.arange(a, b, dtype=torch.int64, device=device)
     lo = _stream(pos, seed, 1)
     hi = _stream(pos, seed, 2) if key_bits == 64 else None
     mask = (1 << min(key_bits, 32)) - 1
@@ -184,7 +205,6 @@ def make_list(n: int, key_bits: int, seed: int, keys: str = "uniform", links: st
         else:
             lo = lo & mask
     elif keys == "zipf":
-        thr = torch.from_numpy(zipf_thresholds(zipf_values, zipf_s)).to(device)
         rank = torch.searchsorted(thr, lo, right=True)  # 0-based rank
         lo = _bijection_bits(rank, 32, seed ^ 0x2222) & mask
         if hi is not None:
@@ -197,43 +217,60 @@ def make_list(n: int, key_bits: int, seed: int, keys: str = "uniform", links: st
         lo = torch.full_like(lo, mask)
         if hi is not None:
             hi = torch.full_like(hi, _M32)
-    elif keys in ("sorted", "reverse"):
+    elif keys in ("sorted", "reverse", "runs4096"):
         lo = lo & mask
-        if hi is None:
-            lo = torch.sort(lo, descending=(keys == "reverse")).values
-        else:
-            comb = (hi >> 1 << 32) | lo  # 63-bit ordering key (stays non-negative)
-            comb = torch.sort(comb, descending=(keys == "reverse")).values
-            hi = (comb >> 32) << 1
-            lo = comb & _M32
-    elif keys == "runs4096":
-        lo = lo & mask
+    else:
+        raise ValueError(keys)
+    comb = _ordered(lo, hi, key_bits)
+    if keys == "runs4096":
+        # alternating presorted / random runs of 4096 list positions (reading Q12): runs
+        # with an even global index are sorted ascending (by the full unsigned key)
         run = 4096
-        if hi is not None:
-            comb = (hi >> 1 << 32) | lo
-        else:
-            comb = lo.clone()
-        full = (n // run) * run
+        assert a % run == 0
+        full = ((b - a) // run) * run
         if full:
             blocks = comb[:full].view(-1, run)
             srt = torch.sort(blocks, dim=1).values
-            is_p = (torch.arange(blocks.shape[0], device=device) % 2 == 0).unsqueeze(1)
+            first = a // run
+            is_p = ((torch.arange(blocks.shape[0], device=device) + first) % 2 == 0).unsqueeze(1)
             comb[:full] = torch.where(is_p, srt, blocks).reshape(-1)
-        if hi is not None:
-            hi = (comb >> 32) << 1
-            lo = comb & _M32
-        else:
-            lo = comb
+    return comb
+
+
+def make_list(n: int, key_bits: int, seed: int, keys: str = "uniform", links: str = "random",
+              device="cpu", key_range: int | None = None, zipf_s: float = 1.1,
+              zipf_values: int = 1 << 20) -> ListInput:
+    """General seeded list generator used by tests and bench.
+
+    keys: 'uniform' (full key_bits range, or [0, key_range)), 'zipf' (Zipf(zipf_s) rank
+    over zipf_values values, mapped to a 32-bit value by a keyed bijection -- DESIGN.md
+    reading Q17), 'equal' (all keys 0x5A..), 'max' (all ones), 'sorted'/'reverse'
+    (along the list), 'runs4096' (C4: alternating presorted / random runs of 4096 list
+    positions, reading Q12).  64-bit keys use all 64 bits in every kind that draws them.
+
+    Everything is drawn per list position (or per run of 4096 positions) in chunks of
+    CHUNK positions, so large lists need no full-size temporaries; the values do not
+    depend on the chunking or on the device.
+    """
+    order = link_order(n, links, seed ^ 0x1111, device)
+    thr = torch.from_numpy(zipf_thresholds(zipf_values, zipf_s)).to(device) if keys == "zipf" else None
+    key = torch.empty(n, dtype=_KEY_TORCH[key_bits], device=device)   # node-indexed
+    if keys in ("sorted", "reverse"):  # a global sort along the list (small lists only)
+        comb = _key_chunk(0, n, key_bits, seed, keys, None, None, device)
+        comb = torch.sort(comb, descending=(keys == "reverse")).values
+        key[order] = _from_ordered(comb, key_bits)
     else:
-        raise ValueError(keys)
-    key_pos = to_key_tensor(lo, key_bits, hi)        # key of the node at list position p
-    key = torch.empty_like(key_pos)
-    key[order] = key_pos                             # node-indexed
+        for a in range(0, n, CHUNK):
+            b = min(n, a + CHUNK)
+            key[order[a:b]] = _from_ordered(_key_chunk(a, b, key_bits, seed, keys, key_range, thr, device),
+                                            key_bits)
     nxt, head = links_from_order(order, n)
     payload = None
     if keys == "runs4096" or key_bits == 64:
-        v = torch.arange(n, dtype=torch.int64, device=device)
-        payload = to_key_tensor(_stream(v, seed, 7), 64, _stream(v, seed, 8))
+        payload = torch.empty(n, dtype=torch.int64, device=device)
+        for a in range(0, n, CHUNK):
+            v = torch.arange(a, min(n, a + CHUNK), dtype=torch.int64, device=device)
+            payload[a:a + v.shape[0]] = to_key_tensor(_stream(v, seed, 7), 64, _stream(v, seed, 8))
     return ListInput(keys=key, next=nxt, head=head, order=order, key_bits=key_bits,
                      payload=payload, name=f"n={n},u{key_bits},{keys},{links}")
 
