@@ -150,9 +150,34 @@ def bench_config(cfg: str, n: int, K: int, ws: int = 1) -> dict:
             "workspace_pool_keep_gb": float(os.environ.get("PBIT_POOL_KEEP_GB", "0"))}
 
 
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def full_size_oracle(cfg: str):
+    """The oracle's time on the FULL config, from the golden it produced
+    (tests/golden/config_<cfg>.json, tools/make_goldens.py; another host: context only)."""
+    p = os.path.join(ROOT, "tests", "golden", f"config_{cfg}.json")
+    try:
+        with open(p) as f:
+            g = json.load(f)
+        return {"n": g["n"], "seconds": g["oracle_s"], "nodes_per_s": round(g["n"] / g["oracle_s"], 1),
+                "cpu": g.get("cpu"), "source": os.path.relpath(p, ROOT)}
+    except Exception:
+        return None
+
+
 def cpu_baseline(cfg: str, sample_n: int, reps: int = 1):
     """The oracle as it stands (paper-literal Pbit, K=4, one thread) on a bounded
-    sample of the workload."""
+    sample of the workload, on this host's cores."""
     import oracle
     import workloads
     c = workloads.CONFIGS[cfg]
@@ -166,8 +191,10 @@ def cpu_baseline(cfg: str, sample_n: int, reps: int = 1):
         ts.append(time.perf_counter() - t0)
     t = statistics.mean(ts)
     return {"value": sample_n / t, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{cfg}-shaped list, n={sample_n} (seed {c['seed']}), paper-literal Pbit K=4, "
-                      f"mean of {reps} run(s), {t:.2f} s each, single thread"}
+            "cpu": cpu_model(), "host_threads": os.cpu_count(),
+            "sample": f"{cfg}-shaped list, n={sample_n} of the config's {c['n']} (seed {c['seed']}), "
+                      f"paper-literal Pbit K=4, mean of {reps} run(s), {t:.2f} s each, single thread",
+            "full_size": full_size_oracle(cfg)}
 
 
 def run_reference(args):
@@ -199,12 +226,14 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u32" if c["key_bits"] <= 32 else "u64",
             "data": "synthetic",
-            "config": bench_config(args.config, c["n"] if args.n is None else args.n,
-                                   args.digit_bits or c["digit_bits"], args.gpus),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "config": dict(bench_config(args.config, sample_n, args.digit_bits or c["digit_bits"], args.gpus),
+                           sample_of_n=c["n"] if args.n is None else args.n),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu": cpu_model(),
+                             "host_threads": os.cpu_count(),
                              "sample": f"each step: a bounded sample of the workload, a {args.config}-shaped list "
-                                       f"of n={sample_n} sorted by the paper-literal Pbit (K=4) on one core; "
-                                       f"{args.steps} timed steps"},
+                                       f"of n={sample_n} (the config has {c['n']}) sorted by the paper-literal "
+                                       f"Pbit (K=4) on one core; {args.steps} timed steps",
+                             "full_size": full_size_oracle(args.config)},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     if ws > 1:
@@ -399,6 +428,10 @@ def run_ours(args):
                 "kernel_ms": round(dom_ms, 4), "alg_bytes_per_node": b, "peak_source": peak_src,
                 "phase_ms": {k_: round(v, 4) for k_, v in phases.items()},
                 "whole_call_impl_bytes_per_node": total_alg,
+                # the method's one-read-one-write bound (read key + next, write
+                # out_next) over the dominant kernel's time and over the whole call
+                "method_bytes_per_node": method_bytes_per_node(kb),
+                "frac_at_method_bytes": round(method_bytes_per_node(kb) * n / (dom_ms / 1e3) / 1e9 / peak, 4),
                 "whole_call_method_frac": round(method_bytes_per_node(kb) * n / (ms / 1e3) / 1e9 / peak, 4)}
     if dom == "walk":
         # the walk visits every node once in list order = one random 128 B line per node
@@ -414,6 +447,10 @@ def run_ours(args):
         whole = {"dram_bytes_per_call": dram, "ms": round(ms, 4), "gbs": round(dram / (ms / 1e3) / 1e9, 1),
                  "frac_of_peak": round(dram / (ms / 1e3) / 1e9 / peak, 4),
                  "frac_of_nominal_8tbs": round(dram / (ms / 1e3) / 1e9 / 8000.0, 4),
+                 # DRAM bytes / time rises with wasted traffic: read it with the amplification
+                 # over the method's bound and the work-normalised fraction beside it
+                 "amplification_over_method_bytes": round(dram / (method_bytes_per_node(kb) * n), 2),
+                 "work_normalised_frac": round(method_bytes_per_node(kb) * n / (ms / 1e3) / 1e9 / peak, 4),
                  "source": tr.get("_source")}
 
     # ---- the paper's tables-versus-lists comparison on this GPU: the same

@@ -200,6 +200,13 @@ int pbit_mg_comm_destroy(void *comm);
  * ends its pending collectives on the call's stream.  The communicator is then unusable. */
 int pbit_mg_comm_abort(void *comm);
 
+/* The transport pbit_sort_list_mg used on this communicator in its last call: 0 = peer
+ * (N4: every rank maps the others' windows through CUDA IPC; the walk reads remote nodes
+ * with peer loads and the exchanges are stores into the destination's memory), 1 = NCCL
+ * (kn replica + ncclSend/ncclRecv; PBIT_MG_TRANSPORT=nccl forces it; also the fallback when
+ * a rank cannot map the others).  -1 for a NULL communicator. */
+int pbit_mg_transport(void *comm);
+
 /* Node ids per rank for pbit_sort_list_mg: ceil(n_global / nranks) rounded up to 64. */
 uint64_t pbit_mg_slice(uint64_t n_global, int nranks);
 

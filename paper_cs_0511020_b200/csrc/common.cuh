@@ -60,6 +60,30 @@ struct RulerSel {
   }
 };
 
+// ----------------------------------------------------------------------------- division
+// x / d for a divisor fixed per launch (Granlund-Montgomery, d >= 2): the multi-GPU walk
+// divides every node id by the rank slice S to find the rank that owns it.
+struct FastDiv {
+  uint32_t d = 2, m = 0, s = 1;
+  __host__ static FastDiv make(uint32_t d) {
+    FastDiv f;
+    f.d = d < 2 ? 2 : d;
+    uint32_t sh = 0;
+    while ((1ull << sh) < f.d) ++sh;  // ceil(log2 d)
+    f.s = sh;
+    f.m = (uint32_t)((((1ull << 32) * ((1ull << sh) - f.d)) / f.d) + 1);
+    return f;
+  }
+  __host__ __device__ __forceinline__ uint32_t div(uint32_t x) const {
+#ifdef __CUDA_ARCH__
+    const uint32_t t = __umulhi(x, m);
+#else
+    const uint32_t t = (uint32_t)(((unsigned long long)x * m) >> 32);
+#endif
+    return (t + ((x - t) >> 1)) >> (s - 1);
+  }
+};
+
 // ----------------------------------------------------------------------------- plan
 // Device-side pass plan written by k_plan: the non-trivial digits, low to high.
 // A digit whose histogram has one bin holding all n keys cannot reorder anything

@@ -60,6 +60,11 @@ constexpr int SWEEP_IPT32 = PBIT_SWEEP_IPT;                       // items per t
 #define PBIT_SWEEP_IPT64 (PBIT_SWEEP_IPT == 16 ? 12 : PBIT_SWEEP_IPT * 3 / 4 + 1)
 #endif
 constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
+// write-out of the stable passes: 128-bit stores over 16 B-aligned groups of every digit
+// run (1), or one 4 B store per element, consecutive threads on consecutive elements (0)
+#ifndef PBIT_VEC_STORE
+#define PBIT_VEC_STORE 1
+#endif
 // per-warp digit counters of the pass ranking: u32 (one word per digit: no two digits
 // share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
 using WCnt = std::conditional_t<PBIT_WCNT32 != 0, uint32_t, uint16_t>;
@@ -153,15 +158,49 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
 }
 
 // ============================================================================ a1: walk
+// Which rulers one walk launch handles and where their records go.  Ruler indices are
+// global (they index the segment table); slots are local to the launching GPU.
+//   static rulers  r in [r_lo, r_lo + n_static)   start at sel.node_of(r), slot r - r_lo
+//   the head       r = head_idx (unless NULL)      starts at the head,      slot n_static
+//   dynamic        r = dyn_base + k                opened by a cut segment, slot dyn_slot0 + k
+// Single GPU: r_lo = 0 and slot(r) = r (head_idx = R, dyn_base = dyn_slot0 = R_static).
+struct WalkMap {
+  uint32_t r_lo, n_static, head_idx, dyn_base, dyn_slot0;
+  __host__ __device__ __forceinline__ uint32_t count() const { return n_static + (head_idx != PBIT_NULL32 ? 1u : 0u); }
+};
+
+// Where the walk reads kn[u]: one array (single GPU, or the multi-GPU replica), or the
+// owners' slices through peer pointers (multi-GPU, NEXT row N4: rank q owns ids
+// [q*S, q*S + S) and its slice is mapped into every rank's address space).
+template <typename RT>
+struct KnSrc {
+  const RT* kn;            // !PEER: node-indexed records
+  const RT* peer[64];      // PEER: rank q's slice (local index u - q*S)
+  FastDiv S;               // PEER: the rank slice
+};
+
+template <typename RT, bool PEER>
+__device__ __forceinline__ RT load_kn(const KnSrc<RT>& src, const RT* const* s_peer, uint32_t u) {
+  const RT* p;
+  if constexpr (PEER) {
+    const uint32_t q = src.S.div(u);
+    p = s_peer[q] + (u - q * src.S.d);
+  } else {
+    p = src.kn + u;
+  }
+  if constexpr (sizeof(RT) == 16) return ld_stream_u4(reinterpret_cast<const uint4*>(p));
+  else return ld_stream_u2(reinterpret_cast<const uint2*>(p));
+}
+
 // One thread walks one segment at a time: from its ruler node along next[] until the
 // next ruler (or NULL), writing (key, id) of each visited node into the segment's slot
 // in list order -- the same sequential traversal as the paper's split loop L=L->next
 // (P:353), which is what makes the result stable.  A segment longer than `cap` is cut:
-// the walker opens a dynamic ruler (slot R_static + k) at the current node and goes on.
+// the walker opens a dynamic ruler (WalkMap) at the current node and goes on.
 // Rulers are handed out per CTA from a contiguous range through a smem counter.
-template <int KB>
+template <int KB, bool PEER = false>
 __global__ void __launch_bounds__(WALK_THREADS)
-k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_static, uint32_t head,
+k_walk(const __grid_constant__ KnSrc<typename Rec<KB>::T> src, RulerSel sel, WalkMap wm, uint32_t head,
        typename Rec<KB>::T* __restrict__ slots, uint32_t cap, uint2* __restrict__ seg,
        uint32_t* __restrict__ dyn_count, uint32_t dyn_cap, uint32_t per_cta, int* __restrict__ err,
        int no_writes) {  // no_writes: timing experiments only
@@ -171,18 +210,23 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
   // whole 32 B sectors: a partial-sector store costs an HBM read-modify-write on B200.
   constexpr int B = (KB == 8 ? WALK_FLUSH_BYTES64 : WALK_FLUSH_BYTES) / (int)sizeof(RT);
   __shared__ uint32_t s_next;
+  __shared__ const RT* s_peer[PEER ? 64 : 1];
   if (threadIdx.x == 0) s_next = 0;
+  if constexpr (PEER)
+    if (threadIdx.x < 64) s_peer[threadIdx.x] = src.peer[threadIdx.x];
   __syncthreads();
   const uint32_t n = sel.n;
+  const uint32_t total = wm.count();
   const uint32_t lo = blockIdx.x * per_cta;
-  const uint32_t hi = min(lo + per_cta, R_static);
+  const uint32_t hi = min(lo + per_cta, total);
   RT buf[B];
   for (;;) {
-    const uint32_t r = lo + atomicAdd(&s_next, 1u);
-    if (r >= hi) break;
-    uint32_t u = r < sel.R ? sel.node_of(r) : head;
-    uint32_t cur = r, j = 0;  // j: records of segment `cur` already stored
-    RT* out = slots + (size_t)cur * cap;
+    const uint32_t i = lo + atomicAdd(&s_next, 1u);
+    if (i >= hi) break;
+    const bool is_head = i == wm.n_static;
+    uint32_t u = is_head ? head : sel.node_of(wm.r_lo + i);
+    uint32_t cur = is_head ? wm.head_idx : wm.r_lo + i, j = 0;  // j: records of segment `cur` already stored
+    RT* out = slots + (size_t)i * cap;
     for (;;) {
       // one group of up to B steps, unrolled so that buf[] is indexed statically
       uint32_t m = 0, succ = PBIT_NULL32;
@@ -190,8 +234,7 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
 #pragma unroll
       for (int q = 0; q < B; ++q) {
         if (!end) {
-          RT x;
-          if constexpr (KB == 8) x = ld_stream_u4(kn + u); else x = ld_stream_u2(kn + u);
+          RT x = load_kn<RT, PEER>(src, s_peer, u);
           uint32_t v;
           if constexpr (KB == 8) { v = x.z; x.z = u; } else { v = x.y; x.y = u; }
           buf[q] = x;
@@ -223,9 +266,9 @@ k_walk(const typename Rec<KB>::T* __restrict__ kn, RulerSel sel, uint32_t R_stat
       if (j == cap) {  // cap is a multiple of B
         const uint32_t k = atomicAdd(dyn_count, 1u);
         if (k >= dyn_cap) { atomicOr(err, E_DYN_FULL); seg[cur] = make_uint2(j, PBIT_NULL32); break; }
-        const uint32_t r2 = R_static + k;
+        const uint32_t r2 = wm.dyn_base + k;
         seg[cur] = make_uint2(cap, r2);
-        cur = r2; j = 0; out = slots + (size_t)cur * cap;
+        cur = r2; j = 0; out = slots + (size_t)(wm.dyn_slot0 + k) * cap;
       }
     }
   }
@@ -484,6 +527,7 @@ struct SweepSmem {
   WCnt wcnt[SWEEP_WARPS][RADIX];
   uint32_t dstart[RADIX];
   uint32_t goff[RADIX];
+  uint32_t gpre[RADIX + 1];  // 128-bit write-out: exclusive scan of each digit run's 16 B groups
   uint32_t scan[SWEEP_WARPS];
   uint32_t tile;
   int bad;
@@ -530,6 +574,8 @@ static __global__ void k_selftest_atomic_order(uint32_t iters, uint32_t* bad) {
   if (nb) atomicAdd(bad, nb);
 }
 
+struct SplitTable;  // the multi-GPU key-range partition (below)
+
 // What one launch of k_onesweep sorts: one key pass (digit `digit`, input buffer `src`).
 struct SweepArgs {
   const void* kin[2];
@@ -557,6 +603,7 @@ struct SweepArgs {
   const uint32_t* seg_pos;        // list position of the k-th segment's first node
   const uint32_t* tile_first;     // ordinal of the segment holding each tile's first position
   const uint32_t* nseg;
+  const SplitTable* split;        // SRC_SPLIT: the multi-GPU partition (device memory)
 };
 
 // In-warp stable ranking modes (RANK template parameter of k_onesweep).
@@ -732,7 +779,43 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
 
 // Where the first pass's tile comes from (k_onesweep SRC): TMA of keys and ids; the
 // walk's segment slots (list sort, pass 0); TMA of keys with ids = positions (array sort).
-enum : int { SRC_TMA = 0, SRC_GATHER = 1, SRC_IOTA = 2 };
+// SRC_SPLIT (multi-GPU): TMA of keys and ids, the digit is the key's bucket among the
+// splitters, and the write-out sends each element to its destination rank (SplitTable).
+enum : int { SRC_TMA = 0, SRC_GATHER = 1, SRC_IOTA = 2, SRC_SPLIT = 3 };
+
+// The key-range partition of the multi-GPU sort (pbit_sort_list_mg, SRC_SPLIT), written
+// on the device by k_split_plan.  Bucket of key k: j = #{s : kstar[s] < k}, then
+// 2j + (j < NS && kstar[j] == k): buckets in key order, the keys equal to a splitter key in
+// their own bucket.  The pass sorts a rank's list-order chunk stably by bucket; element g
+// of that order goes to rank d = #{s in 1..G-1 : left[s] <= g}, at index g + dst_off[d] of
+// that rank's receive arrays (dst_k[d], dst_i[d]: a peer's window -- N4 -- or, with the
+// NCCL transport, this rank's send buffer with dst_off = 0).
+struct SplitTable {
+  uint32_t G, NS;
+  unsigned long long kstar[64];
+  uint32_t left[65];
+  uint32_t dst_off[64];
+  void* dst_k[64];
+  uint32_t* dst_i[64];
+};
+
+__device__ __forceinline__ uint32_t split_bucket(const SplitTable& sp, unsigned long long k) {
+  uint32_t lo = 0, hi = sp.NS;  // lower_bound: first s with kstar[s] >= k
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sp.kstar[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  return 2u * lo + ((lo < sp.NS && sp.kstar[lo] == k) ? 1u : 0u);
+}
+
+__device__ __forceinline__ uint32_t split_dest(const SplitTable& sp, uint32_t g) {
+  uint32_t lo = 1, hi = sp.G;  // ranks d >= 1 whose first element left[d] <= g
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (sp.left[mid] <= g) lo = mid + 1; else hi = mid;
+  }
+  return lo - 1;
+}
 
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int SRC = SRC_TMA>
 __global__ void __launch_bounds__(SWEEP_THREADS, 2)
@@ -761,6 +844,11 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   unsigned long long* status = a.status;
   const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
 
+  SplitTable& sp = *reinterpret_cast<SplitTable*>(smem_raw + sizeof(S));  // SRC_SPLIT only
+  if constexpr (SRC == SRC_SPLIT) {
+    for (uint32_t i = threadIdx.x; i < sizeof(SplitTable) / 4; i += SWEEP_THREADS)
+      reinterpret_cast<uint32_t*>(&sp)[i] = reinterpret_cast<const uint32_t*>(a.split)[i];
+  }
   if (t == 0) {
     sm.bad = *a.err;  // an invalid list (found after the pass was queued): no pass runs
     sm.tile = atomicAdd(a.tile_ctr + slot, 1u);
@@ -811,8 +899,16 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 #pragma unroll
   for (int i = 0; i < IPT; ++i) key[i] = AOS ? (KeyT)srec[wofs + i * 32 + lane].x : sm.k[wofs + i * 32 + lane];
   const bool combine = a.combine != 0;
-  if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
-  else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
+  if constexpr (SRC == SRC_SPLIT) {  // digit = the key's splitter bucket
+    uint32_t dg[IPT];
+#pragma unroll
+    for (int i = 0; i < IPT; ++i) dg[i] = split_bucket(sp, (unsigned long long)key[i]);
+    if (full_tile) rank_items<uint32_t, RADIX_BITS, IPT, RANK, true>(dg, rd, 0, sm.wcnt[w], wofs, lane, tile_count, combine);
+    else rank_items<uint32_t, RADIX_BITS, IPT, RANK, false>(dg, rd, 0, sm.wcnt[w], wofs, lane, tile_count, combine);
+  } else {
+    if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
+    else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
+  }
   __syncthreads();
 
   // ---- per digit (thread t = digit t): exclusive over warps, tile total, aggregate
@@ -881,6 +977,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   }
 
   // ---- decoupled lookback, one thread per digit value, LB_WIN predecessors per step
+  uint32_t ngrp = 0;  // 16 B-aligned groups of 4 output slots the digit's run touches
   if (t < RADIX) {
     constexpr int LB_WIN = 4;
     unsigned long long excl = 0;
@@ -907,12 +1004,80 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
       st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (2ull << 32) | (excl + total));
     }
     sm.goff[t] = bases[t] + (uint32_t)excl - sm.dstart[t];
+    const uint32_t gs = bases[t] + (uint32_t)excl;  // the run's first global slot
+    ngrp = total ? ((gs + total + 3u) >> 2) - (gs >> 2) : 0u;
   }
   __syncthreads();
+  constexpr bool VEC = PBIT_VEC_STORE && SRC != SRC_SPLIT;
+  if constexpr (VEC) {  // exclusive scan of the group counts over the digits
+    uint32_t x = ngrp;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= (uint32_t)o) x += y;
+    }
+    if (lane == 31) sm.scan[w] = x;
+    __syncthreads();
+    uint32_t add = 0;
+#pragma unroll
+    for (int ww = 0; ww < SWEEP_WARPS; ++ww) add += (ww < (int)w) ? sm.scan[ww] : 0u;
+    if (t < RADIX) sm.gpre[t] = x - ngrp + add;
+    if (t == RADIX - 1) sm.gpre[RADIX] = x + add;
+    __syncthreads();
+  }
 
   // ---- coalesced write-out: consecutive threads store consecutive staged elements,
   // which land contiguously inside each digit run
-  if (!last) {
+  if constexpr (SRC == SRC_SPLIT) {
+    // element g of the bucket order goes to its destination rank's receive arrays
+    for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
+      const KeyT k = sm.k[j];
+      const uint32_t g = sm.goff[split_bucket(sp, (unsigned long long)k)] + j;
+      const uint32_t d = split_dest(sp, g);
+      const uint32_t at = g + sp.dst_off[d];
+      reinterpret_cast<KeyT*>(sp.dst_k[d])[at] = k;
+      sp.dst_i[d][at] = sm.iout[j];
+    }
+  } else if (VEC && ((((uintptr_t)iout | (last ? 0 : (uintptr_t)kout)) & 15u) == 0)) {
+    // 128-bit stores: every digit run is cut at 16 B boundaries of the OUTPUT arrays into
+    // groups of 4 slots; thread q takes group q (its digit by binary search over the group
+    // prefix); a whole group leaves as one 16 B store of ids (and one or two of keys), the
+    // <= 2 partial groups at the ends of a run as scalar stores
+    const uint32_t ngroups = sm.gpre[RADIX];
+    for (uint32_t q = t; q < ngroups; q += SWEEP_THREADS) {
+      uint32_t lo = 0, hi = RADIX;  // the last digit d with gpre[d] <= q
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (sm.gpre[mid] <= q) lo = mid; else hi = mid;
+      }
+      const uint32_t d = lo;
+      const uint32_t go = sm.goff[d];
+      const uint32_t j_lo = sm.dstart[d];
+      const uint32_t j_hi = d + 1 < (uint32_t)RADIX ? sm.dstart[d + 1] : tile_count;
+      const uint32_t A = (((go + j_lo) >> 2) + (q - sm.gpre[d])) << 2;  // first slot of the group
+      const int j0 = (int)(A - go);  // its staged index (negative before the run's first slot)
+      if (j0 >= (int)j_lo && j0 + 4 <= (int)j_hi) {
+        *reinterpret_cast<uint4*>(iout + A) = make_uint4(sm.iout[j0], sm.iout[j0 + 1], sm.iout[j0 + 2], sm.iout[j0 + 3]);
+        if (!last) {
+          if constexpr (sizeof(KeyT) == 8) {
+            *reinterpret_cast<ulonglong2*>(kout + A) = make_ulonglong2(sm.k[j0], sm.k[j0 + 1]);
+            *reinterpret_cast<ulonglong2*>(kout + A + 2) = make_ulonglong2(sm.k[j0 + 2], sm.k[j0 + 3]);
+          } else {
+            *reinterpret_cast<uint4*>(kout + A) = make_uint4(sm.k[j0], sm.k[j0 + 1], sm.k[j0 + 2], sm.k[j0 + 3]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int j = j0 + e;
+          if (j >= (int)j_lo && j < (int)j_hi) {
+            iout[A + e] = sm.iout[j];
+            if (!last) kout[A + e] = sm.k[j];
+          }
+        }
+      }
+    }
+  } else if (!last) {
 #pragma unroll 4
     for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
       const KeyT k = sm.k[j];
@@ -978,14 +1143,16 @@ k_array_finish(const typename KeyOf<KB>::T* __restrict__ ksorted, uint32_t n, vo
 
 // ============================================================================ a5: relink
 // out_next[ids[p]] = ids[p+1], out_next[ids[n-1]] = NULL, head = ids[0]: the paper's
-// end-splice merge of sorted fragments, one write per node.
+// end-splice merge of sorted fragments, one write per node; with out_prev (N2,
+// the doubly-linked repair of P:1179-1181) also out_prev[ids[p]] = ids[p-1] in the SAME
+// pass chain: records carry (v, succ, pred) instead of (v, succ).
 //
 // On B200 a random 4 B store costs a 32 B HBM read + write even when the stores are
 // confined to a 64 KB window (measured: tools/micro/winstore.cu), and distributed shared
 // memory windows are 2-4x slower than one CTA's (tools/micro/dsmem.cu), so no kernel here
-// issues scattered stores to HBM.  The pairs (v, succ) are grouped by fine bin
+// issues scattered stores to HBM.  The records are grouped by fine bin
 // v >> RELINK_FINE_SHIFT with MSD partition levels of <= 8 bits (k_relink_part), then each
-// fine bin is applied in a 64 KB shared-memory window and written out coalesced.
+// fine bin is applied in a 64 KB shared-memory window per output and written out coalesced.
 //
 // The ids are a permutation of [0, n), so every bin's size is known in closed form (bin
 // b of a level with shift s holds exactly the ids [b << s, (b+1) << s)): no histogram,
@@ -993,9 +1160,18 @@ k_array_finish(const typename KeyOf<KB>::T* __restrict__ ksorted, uint32_t n, vo
 // space in a bin with one global atomicAdd per (tile, bin) -- no lookback.
 constexpr int RELINK_FINE_SHIFT = 14;  // 16384 ids = 64 KB smem window
 constexpr int PART_THREADS = 512;
-constexpr int PART_IPT = 8;
-constexpr int PART_TILE = PART_THREADS * PART_IPT;  // 4096 pairs; divides every parent bin (>= 2^22)
-constexpr int PART_CTAS_PER_SM = 2;
+
+struct u32x3 { uint32_t x, y, z; };  // (v, succ, pred): 12 B relink record
+template <int W> struct RelinkRec { using T = uint2; };   // (v, succ)
+template <> struct RelinkRec<3> { using T = u32x3; };
+
+// W words per record: 4096-record tiles of pairs (2 CTAs/SM), 2048 of triples (the
+// tiles divide every parent bin, >= 2^22 ids)
+template <int W> struct PartCfg {
+  static constexpr int IPT = W == 2 ? 8 : 4;
+  static constexpr int TILE = PART_THREADS * IPT;
+};
+constexpr int PART_TILE = PartCfg<2>::TILE;
 
 // The MSD levels for n ids: level l partitions by v's bits [shift_l, shift_l + bits_l);
 // level 0 takes the top bits, the last level has shift RELINK_FINE_SHIFT.
@@ -1021,47 +1197,53 @@ struct RelinkLevels {
 };
 
 // One partition level.  FROM_IDS (level 0 of the single-GPU sort): the input is the
-// sorted id array and the pair of position p is (ids[p], ids[p+1]) (NULL after the last).
-// Otherwise the input is pairs; v_off is subtracted from v on load (the multi-GPU path
-// receives global ids).  A tile lies inside one bin of the previous level (tiles divide
-// the bins), so its local bin index is (v >> shift) & (2^bits - 1) and its global bin
-// index is (tile's parent bin) << bits | local.
+// sorted id array and the record of position p is (ids[p], ids[p+1][, ids[p-1]]) (NULL
+// past either end).  Otherwise the input is records; v_off is subtracted from v on load
+// (the multi-GPU path receives global ids).  A tile lies inside one bin of the previous
+// level (tiles divide the bins), so its local bin index is (v >> shift) & (2^bits - 1) and
+// its global bin index is (tile's parent bin) << bits | local.
 //
-// Persistent CTAs (PART_CTAS_PER_SM per SM) walk the tiles round-robin; the next tile's
-// TMA bulk load is issued before the current tile is ranked, so HBM reads stay in flight
-// while the CTA ranks, claims and stores.
+// Persistent CTAs walk the tiles round-robin; the next tile's TMA bulk load is issued
+// before the current tile is ranked, so HBM reads stay in flight while the CTA ranks,
+// claims and stores.
+template <int W>
 struct PartSmem {
-  uint2 in[2][PART_TILE];  // double-buffered tile loads (FROM_IDS: u32 ids + 4 look-ahead)
-  uint2 stage[PART_TILE];  // the tile in bin order
+  using R = typename RelinkRec<W>::T;
+  static constexpr int TILE = PartCfg<W>::TILE;
+  R in[2][TILE];  // double-buffered tile loads (FROM_IDS: u32 ids + 4 look-behind + 4 look-ahead)
+  R stage[TILE];  // the tile in bin order
   uint32_t cnt[256], start[256], gofs[256], warp[PART_THREADS / 32];
   unsigned long long mbar[2];
 };
 
-template <bool FROM_IDS>
-__global__ void __launch_bounds__(PART_THREADS, PART_CTAS_PER_SM)
-k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, uint2* __restrict__ pout,
-              uint32_t n, uint32_t v_off, int shift, int bits, uint32_t* __restrict__ cursor,
-              const int* __restrict__ err, int dir) {
+template <bool FROM_IDS, int W>
+__global__ void __launch_bounds__(PART_THREADS, 2)
+k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* __restrict__ pin,
+              typename RelinkRec<W>::T* __restrict__ pout, uint32_t n, uint32_t v_off, int shift, int bits,
+              uint32_t* __restrict__ cursor, const int* __restrict__ err) {
+  using R = typename RelinkRec<W>::T;
+  constexpr int TILE = PartCfg<W>::TILE;
+  constexpr int IPT = PartCfg<W>::IPT;
   pdl_enter();
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  PartSmem& sm = *reinterpret_cast<PartSmem*>(smem_raw);
+  PartSmem<W>& sm = *reinterpret_cast<PartSmem<W>*>(smem_raw);
   if (*err) return;
   const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t nb = 1u << bits, mask = nb - 1;
-  const uint32_t ntiles = (n + PART_TILE - 1) / PART_TILE;
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
   auto issue = [&](uint32_t tile, int buf) {  // thread 0: TMA bulk load of one tile
-    const uint32_t base = tile * (uint32_t)PART_TILE;
+    const uint32_t base = tile * (uint32_t)TILE;
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[buf]);
     uint32_t bytes;
     const void* src;
-    if constexpr (FROM_IDS) {  // the tile's ids plus 4 look-ahead (dir +1) or look-behind (-1)
-      const uint32_t lo = dir > 0 ? base : (base >= 4u ? base - 4u : 0u);
-      const uint32_t c = min(base + (uint32_t)PART_TILE + 4u, n) - lo;
+    if constexpr (FROM_IDS) {  // the tile's ids plus 4 look-ahead (and 4 look-behind for W = 3)
+      const uint32_t lo = (W == 3 && base >= 4u) ? base - 4u : base;
+      const uint32_t c = min(base + (uint32_t)TILE + 4u, n) - lo;
       bytes = ((c + 3u) & ~3u) * 4u;
       src = ids + lo;
     } else {
-      const uint32_t c = min((uint32_t)PART_TILE, n - base);
-      bytes = ((c + 1u) & ~1u) * 8u;
+      const uint32_t c = min((uint32_t)TILE, n - base);
+      bytes = ((c * (uint32_t)sizeof(R)) + 15u) & ~15u;  // buffers are padded by 16 B
       src = pin + base;
     }
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
@@ -1090,21 +1272,20 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
                      : "=r"(done) : "r"(m), "r"(par) : "memory");
     }
     __syncthreads();
-    const uint32_t base = tile * (uint32_t)PART_TILE;
-    const uint32_t cnt = min((uint32_t)PART_TILE, n - base);
-    uint2 x[PART_IPT];
-    uint32_t r[PART_IPT];
+    const uint32_t base = tile * (uint32_t)TILE;
+    const uint32_t cnt = min((uint32_t)TILE, n - base);
+    R x[IPT];
+    uint32_t r[IPT];
     const uint32_t* in_ids = reinterpret_cast<const uint32_t*>(&sm.in[buf][0]);
-    const uint32_t off = (FROM_IDS && dir < 0) ? (base >= 4u ? 4u : 0u) : 0u;  // look-behind shift
+    const uint32_t off = (FROM_IDS && W == 3 && base >= 4u) ? 4u : 0u;  // look-behind shift
 #pragma unroll
-    for (int i = 0; i < PART_IPT; ++i) {
+    for (int i = 0; i < IPT; ++i) {
       const uint32_t j = i * PART_THREADS + t;
       if (j < cnt) {
         if constexpr (FROM_IDS) {
-          // dir +1: (ids[p], ids[p+1]) -> out_next; dir -1: (ids[p], ids[p-1]) -> out_prev
           x[i].x = in_ids[off + j];
-          if (dir > 0) x[i].y = base + j + 1 < n ? in_ids[j + 1] : PBIT_NULL32;
-          else x[i].y = base + j > 0 ? in_ids[off + j - 1] : PBIT_NULL32;
+          x[i].y = base + j + 1 < n ? in_ids[off + j + 1] : PBIT_NULL32;
+          if constexpr (W == 3) x[i].z = base + j > 0 ? in_ids[off + j - 1] : PBIT_NULL32;
         } else {
           x[i] = sm.in[buf][j];
           x[i].x -= v_off;
@@ -1136,21 +1317,22 @@ k_relink_part(const uint32_t* __restrict__ ids, const uint2* __restrict__ pin, u
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < PART_IPT; ++i) {
+    for (int i = 0; i < IPT; ++i) {
       const uint32_t j = i * PART_THREADS + t;
       if (j < cnt) sm.stage[sm.start[(x[i].x >> shift) & mask] + r[i]] = x[i];
     }
     // gofs[b] = where the bin's claimed run starts minus where it starts in the stage
-    // (mod 2^32), so a staged pair j goes to gofs[b] + j: one table lookup per pair
+    // (mod 2^32), so a staged record j goes to gofs[b] + j: one table lookup per record
     if (t < nb) sm.gofs[t] = (((parent << bits) | t) << shift) + claim - my_start;
     __syncthreads();
-    // coalesced write-out: consecutive threads store consecutive staged pairs, which land
-    // contiguously inside each bin's run
+    // coalesced write-out: consecutive threads store consecutive staged records, which
+    // land contiguously inside each bin's run
 #pragma unroll 4
     for (uint32_t j = t; j < cnt; j += PART_THREADS) {
-      const uint2 p = sm.stage[j];
+      const R p = sm.stage[j];
       const uint32_t b = (p.x >> shift) & mask;
-      __stcs(pout + (sm.gofs[b] + j), p);
+      if constexpr (W == 2) __stcs(pout + (sm.gofs[b] + j), p);
+      else pout[sm.gofs[b] + j] = p;
     }
     __syncthreads();  // stage, start and gofs are rewritten by the next tile
   }
@@ -1163,34 +1345,43 @@ static __global__ void k_relink_head(const uint32_t* __restrict__ ids, uint32_t*
   *d_head = ids[0];
 }
 
-// Last step: one CTA per fine bin: scatter into a 64 KB smem window, write it coalesced.
-// FROM_IDS: n <= 2^14, one window, the pairs come straight from the sorted ids.
-// `out_next` is the output array: out_next (dir +1) or out_prev (dir -1, N2).
-template <bool FROM_IDS>
+// Last step: one CTA per fine bin: scatter into a 64 KB smem window per output, write it
+// out coalesced.  FROM_IDS: n <= 2^14, one window, the records come straight from the
+// sorted ids.  W = 3 also fills out_prev.
+template <bool FROM_IDS, int W>
 __global__ void __launch_bounds__(512)
-k_relink_apply(const uint32_t* __restrict__ ids, const uint2* __restrict__ pairs, uint32_t n, uint32_t v_off,
-               uint32_t* __restrict__ out_next, const int* __restrict__ err, int dir) {
+k_relink_apply(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* __restrict__ recs, uint32_t n,
+               uint32_t v_off, uint32_t* __restrict__ out_next, uint32_t* __restrict__ out_prev,
+               const int* __restrict__ err) {
+  using R = typename RelinkRec<W>::T;
   pdl_enter();
-  extern __shared__ __align__(16) uint32_t s_win[];
+  extern __shared__ __align__(16) uint32_t s_win[];  // [W - 1][2^RELINK_FINE_SHIFT]
+  uint32_t* s_prev = s_win + (1u << RELINK_FINE_SHIFT);
   if (*err) return;
   const uint32_t f0 = blockIdx.x << RELINK_FINE_SHIFT;
   const uint32_t cnt = min((uint32_t)(1u << RELINK_FINE_SHIFT), n - f0);
   for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
     if constexpr (FROM_IDS) {
-      if (dir > 0) s_win[ids[i]] = i + 1 < n ? ids[i + 1] : PBIT_NULL32;
-      else s_win[ids[i]] = i > 0 ? ids[i - 1] : PBIT_NULL32;
+      s_win[ids[i]] = i + 1 < n ? ids[i + 1] : PBIT_NULL32;
+      if constexpr (W == 3) s_prev[ids[i]] = i > 0 ? ids[i - 1] : PBIT_NULL32;
     } else {
-      const uint2 p = __ldcs(pairs + f0 + i);
-      s_win[p.x - v_off - f0] = p.y;
+      R p;
+      if constexpr (W == 2) p = __ldcs(recs + f0 + i); else p = recs[f0 + i];
+      const uint32_t v = p.x - v_off - f0;
+      s_win[v] = p.y;
+      if constexpr (W == 3) s_prev[v] = p.z;
     }
   }
   __syncthreads();
-  uint32_t* dst = out_next + f0;
-  if ((cnt & 3u) == 0 && ((uintptr_t)dst & 15u) == 0) {
-    for (uint32_t i = threadIdx.x; i < cnt / 4; i += blockDim.x)
-      __stcs(reinterpret_cast<uint4*>(dst) + i, reinterpret_cast<const uint4*>(s_win)[i]);
-  } else {
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = s_win[i];
+  for (int o = 0; o < W - 1; ++o) {
+    uint32_t* dst = (o == 0 ? out_next : out_prev) + f0;
+    const uint32_t* src = o == 0 ? s_win : s_prev;
+    if ((cnt & 3u) == 0 && ((uintptr_t)dst & 15u) == 0) {
+      for (uint32_t i = threadIdx.x; i < cnt / 4; i += blockDim.x)
+        __stcs(reinterpret_cast<uint4*>(dst) + i, reinterpret_cast<const uint4*>(src)[i]);
+    } else {
+      for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) dst[i] = src[i];
+    }
   }
 }
 

@@ -34,13 +34,14 @@ static inline void once_per_device(std::atomic<unsigned long long>& done, F&& se
 template <typename KeyT, int RB, int IPT, int RANK, int SRC>
 static void launch_one_m(const SweepArgs& a, cudaStream_t st) {
   using S = SweepSmem<KeyT, RB, IPT>;
+  constexpr size_t smem = sizeof(S) + (SRC == SRC_SPLIT ? sizeof(SplitTable) : 0);
   static std::atomic<unsigned long long> attr{0};
   once_per_device(attr, [] {
     cudaFuncSetAttribute(k_onesweep<KeyT, RB, IPT, RANK, SRC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)sizeof(S));
+                         (int)smem);
   });
   const uint32_t ntiles = (a.n + S::TILE - 1) / S::TILE;
-  launch_pdl(k_onesweep<KeyT, RB, IPT, RANK, SRC>, ntiles, SWEEP_THREADS, sizeof(S), st, a);
+  launch_pdl(k_onesweep<KeyT, RB, IPT, RANK, SRC>, ntiles, SWEEP_THREADS, smem, st, a);
 }
 
 template <typename KeyT, int RB, int IPT, int SRC = SRC_TMA>
@@ -136,50 +137,68 @@ static inline size_t relink_cursor_words(uint32_t n) {
   return c + 1;
 }
 
-// a5 relink of n local ids: out_next[v] = succ.  Source: the sorted ids (`ids`, pairs
-// formed on the fly) or pairs (`pairs`, v - v_off = local id).  pbuf[2]: n pairs each;
-// when the source is pairs it must not be pbuf[0] (level 0 writes pbuf[0]).
-// Returns the number of kernels launched.
-// dir = -1 (ids source only): out_next receives the predecessors instead (out_prev, the
-// doubly-linked repair of P:1179-1181).
-static uint32_t launch_relink(const uint32_t* ids, const uint2* pairs, uint32_t v_off, uint32_t n, uint2* pbuf0,
-                              uint2* pbuf1, uint32_t* cursors, uint32_t* out_next, const int* err, cudaStream_t st,
-                              int sms, int dir = 1) {
+// a5 relink of n local ids: out_next[v] = succ (and out_prev[v] = pred when out_prev is
+// set: records of three words).  Source: the sorted ids (`ids`, records formed on the fly)
+// or records (`recs`, v - v_off = local id; pairs if out_prev is NULL, else triples).
+// rbuf[2]: n records each (+16 B of padding); when the source is records it must not be
+// rbuf[0] (level 0 writes rbuf[0]).  Returns the number of kernels launched.
+template <int W>
+static uint32_t launch_relink_w(const uint32_t* ids, const void* recs, uint32_t v_off, uint32_t n, void* rbuf0,
+                                void* rbuf1, uint32_t* cursors, uint32_t* out_next, uint32_t* out_prev,
+                                const int* err, cudaStream_t st, int sms) {
+  using R = typename RelinkRec<W>::T;
+  constexpr size_t WIN = (size_t)(W - 1) * (4u << RELINK_FINE_SHIFT);
   static std::atomic<unsigned long long> attr{0};
+  static int part_occ = 1;
   once_per_device(attr, [] {
-    cudaFuncSetAttribute(k_relink_apply<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
-    cudaFuncSetAttribute(k_relink_apply<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << RELINK_FINE_SHIFT);
-    cudaFuncSetAttribute(k_relink_part<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
-    cudaFuncSetAttribute(k_relink_part<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem));
+    cudaFuncSetAttribute(k_relink_apply<true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WIN);
+    cudaFuncSetAttribute(k_relink_apply<false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WIN);
+    cudaFuncSetAttribute(k_relink_part<true, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem<W>));
+    cudaFuncSetAttribute(k_relink_part<false, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PartSmem<W>));
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_relink_part<false, W>, PART_THREADS,
+                                                      sizeof(PartSmem<W>)) != cudaSuccess) {
+      cudaGetLastError();
+      occ = 1;
+    }
+    part_occ = std::max(occ, 1);
   });
   if (n == 0) return 0;
   RelinkLevels lv(n);
   const uint32_t nfine = (n + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
   if (lv.L == 0) {
-    if (ids) k_relink_apply<true><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(ids, nullptr, n, 0, out_next, err, dir);
-    else k_relink_apply<false><<<1, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, pairs, n, v_off, out_next, err, 1);
+    if (ids) k_relink_apply<true, W><<<1, 512, WIN, st>>>(ids, nullptr, n, 0, out_next, out_prev, err);
+    else k_relink_apply<false, W><<<1, 512, WIN, st>>>(nullptr, (const R*)recs, n, v_off, out_next, out_prev, err);
     return 1;
   }
-  const uint32_t ntiles = (n + PART_TILE - 1) / PART_TILE;
-  const uint32_t grid = std::min<uint32_t>(ntiles, (uint32_t)(sms * PART_CTAS_PER_SM));
-  const size_t psm = sizeof(PartSmem);
-  const uint2* in = pairs;
-  uint2* buf[2] = {pbuf0, pbuf1};
+  constexpr uint32_t TILE = PartCfg<W>::TILE;
+  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const uint32_t grid = std::min<uint32_t>(ntiles, (uint32_t)(sms * part_occ));
+  const size_t psm = sizeof(PartSmem<W>);
+  const R* in = (const R*)recs;
+  R* buf[2] = {(R*)rbuf0, (R*)rbuf1};
   for (int l = 0; l < lv.L; ++l) {
-    uint2* out = buf[l & 1];
+    R* out = buf[l & 1];
     if (l == 0 && ids)
-      k_relink_part<true><<<grid, PART_THREADS, psm, st>>>(ids, nullptr, out, n, 0, lv.shift[l], lv.bits[l], cursors,
-                                                           err, dir);
+      k_relink_part<true, W><<<grid, PART_THREADS, psm, st>>>(ids, nullptr, out, n, 0, lv.shift[l], lv.bits[l],
+                                                              cursors, err);
     else
-      k_relink_part<false><<<grid, PART_THREADS, psm, st>>>(nullptr, in, out, n, l == 0 ? v_off : 0u, lv.shift[l],
-                                                            lv.bits[l], cursors, err, 1);
+      k_relink_part<false, W><<<grid, PART_THREADS, psm, st>>>(nullptr, in, out, n, l == 0 ? v_off : 0u,
+                                                               lv.shift[l], lv.bits[l], cursors, err);
     cursors += RelinkLevels::cursors(n, lv.shift[l]);
     in = out;
   }
   // the relink kernels are launched plainly: with PDL the waiting apply CTAs would take
   // SM room from the persistent partition kernel (C3 relink +0.04 ms, measured)
-  k_relink_apply<false><<<nfine, 512, 4u << RELINK_FINE_SHIFT, st>>>(nullptr, in, n, 0, out_next, err, 1);
+  k_relink_apply<false, W><<<nfine, 512, WIN, st>>>(nullptr, in, n, 0, out_next, out_prev, err);
   return (uint32_t)lv.L + 1;
+}
+
+static inline uint32_t launch_relink(const uint32_t* ids, const void* recs, uint32_t v_off, uint32_t n, void* rbuf0,
+                                     void* rbuf1, uint32_t* cursors, uint32_t* out_next, uint32_t* out_prev,
+                                     const int* err, cudaStream_t st, int sms) {
+  return out_prev ? launch_relink_w<3>(ids, recs, v_off, n, rbuf0, rbuf1, cursors, out_next, out_prev, err, st, sms)
+                  : launch_relink_w<2>(ids, recs, v_off, n, rbuf0, rbuf1, cursors, out_next, nullptr, err, st, sms);
 }
 
 }  // namespace pbit

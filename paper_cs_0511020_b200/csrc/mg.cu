@@ -2,29 +2,44 @@
 // NCCL communicator, plus the NCCL communicator helpers.
 //
 // Rank r owns node ids [r*S, r*S + n_local), S = 64 * ceil(ceil(n/G) / 64), and after the
-// exchange holds sorted positions [r*S, r*S + S) of the output.  SURVEY §8(e):
-//   1  pack own slice -> kn replica         ncclAllGather(kn), ncclAllReduce(digit histograms)
-//   2  count-walk own rulers                 ncclAllGather(segment table), ncclAllReduce(error)
-//   3  rank the ruler list (every rank, redundantly; validates the list)
-//   4  emit-walk the segments covering own positions [r*S, r*S+S) -> list-order chunk
+// key-range exchange holds sorted positions [r*S, r*S + S) of the output.
+// Two transports move the data between the ranks:
+//
+//   PEER (NEXT row N4, the default where every rank can map every other rank's memory --
+//   NVLink / NVSwitch peers, CUDA IPC): no replica.  Each rank packs its slice into a
+//   window of device memory that every rank maps; the walk reads kn[v] from v's owner
+//   with peer loads; the list-order chunk is gathered from the walkers' segment slots;
+//   the key-range partition pass stores every element straight into its destination
+//   rank's receive arrays (the scatter fused with the all-to-all); the relink records are
+//   stored straight into their owner's receive buffer.  NCCL carries only small
+//   collectives (histograms, segment tables, counts) that also order the phases.
+//   NCCL (the bit-identity reference): a kn replica by ncclAllGather, a count walk and an
+//   emit walk over it, and ncclSend/ncclRecv for both exchanges.
+//
+// Steps (both transports):
 //   0  the ranks agree on their arguments (one all-reduce; pbit.h)
-//   5  stable local sort of the chunk by the full key; exact splitters of the global
-//      (key, list position) order at ranks (s+1)*S by radix refinement (ncclAllReduce
-//      of candidate counts per digit); the host planner splits ties in rank order;
-//      the sorted ranges are exchanged                                   ncclSend/Recv
-//   6  full local sort of the received runs (stable LSD, all non-trivial digits)
-//   7  stitch (ncclAllGather of first ids) and route (v, succ) to the owner of v
-//                                           ncclSend/Recv; local windowed relink
-// Received streams are concatenated in source-rank order: elements with equal keys from
-// lower ranks have smaller list positions, so the stable local sort of step 6 restores
-// the global stable order exactly.
+//   1  pack the own slice (+ every digit's histogram)           ncclAllReduce(histograms)
+//   2  ruling-set walk of the own rulers                         ncclAllGather(segment table)
+//   3  rank the ruler list (every rank, redundantly; validates the list)
+//   4  the list-order chunk of positions [r*S, r*S + S)
+//   5  exact splitters of the global (key, list position) order, 8 bits per round on the
+//      device (ncclAllReduce of candidate histograms); bucket counts and the exchange plan
+//      on the device (ncclAllGather)
+//   6  one stable partition pass by splitter bucket -> the destination ranks
+//   7  stable local sort of the received runs (source-rank order = list-position order for
+//      equal keys, so the stable passes restore the global stable order)
+//   8  stitch (ncclAllGather of first / last ids) and route (v, succ[, pred]) to the owner
+//      of v; the owner applies them with the single-GPU binned relink.
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
 #include <string.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <chrono>
+#include <map>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -45,7 +60,7 @@ struct Bump {
   template <typename T>
   T* take(size_t count) {
     T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
-    off += (count * sizeof(T) + 255) & ~(size_t)255;
+    off += (count * sizeof(T) + 16 + 255) & ~(size_t)255;  // +16 B: tile loads may read past the end
     return p;
   }
 };
@@ -108,16 +123,177 @@ static int mg_wait(cudaStream_t st, ncclComm_t comm) {
     }                                \
   } while (0)
 
+// An ncclGroupStart ... ncclGroupEnd bracket whose end runs on every exit path (an error
+// inside the group still closes it).
+struct NcclGroup {
+  bool open = false;
+  ncclResult_t start() { const ncclResult_t r = ncclGroupStart(); open = r == ncclSuccess; return r; }
+  ncclResult_t end() { open = false; return ncclGroupEnd(); }
+  ~NcclGroup() { if (open) ncclGroupEnd(); }
+};
+
+// Small host-visible results land in pinned memory (a pageable destination would make
+// each cudaMemcpyAsync wait for the stream): one box per host thread, one call at a time.
+struct MgBox {
+  Plan plan;
+  int err;
+  uint32_t res[4];
+};
+MgBox* mg_box() {
+  struct Holder {
+    MgBox* pinned = nullptr;
+    MgBox pageable{};
+    bool tried = false;
+    ~Holder() { if (pinned) cudaFreeHost(pinned); }
+  };
+  static thread_local Holder h;
+  if (!h.tried) {
+    h.tried = true;
+    if (cudaHostAlloc((void**)&h.pinned, sizeof(MgBox), cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      h.pinned = nullptr;
+    }
+  }
+  return h.pinned ? h.pinned : &h.pageable;
+}
+
+// ----------------------------------------------------------------------------- peer window (N4)
+// One window of device memory per communicator and rank (cudaMalloc, so it can be shared by
+// CUDA IPC), mapped by every rank: peers read its kn slice and segment slots and write its
+// receive arrays.  Cached between calls, re-created (collectively) when a call needs more;
+// released by pbit_mg_comm_destroy / _abort.  Ranks in the same process (the multi-rank
+// test harness) use each other's pointers directly.
+struct PeerWin {
+  int G = 0;
+  char* local = nullptr;
+  size_t bytes = 0;
+  char* peer[64] = {};
+  bool mapped[64] = {};
+};
+std::mutex g_win_mu;
+std::map<void*, PeerWin> g_wins;
+
+void win_release(PeerWin& w) {
+  for (int q = 0; q < 64; ++q) {
+    if (w.mapped[q] && w.peer[q]) cudaIpcCloseMemHandle(w.peer[q]);
+    w.peer[q] = nullptr;
+    w.mapped[q] = false;
+  }
+  if (w.local) cudaFree(w.local);
+  cudaGetLastError();
+  w.local = nullptr;
+  w.bytes = 0;
+  w.G = 0;
+}
+
+struct IpcRec {
+  cudaIpcMemHandle_t h;
+  uint64_t ptr, pid, host;
+  int32_t ok, pad;
+};
+
+uint64_t host_key() {
+  char name[256] = {};
+  gethostname(name, sizeof name - 1);
+  uint64_t h = 1469598103934665603ull;
+  for (const char* c = name; *c; ++c) h = (h ^ (uint8_t)*c) * 1099511628211ull;
+  return h;
+}
+
+// Every rank returns the same verdict: PBIT_OK with the window mapped everywhere, or
+// PBIT_ERR_UNSUPPORTED (some rank could not allocate, export or map) -- the caller then
+// takes the NCCL transport.
+int peer_window(ncclComm_t comm, int G, int r, size_t need, cudaStream_t st, PeerWin** out) {
+  PeerWin* wp;
+  {  // the map lock covers the lookup only: the collectives below must not hold it (ranks
+     // of one process -- the test harness -- would wait for each other in them)
+    std::lock_guard<std::mutex> lk(g_win_mu);
+    wp = &g_wins[(void*)comm];  // std::map references stay valid; one thread per communicator
+  }
+  PeerWin& w = *wp;
+  *out = &w;
+  if (w.local && w.G == G && w.bytes >= need) return PBIT_OK;  // the same on every rank (same calls)
+  win_release(w);
+  int ok = 1;
+  IpcRec me{};
+  if (cudaMalloc((void**)&w.local, need) != cudaSuccess) { cudaGetLastError(); w.local = nullptr; ok = 0; }
+  if (ok && cudaIpcGetMemHandle(&me.h, w.local) != cudaSuccess) { cudaGetLastError(); ok = 0; }
+  me.ptr = (uint64_t)(uintptr_t)w.local;
+  me.pid = (uint64_t)getpid();
+  me.host = host_key();
+  me.ok = ok;
+  std::vector<IpcRec> all(G);
+  char* d = nullptr;
+  int rc = PBIT_OK;
+  if (ws_alloc((void**)&d, sizeof(IpcRec) * (G + 1) + 64, st) != cudaSuccess) {
+    cudaGetLastError();
+    win_release(w);
+    return PBIT_ERR_OOM;
+  }
+  int* d_ok = (int*)(d + sizeof(IpcRec) * (G + 1));
+  int* h_ok = &mg_box()->err;
+  if (cudaMemcpyAsync(d + sizeof(IpcRec) * G, &me, sizeof me, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+      ncclAllGather(d + sizeof(IpcRec) * G, d, sizeof(IpcRec), ncclUint8, comm, st) != ncclSuccess ||
+      cudaMemcpyAsync(all.data(), d, sizeof(IpcRec) * G, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    rc = PBIT_ERR_NCCL;
+  if (!rc) rc = mg_wait(st, comm);
+  if (!rc) {
+    for (int q = 0; q < G && ok; ++q) {
+      if (q == r) { w.peer[q] = w.local; continue; }
+      if (!all[q].ok) { ok = 0; break; }
+      if (all[q].pid == me.pid && all[q].host == me.host) {  // same process: the pointer is valid here
+        w.peer[q] = (char*)(uintptr_t)all[q].ptr;
+      } else if (cudaIpcOpenMemHandle((void**)&w.peer[q], all[q].h, cudaIpcMemLazyEnablePeerAccess) == cudaSuccess) {
+        w.mapped[q] = true;
+      } else {
+        cudaGetLastError();
+        w.peer[q] = nullptr;
+        ok = 0;
+      }
+    }
+    // every rank must have mapped every window: agree (min) before anyone relies on it
+    *h_ok = 0;
+    if (cudaMemcpyAsync(d_ok, &ok, sizeof ok, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        ncclAllReduce(d_ok, d_ok + 1, 1, ncclInt32, ncclMin, comm, st) != ncclSuccess ||
+        cudaMemcpyAsync(h_ok, d_ok + 1, sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      rc = PBIT_ERR_NCCL;
+    if (!rc) rc = mg_wait(st, comm);
+  }
+  cudaFreeAsync(d, st);
+  if (rc) { win_release(w); return rc; }
+  if (!*h_ok) { win_release(w); return PBIT_ERR_UNSUPPORTED; }
+  w.G = G;
+  w.bytes = need;
+  return PBIT_OK;
+}
+
+enum Transport { T_PEER = 0, T_NCCL = 1 };
+
+// PBIT_MG_TRANSPORT=nccl|peer (default: peer where the ranks can map each other)
+int transport_request() {
+  static const int v = [] {
+    const char* e = getenv("PBIT_MG_TRANSPORT");
+    return e && !strcmp(e, "nccl") ? (int)T_NCCL : (int)T_PEER;
+  }();
+  return v;
+}
+
+// pbit_sort_list_mg's own status for "the per-rank dynamic ruler table overflowed" (a list
+// whose rulers leave some rank far more nodes to walk than it owns): the call is redone
+// with the NCCL transport, whose walk does not cut segments.
+constexpr int RC_DYN_OVERFLOW = 100;
+
 template <int KB>
 int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint32_t n, uint32_t S,
            uint32_t n_local, int K, KeyMap km, uint32_t* out_head, uint32_t* out_next_local,
            uint32_t* out_prev_local, bool with_prev, ncclComm_t comm, int G, int r, cudaStream_t st,
-           uint32_t* launches_out) {
+           int transport, uint32_t* launches_out) {
   using RT = typename Rec<KB>::T;
-  uint32_t launches = 0;
   using KeyT = typename KeyOf<KB>::T;
   constexpr int REC_WORDS = sizeof(RT) / 4;
   const ncclDataType_t key_t = KB == 8 ? ncclUint64 : ncclUint32;
+  const bool peer = transport == T_PEER;
+  uint32_t launches = 0;
   int rc = PBIT_OK;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -128,10 +304,9 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   make_plan(n, KB * 8, K, &p);
   // a rank's id slice must be a whole number of ruler blocks: S is a multiple of 64
   // (pbit_mg_slice), so the spacing is at most 64 here (make_plan picks 128 from 2^30)
-  if (p.s_log2 > 6) {
-    p.s_log2 = 6;
-    p.R = (uint32_t)(((uint64_t)n + 63) >> 6);
-  }
+  if (p.s_log2 > 6) p.s_log2 = 6;
+  p.R = (uint32_t)(((uint64_t)n + (1ull << p.s_log2) - 1) >> p.s_log2);
+  p.cap = 4u << p.s_log2;
   const int radix = 1 << K;
   const uint32_t s = 1u << p.s_log2;
   const uint32_t bpr = S / s;                      // ruler blocks per rank
@@ -139,15 +314,18 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     set_last_error("pbit_sort_list_mg", "ruler blocks do not tile the rank slices");
     return PBIT_ERR_UNSUPPORTED;
   }
-  const uint32_t Gs = (uint32_t)G * bpr;           // segment-table entries (+1: head ruler)
+  const uint32_t Gs = (uint32_t)G * bpr;           // static rulers (+1: the head's extra ruler)
+  const uint32_t cap = p.cap;
+  const uint32_t dcap = peer ? S / cap + 1 : 0u;   // dynamic rulers per rank (cut segments)
+  const uint32_t Rmax = Gs + 1 + (uint32_t)G * dcap;
   RulerSel sel{n, (uint32_t)p.s_log2, p.R};
   const bool head_is_ruler = sel.is_ruler(head);
   const uint32_t head_ruler = head_is_ruler ? (head >> p.s_log2) : Gs;
-  const bool own_head = head / S == (uint32_t)r;
+  const uint32_t head_owner = head / S;
+  const bool own_head = head_owner == (uint32_t)r;
   const uint32_t P0 = std::min<uint64_t>(n, (uint64_t)r * S), P1 = std::min<uint64_t>(n, (uint64_t)(r + 1) * S);
   const uint32_t m = P1 - P0;                      // sorted positions held by this rank
   const uint32_t lo = r * S;
-  const uint32_t Rmax = Gs + 1;
   RulerSel sub{Rmax, 4u, (Rmax + 15) >> 4};
   const bool hs = sub.is_ruler(head_ruler);
   const uint32_t nsub = sub.R + (hs ? 0u : 1u);
@@ -155,68 +333,105 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   const size_t tile = sweep_tile(KB * 8);
   const size_t ntiles = (S + tile - 1) / tile;
   const int D = p.D;
+  const uint32_t NS = (uint32_t)G - 1;             // splitters
+  const uint32_t NB = 2 * NS + 1;                  // splitter buckets
+  const int W = with_prev ? 3 : 2;                 // relink record words
+  const uint32_t n_static = p.R > r * bpr ? std::min(bpr, p.R - r * bpr) : 0u;
+  const uint32_t nslots = bpr + 1 + dcap;
 
-  // ---- workspace
+  // ---- the window (peer transport): [kn slice][segment slots][recv keys][recv ids]; the
+  // relink records a rank receives land in its slot area (dead by then)
+  const size_t a_kn = ((size_t)S * sizeof(RT) + 255) & ~(size_t)255;
+  const size_t a_slots = std::max(((size_t)nslots * cap * sizeof(RT) + 255) & ~(size_t)255,
+                                  ((size_t)S * 12 + 16 + 255) & ~(size_t)255);
+  const size_t a_rk = ((size_t)S * sizeof(KeyT) + 16 + 255) & ~(size_t)255;
+  const size_t a_ri = ((size_t)S * 4 + 16 + 255) & ~(size_t)255;
+  PeerWin* win = nullptr;
+  if (peer) {
+    if (int e = peer_window(comm, G, r, a_kn + a_slots + a_rk + a_ri, st, &win)) return e;
+  }
+  auto wk = [&](int q, size_t off) -> char* { return win->peer[q] + off; };
+
+  // ---- workspace (the library's pool)
   Bump b;
-  RT* kn = nullptr; uint2* seg = nullptr; uint32_t *dist = nullptr, *seg_ord = nullptr, *seg_pos = nullptr;
-  uint32_t* part_first = nullptr; unsigned long long* sdist[2] = {}; uint32_t* scnt[2] = {}; uint32_t* ssucc[2] = {};
-  KeyT* kbuf[2] = {}; uint32_t* ibuf[2] = {}; unsigned long long* status = nullptr;
-  uint2 *send_p = nullptr, *pr[2] = {};
-  uint32_t *hist_l = nullptr, *hist_g = nullptr, *hist_a = nullptr, *hist_b = nullptr, *bases_p = nullptr,
-           *bases_l = nullptr, *cursors = nullptr, *cntmat = nullptr, *firsts = nullptr, *cnt = nullptr,
-           *offs = nullptr, *fill = nullptr, *cntall = nullptr, *tile_ctr = nullptr, *nseg = nullptr,
-           *zero = nullptr, *tile_first_unused = nullptr, *mg_c = nullptr, *mg_call = nullptr;
-  unsigned long long* mg_q = nullptr;
-  Plan *plan_g = nullptr, *plan_p = nullptr, *plan_l = nullptr;
+  RT* kn_rep = nullptr; uint2* seg = nullptr; uint32_t *dist = nullptr, *seg_ord = nullptr, *seg_pos = nullptr;
+  unsigned long long* sdist[2] = {}; uint32_t* scnt[2] = {}; uint32_t* ssucc[2] = {};
+  KeyT *keys_c = nullptr, *kb1 = nullptr, *recv_k = nullptr, *send_k = nullptr;
+  uint32_t *ids_c = nullptr, *ib1 = nullptr, *recv_i = nullptr, *send_i = nullptr;
+  unsigned long long* status = nullptr;
+  void *rbuf0 = nullptr, *rbuf1 = nullptr, *psend = nullptr, *precvb = nullptr;
+  RT* slots_own = nullptr;
+  // control block (zeroed per call)
+  uint32_t *hist_l = nullptr, *hist_g = nullptr, *bases_g = nullptr, *hist_r = nullptr, *bases_r = nullptr,
+           *part_first = nullptr, *tile_ctr = nullptr, *nseg = nullptr, *zero = nullptr, *dyn_count = nullptr,
+           *shist = nullptr, *bcnt = nullptr, *cntall_b = nullptr, *sbases = nullptr, *srecv = nullptr,
+           *fl = nullptr, *fl_all = nullptr, *edges = nullptr, *pcnt = nullptr, *pcntall = nullptr,
+           *pbase = nullptr, *psbase = nullptr, *precv = nullptr, *pfill = nullptr, *cursors = nullptr,
+           *barrier_w = nullptr;
+  unsigned long long* below = nullptr;
+  Plan *plan_g = nullptr, *plan_r = nullptr;
+  SplitTable* split = nullptr;
   int* err = nullptr;
   size_t ctl_off = 0, ctl_end = 0;
-  std::vector<uint32_t> h_counts, h_cntall;
-  Plan h_plan{};
-  int h_err = 0;
-  uint32_t h_firsts[130];  // first and last sorted id of every rank
   auto carve = [&]() {
-    kn = b.take<RT>((size_t)G * S);
+    if (!peer) kn_rep = b.take<RT>((size_t)G * S);
     seg = b.take<uint2>(Rmax);
     dist = b.take<uint32_t>(Rmax);
     seg_ord = b.take<uint32_t>(Rmax);
     seg_pos = b.take<uint32_t>(Rmax);
-    tile_first_unused = b.take<uint32_t>(1);
     for (int i = 0; i < 2; ++i) {
       sdist[i] = b.take<unsigned long long>(nsub + 1);
       scnt[i] = b.take<uint32_t>(nsub + 1);
       ssucc[i] = b.take<uint32_t>(nsub + 1);
-      kbuf[i] = b.take<KeyT>(S);
-      ibuf[i] = b.take<uint32_t>(S);
-      pr[i] = b.take<uint2>(S);
+    }
+    keys_c = b.take<KeyT>(S);
+    ids_c = b.take<uint32_t>(S);
+    kb1 = b.take<KeyT>(S);
+    ib1 = b.take<uint32_t>(S);
+    if (!peer) {
+      recv_k = b.take<KeyT>(S);
+      recv_i = b.take<uint32_t>(S);
+      send_k = b.take<KeyT>(S);
+      send_i = b.take<uint32_t>(S);
+      psend = b.take<uint32_t>((size_t)S * W);
+      precvb = b.take<uint32_t>((size_t)S * W);
     }
     status = b.take<unsigned long long>(ntiles * 256);
-    send_p = b.take<uint2>(S);
+    rbuf0 = b.take<uint32_t>((size_t)S * W);
+    rbuf1 = b.take<uint32_t>((size_t)S * W);
     ctl_off = b.off;
-    part_first = b.take<uint32_t>(G + 2);  // zeroed with the control block
     hist_l = b.take<uint32_t>((size_t)D * radix);
     hist_g = b.take<uint32_t>((size_t)D * radix);
-    hist_a = b.take<uint32_t>((size_t)D * radix);
-    hist_b = b.take<uint32_t>((size_t)D * radix);
-    bases_p = b.take<uint32_t>((size_t)D * radix);
-    bases_l = b.take<uint32_t>((size_t)D * radix);
-    cursors = b.take<uint32_t>(relink_cursor_words(S));
-    cntmat = b.take<uint32_t>((size_t)G * radix);
-    firsts = b.take<uint32_t>(2 * G + 2);
-    cnt = b.take<uint32_t>(G);
-    offs = b.take<uint32_t>(G);
-    fill = b.take<uint32_t>(G);
-    cntall = b.take<uint32_t>((size_t)G * G);
+    bases_g = b.take<uint32_t>((size_t)D * radix);
+    hist_r = b.take<uint32_t>((size_t)D * radix);
+    bases_r = b.take<uint32_t>((size_t)D * radix);
+    part_first = b.take<uint32_t>(G + 2);
     tile_ctr = b.take<uint32_t>(80);
     nseg = b.take<uint32_t>(1);
     zero = b.take<uint32_t>(1);
+    dyn_count = b.take<uint32_t>(1);
+    shist = b.take<uint32_t>(64 * 256);
+    below = b.take<unsigned long long>(64);
+    bcnt = b.take<uint32_t>(128);
+    cntall_b = b.take<uint32_t>((size_t)G * 128);
+    sbases = b.take<uint32_t>(128);
+    srecv = b.take<uint32_t>(2 * 64);
+    fl = b.take<uint32_t>(2);
+    fl_all = b.take<uint32_t>(2 * 64);
+    edges = b.take<uint32_t>(4);
+    pcnt = b.take<uint32_t>(64);
+    pcntall = b.take<uint32_t>(64 * 64);
+    pbase = b.take<uint32_t>(64);
+    psbase = b.take<uint32_t>(64);
+    precv = b.take<uint32_t>(2 * 64);
+    pfill = b.take<uint32_t>(64);
+    cursors = b.take<uint32_t>(relink_cursor_words(S));
+    barrier_w = b.take<uint32_t>(2);
     plan_g = b.take<Plan>(1);
-    plan_p = b.take<Plan>(1);
-    plan_l = b.take<Plan>(1);
+    plan_r = b.take<Plan>(1);
+    split = b.take<SplitTable>(1);
     err = b.take<int>(1);
     ctl_end = b.off;
-    mg_q = b.take<unsigned long long>((size_t)64 * 256);
-    mg_c = b.take<uint32_t>((size_t)64 * 256);
-    mg_call = b.take<uint32_t>((size_t)2 * 64 * 64);
   };
   carve();
   const size_t bytes = b.off;
@@ -224,36 +439,81 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   if (ws_alloc((void**)&base, bytes, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   b = Bump{base, 0};
   carve();
+  if (peer) {
+    slots_own = (RT*)(win->local + a_kn);
+    recv_k = (KeyT*)(win->local + a_kn + a_slots);
+    recv_i = (uint32_t*)(win->local + a_kn + a_slots + a_rk);
+  }
 
+  // host-side state (declared before the first goto)
+  MgBox* hb = mg_box();
+  const Plan& h_plan = hb->plan;
+  uint32_t h_left[66] = {}, h_srecv[128] = {}, h_prow[64] = {}, h_psbase[64] = {}, h_precv[128] = {};
+  SplitTable h_split{};
+  cudaEvent_t plan_ev = nullptr;
+  const KeyT* rk = nullptr;
+  const uint32_t* ri = nullptr;
+  const uint32_t* fin = nullptr;
   {
     CUDACHK(cudaMemsetAsync(base + ctl_off, 0, ctl_end - ctl_off, st));
     CUDACHK(cudaMemsetAsync(seg, 0, sizeof(uint2) * Rmax, st));
     CUDACHK(cudaMemsetAsync(status, 0, ntiles * 256 * 8, st));
 
-    // ---- 1. pack the own slice into its place of the replica; local histograms
-    if (n_local) {
-      const int blocks = full_wave(k_pack<KB>, PACK_THREADS, (size_t)D * radix * 4, sms,
-                                   (n_local + PACK_THREADS - 1) / PACK_THREADS);
-      ++launches;
-      k_pack<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys_local, next_local, n_local, n,
-                                                                       kn + lo, hist_l, K, D, err, km);
-    }
-    NCCLCHK(ncclAllGather(kn + lo, kn, (size_t)S * REC_WORDS, ncclUint32, comm, st));
-    NCCLCHK(ncclAllReduce(hist_l, hist_g, (size_t)D * radix, ncclUint32, ncclSum, comm, st));
-
-    // ---- 2. count-walk the own rulers, share the segment table
+    // ---- 1. pack the own slice; histograms of every digit of every key
     {
+      RT* kn_own = peer ? (RT*)win->local : kn_rep + lo;
+      if (n_local) {
+        const int blocks = full_wave(k_pack<KB>, PACK_THREADS, (size_t)D * radix * 4, sms,
+                                     (n_local + PACK_THREADS - 1) / PACK_THREADS);
+        ++launches;
+        k_pack<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys_local, next_local, n_local, n, kn_own,
+                                                                         hist_l, K, D, err, km);
+      }
+      if (!peer) NCCLCHK(ncclAllGather(kn_rep + lo, kn_rep, (size_t)S * REC_WORDS, ncclUint32, comm, st));
+      NCCLCHK(ncclAllReduce(hist_l, hist_g, (size_t)D * radix, ncclUint32, ncclSum, comm, st));
+      // the global pass plan (a digit trivial globally is trivial on every rank): read by
+      // the host while the walk, the ranking and the exchange run
+      ++launches;
+      k_plan<<<1, 256, 0, st>>>(hist_g, bases_g, plan_g, D, K, n, err);
+      CUDACHK(cudaMemcpyAsync(&hb->plan, plan_g, sizeof(Plan), cudaMemcpyDeviceToHost, st));
+      CUDACHK(cudaEventCreateWithFlags(&plan_ev, cudaEventDisableTiming));
+      CUDACHK(cudaEventRecord(plan_ev, st));
+    }
+
+    // ---- 2. walk the own rulers; share the segment table
+    if (peer) {
+      KnSrc<RT> src{};
+      for (int q = 0; q < G; ++q) src.peer[q] = (const RT*)wk(q, 0);
+      src.S = FastDiv::make(S);
+      const WalkMap wm{r * bpr, n_static, own_head && !head_is_ruler ? Gs : PBIT_NULL32, Gs + 1 + (uint32_t)r * dcap,
+                       bpr + 1};
+      const uint32_t total = wm.count();
+      if (total) {
+        static const int occ = [] {
+          int o = 0;
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_walk<KB, true>, WALK_THREADS, 0);
+          return std::max(o, 1);
+        }();
+        int blocks = sms * occ;
+        if ((uint32_t)blocks * 4 > total) blocks = std::max(1u, (total + 3) / 4);
+        const uint32_t per = (total + blocks - 1) / blocks;
+        ++launches;
+        k_walk<KB, true><<<blocks, WALK_THREADS, 0, st>>>(src, sel, wm, head, slots_own, cap, seg, dyn_count, dcap,
+                                                          per, err, 0);
+      }
+    } else {
       const uint32_t b_lo = r * bpr, b_hi = (r + 1) * bpr;
       const uint32_t total = bpr + (own_head && !head_is_ruler ? 1u : 0u);
       int blocks = sms * (2048 / WALK_THREADS);
       if ((uint32_t)blocks * 4 > total) blocks = std::max(1u, (total + 3) / 4);
       const uint32_t per = (total + blocks - 1) / blocks;
       ++launches;
-      k_walk_count<KB><<<blocks, WALK_THREADS, 0, st>>>(kn, sel, b_lo, b_hi,
+      k_walk_count<KB><<<blocks, WALK_THREADS, 0, st>>>(kn_rep, sel, b_lo, b_hi,
                                                         own_head && !head_is_ruler ? Gs : PBIT_NULL32, head, seg, per,
                                                         err);
     }
     NCCLCHK(ncclAllGather(seg + (size_t)r * bpr, seg, (size_t)bpr * 2, ncclUint32, comm, st));
+    if (dcap) NCCLCHK(ncclAllGather(seg + Gs + 1 + (size_t)r * dcap, seg + Gs + 1, (size_t)dcap * 2, ncclUint32, comm, st));
     NCCLCHK(ncclAllReduce(seg + Gs, seg + Gs, 2, ncclUint32, ncclMax, comm, st));
     NCCLCHK(ncclAllReduce(err, err, 1, ncclInt32, ncclMax, comm, st));
 
@@ -279,205 +539,189 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       k_rank_walk_b<<<sblocks, 256, 0, st>>>(seg, sub, Rmax, zero, 0, head_ruler, nsub, head_sub, sdist[cur],
                                              scnt[cur], dist, seg_ord, seg_pos, part_first, S, n, nseg, err);
     }
-    ++launches;
-    k_plan<<<1, 256, 0, st>>>(hist_g, bases_l, plan_g, D, K, n, err);
-    CUDACHK(cudaMemcpyAsync(&h_plan, plan_g, sizeof(Plan), cudaMemcpyDeviceToHost, st));
-    CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
-    MGWAIT();
-    if (h_err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
 
-    // ---- 4. emit the list-order chunk of positions [P0, P1)
+    // ---- 4. the list-order chunk of positions [P0, P1)
     if (m) {
-      const int blocks = std::max(1, std::min((int)((Gs / G + 2 + 255) / 256), sms * 8));
+      const int blocks = std::max(1, std::min((int)((m / 64 + 2 + 255) / 256), sms * 8));
       ++launches;
-      k_emit_walk<KB><<<blocks, 256, 0, st>>>(kn, sel, head, seg, seg_ord, seg_pos, part_first, r, nseg, P0, P1,
-                                              kbuf[0], ibuf[0], err);
-    }
-
-    const Plan* final_plan = plan_l;  // parity of the final ids: fin[npasses & 1]
-    uint32_t* fin[2] = {ibuf[0], ibuf[1]};
-    if (h_plan.npasses == 0) {
-      // every digit trivial: all keys equal, the list order is the sorted order
-      CUDACHK(cudaMemsetAsync(plan_l, 0, sizeof(Plan), st));
-    } else {
-      // ---- 5a. stable local sort of the chunk (kbuf[0], ibuf[0]) by the full key
-      SweepArgs pa{};
-      pa.kin[0] = kbuf[0]; pa.kin[1] = kbuf[1]; pa.vin[0] = ibuf[0]; pa.vin[1] = ibuf[1];
-      pa.kout[0] = kbuf[0]; pa.kout[1] = kbuf[1]; pa.vout[0] = ibuf[0]; pa.vout[1] = ibuf[1];
-      pa.bases = bases_p; pa.status = status; pa.tile_ctr = tile_ctr; pa.err = err; pa.n = m;
-      // keep_keys below: the sorted keys are needed for the splitters and the exchange
-      if (m) {
-        ++launches;
-        k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
-            kbuf[0], m, K, D, hist_a, err);
-      }
-      ++launches;
-      k_plan<<<1, 256, 0, st>>>(hist_a, bases_p, plan_p, D, K, m, err);
-      Plan h_pp{};
-      CUDACHK(cudaMemcpyAsync(&h_pp, plan_p, sizeof(Plan), cudaMemcpyDeviceToHost, st));
-      MGWAIT();
-      if (m) { launch_key_passes_k<KB>(K, pa, h_pp, true, st, nullptr, 0, SRC_TMA); launches += h_pp.npasses; }
-      const int pa_par = (int)(h_pp.npasses & 1u);  // sorted chunk in kbuf/ibuf[pa_par]
-      const KeyT* sk = kbuf[pa_par];
-
-      // ---- 5b. exact splitters of the final (key, list position) order: split s sits at
-      // global rank x_s = (s+1)*S.  Radix refinement from the top digit: per round, the
-      // global count of keys below each candidate (prefix, c) -- lower bounds in every
-      // rank's sorted chunk, summed by ncclAllReduce -- fixes one more digit of k*_s.
-      const int NS = G - 1;
-      std::vector<unsigned long long> prefix(std::max(NS, 1), 0ull), h_q;
-      std::vector<uint32_t> h_cnt;
-      for (int i = D - 1; i >= 0 && NS > 0; --i) {
-        const int wbits = i == D - 1 ? KB * 8 - K * (D - 1) : K;
-        const int nc = 1 << wbits;
-        h_q.assign((size_t)NS * nc, 0ull);
-        for (int sp = 0; sp < NS; ++sp)
-          for (int c = 0; c < nc; ++c) h_q[(size_t)sp * nc + c] = ((prefix[sp] << wbits) | (unsigned long long)c) << (K * i);
-        CUDACHK(cudaMemcpyAsync(mg_q, h_q.data(), 8ull * NS * nc, cudaMemcpyHostToDevice, st));
-        ++launches;
-        k_count_below<KeyT><<<(NS * nc + 255) / 256, 256, 0, st>>>(sk, m, mg_q, NS * nc, 0, mg_c);
-        NCCLCHK(ncclAllReduce(mg_c, mg_c, (size_t)NS * nc, ncclUint32, ncclSum, comm, st));
-        h_cnt.resize((size_t)NS * nc);
-        CUDACHK(cudaMemcpyAsync(h_cnt.data(), mg_c, 4ull * NS * nc, cudaMemcpyDeviceToHost, st));
-        MGWAIT();
-        for (int sp = 0; sp < NS; ++sp) {
-          const uint64_t x = std::min<uint64_t>(n, (uint64_t)(sp + 1) * S);
-          int pick = 0;  // the largest candidate with (global count below it) <= x
-          for (int c = 0; c < nc; ++c)
-            if (h_cnt[(size_t)sp * nc + c] <= x) pick = c;
-          prefix[sp] = (prefix[sp] << wbits) | (unsigned long long)pick;
-        }
-      }
-      // ---- 5c. per-rank counts below / up to each splitter key; the exchange plan
-      std::vector<uint64_t> soff(G), scount(G), roff(G), rcount(G);
-      {
-        std::vector<uint64_t> h_lt((size_t)G * std::max(NS, 1)), h_le((size_t)G * std::max(NS, 1));
-        if (NS > 0) {
-          CUDACHK(cudaMemcpyAsync(mg_q, prefix.data(), 8ull * NS, cudaMemcpyHostToDevice, st));
-          ++launches;
-          k_count_below<KeyT><<<1, 64, 0, st>>>(sk, m, mg_q, NS, 0, mg_c);
-          ++launches;
-          k_count_below<KeyT><<<1, 64, 0, st>>>(sk, m, mg_q, NS, 1, mg_c + NS);
-          NCCLCHK(ncclAllGather(mg_c, mg_call, (size_t)2 * NS, ncclUint32, comm, st));
-          h_cnt.resize((size_t)2 * NS * G);
-          CUDACHK(cudaMemcpyAsync(h_cnt.data(), mg_call, 8ull * NS * G, cudaMemcpyDeviceToHost, st));
-          MGWAIT();
-          for (int q = 0; q < G; ++q)
-            for (int sp = 0; sp < NS; ++sp) {
-              h_lt[(size_t)q * NS + sp] = h_cnt[(size_t)q * 2 * NS + sp];
-              h_le[(size_t)q * NS + sp] = h_cnt[(size_t)q * 2 * NS + NS + sp];
-            }
-        }
-        pbit_mg_exchange_plan(G, r, n, S, h_lt.data(), h_le.data(), soff.data(), scount.data(), roff.data(),
-                              rcount.data());
-      }
-      uint64_t racc = 0;
-      for (int d = 0; d < G; ++d) racc += rcount[d];
-      if (racc != m) { set_last_error("pbit_sort_list_mg", "exchange size mismatch"); rc = PBIT_ERR_CUDA; goto done; }
-      // ---- 5d. exchange sorted ranges; receive in source-rank order into the other buffer
-      const int pb = pa_par ^ 1;
-      NCCLCHK(ncclGroupStart());
-      for (int d = 0; d < G; ++d) {
-        if (scount[d]) {
-          NCCLCHK(ncclSend(kbuf[pa_par] + soff[d], scount[d], key_t, d, comm, st));
-          NCCLCHK(ncclSend(ibuf[pa_par] + soff[d], scount[d], ncclUint32, d, comm, st));
-        }
-        if (rcount[d]) {
-          NCCLCHK(ncclRecv(kbuf[pb] + roff[d], rcount[d], key_t, d, comm, st));
-          NCCLCHK(ncclRecv(ibuf[pb] + roff[d], rcount[d], ncclUint32, d, comm, st));
-        }
-      }
-      NCCLCHK(ncclGroupEnd());
-
-      // ---- 6. stable sort of the received runs (source order = list-position order for
-      // equal keys), buffers swapped so the passes start from buffer pb
-      CUDACHK(cudaMemsetAsync(status, 0, ntiles * 256 * 8, st));
-      CUDACHK(cudaMemsetAsync(tile_ctr, 0, 80 * 4, st));
-      CUDACHK(cudaMemsetAsync(hist_b, 0, 4ull * D * radix, st));
-      if (m) {
-        ++launches;
-        k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
-            kbuf[pb], m, K, D, hist_b, err);
-      }
-      ++launches;
-      k_plan<<<1, 256, 0, st>>>(hist_b, bases_l, plan_l, D, K, m, err);
-      Plan h_pl{};
-      CUDACHK(cudaMemcpyAsync(&h_pl, plan_l, sizeof(Plan), cudaMemcpyDeviceToHost, st));
-      MGWAIT();
-      SweepArgs la = pa;
-      la.kin[0] = kbuf[pb]; la.kin[1] = kbuf[pb ^ 1]; la.vin[0] = ibuf[pb]; la.vin[1] = ibuf[pb ^ 1];
-      la.kout[0] = kbuf[pb]; la.kout[1] = kbuf[pb ^ 1]; la.vout[0] = ibuf[pb]; la.vout[1] = ibuf[pb ^ 1];
-      la.bases = bases_l;
-      if (m) { launch_key_passes_k<KB>(K, la, h_pl, false, st, nullptr, 0, SRC_TMA); launches += h_pl.npasses; }
-      fin[0] = ibuf[pb];
-      fin[1] = ibuf[pb ^ 1];
-    }
-
-    // ---- 7. stitch and relink: every rank's first and last sorted id (all-gather), then
-    // (v, successor) -- and, for out_prev, (v, predecessor) -- routed to the owner of v
-    ++launches;
-    k_first_last_id<<<1, 1, 0, st>>>(final_plan, fin[0], fin[1], m, firsts + 2 * G);
-    NCCLCHK(ncclAllGather(firsts + 2 * G, firsts, 2, ncclUint32, comm, st));
-    CUDACHK(cudaMemcpyAsync(h_firsts, firsts, 8ull * G, cudaMemcpyDeviceToHost, st));
-    MGWAIT();
-    for (int dir = 1; dir >= -1; dir -= 2) {
-      // with_prev is the same on every rank (agreed before the first collective): a rank
-      // without own nodes still routes its share of the (v, pred) pairs
-      if (dir < 0 && !with_prev) continue;
-      uint32_t* out_local = dir > 0 ? out_next_local : out_prev_local;
-      uint32_t edge = PBIT_NULL32;  // next rank's first id / previous rank's last id
-      if (dir > 0) {
-        for (int d = r + 1; d < G; ++d)
-          if (h_firsts[2 * d] != PBIT_NULL32) { edge = h_firsts[2 * d]; break; }
+      if (peer) {
+        PeerSlots ps{};
+        for (int q = 0; q < G; ++q) ps.slots[q] = wk(q, a_kn);
+        MgRulers mr{FastDiv::make(bpr), FastDiv::make(std::max(dcap, 2u)), Gs, p.R, head_owner};
+        k_mg_gather<KB><<<blocks, 256, 0, st>>>(ps, mr, cap, seg, seg_ord, seg_pos, part_first, r, nseg, P0, P1,
+                                                keys_c, ids_c, err);
       } else {
-        for (int d = r - 1; d >= 0; --d)
-          if (h_firsts[2 * d + 1] != PBIT_NULL32) { edge = h_firsts[2 * d + 1]; break; }
-      }
-      CUDACHK(cudaMemsetAsync(cnt, 0, 4ull * G, st));
-      CUDACHK(cudaMemsetAsync(fill, 0, 4ull * G, st));
-      const int pblocks = std::max(1, std::min((int)((m + 4095) / 4096), sms * 4));
-      if (m) {
-        ++launches;
-        k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, edge, dir, S, G, cnt, nullptr,
-                                               nullptr, nullptr, 0, err);
-      }
-      NCCLCHK(ncclAllGather(cnt, cntall, G, ncclUint32, comm, st));
-      h_cntall.resize((size_t)G * G);
-      CUDACHK(cudaMemcpyAsync(h_cntall.data(), cntall, 4ull * G * G, cudaMemcpyDeviceToHost, st));
-      MGWAIT();
-      std::vector<uint32_t> h_offs(G);
-      uint32_t acc = 0;
-      for (int d = 0; d < G; ++d) { h_offs[d] = acc; acc += h_cntall[(size_t)r * G + d]; }
-      CUDACHK(cudaMemcpyAsync(offs, h_offs.data(), 4ull * G, cudaMemcpyHostToDevice, st));
-      if (m) {
-        ++launches;
-        k_pairs_owner<<<pblocks, 256, 0, st>>>(final_plan, fin[0], fin[1], m, edge, dir, S, G, nullptr, offs, fill,
-                                               send_p, 1, err);
-      }
-      uint32_t racc = 0;
-      NCCLCHK(ncclGroupStart());
-      for (int d = 0; d < G; ++d) {
-        const uint32_t sc = h_cntall[(size_t)r * G + d], rcn = h_cntall[(size_t)d * G + r];
-        if (sc) NCCLCHK(ncclSend(send_p + h_offs[d], 2ull * sc, ncclUint32, d, comm, st));
-        if (rcn) NCCLCHK(ncclRecv(pr[1] + racc, 2ull * rcn, ncclUint32, d, comm, st));
-        racc += rcn;
-      }
-      NCCLCHK(ncclGroupEnd());
-      if (racc != n_local) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
-      // the received pairs (global v): out[v - lo] = w for every own id v, in any order
-      if (n_local) {
-        CUDACHK(cudaMemsetAsync(cursors, 0, relink_cursor_words(S) * 4, st));
-        launches += launch_relink(nullptr, pr[1], lo, n_local, pr[0], pr[1], cursors, out_local, err, st, sms);
+        k_emit_walk<KB><<<blocks, 256, 0, st>>>(kn_rep, sel, head, seg, seg_ord, seg_pos, part_first, r, nseg, P0, P1,
+                                                keys_c, ids_c, err);
       }
     }
-    CUDACHK(cudaMemcpyAsync(&h_err, err, 4, cudaMemcpyDeviceToHost, st));
+
+    if (G > 1) {
+      // ---- 5. splitters, bucket counts, exchange plan -- all on the device
+      h_split.G = (uint32_t)G;
+      h_split.NS = NS;
+      for (int d = 0; d < G; ++d) {
+        h_split.dst_k[d] = peer ? (void*)wk(d, a_kn + a_slots) : (void*)send_k;
+        h_split.dst_i[d] = peer ? (uint32_t*)wk(d, a_kn + a_slots + a_rk) : send_i;
+      }
+      CUDACHK(cudaMemcpyAsync(split, &h_split, sizeof h_split, cudaMemcpyHostToDevice, st));
+      const int rounds = KB;  // 8 bits per round
+      const int cblocks = std::max(1, std::min((int)((m + 255) / 256), sms * 2));
+      static std::atomic<unsigned long long> attr{0};
+      once_per_device(attr, [] {
+        cudaFuncSetAttribute(k_split_count<KeyT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 256 * 4);
+      });
+      for (int i = rounds - 1; i >= 0; --i) {
+        if (m) {
+          ++launches;
+          k_split_count<KeyT><<<cblocks, 256, NS * 256 * 4, st>>>(keys_c, m, NS, split->kstar, 8 * i, shist, err);
+        }
+        NCCLCHK(ncclAllReduce(shist, shist, (size_t)NS * 256, ncclUint32, ncclSum, comm, st));
+        ++launches;
+        k_split_select<<<1, 64, 0, st>>>(shist, NS, n, S, split->kstar, below);
+      }
+      if (m) {
+        ++launches;
+        k_split_buckets<KeyT><<<cblocks, 256, 0, st>>>(keys_c, m, split, bcnt, err);
+      }
+      NCCLCHK(ncclAllGather(bcnt, cntall_b, NB, ncclUint32, comm, st));
+      ++launches;
+      k_split_plan<<<1, 32, 0, st>>>(cntall_b, (uint32_t)G, (uint32_t)r, n, S, split, sbases, srecv);
+      if (!peer) {  // the NCCL transport scatters into the local send buffer in bucket order
+        CUDACHK(cudaMemsetAsync(split->dst_off, 0, sizeof(uint32_t) * 64, st));
+        CUDACHK(cudaMemcpyAsync(h_left, split->left, sizeof(uint32_t) * (G + 1), cudaMemcpyDeviceToHost, st));
+        CUDACHK(cudaMemcpyAsync(h_srecv, srecv, sizeof(uint32_t) * 2 * G, cudaMemcpyDeviceToHost, st));
+      }
+
+      // ---- 6. one stable partition pass by splitter bucket, scattered to the destinations
+      if (m) {
+        SweepArgs sa{};
+        sa.kin[0] = keys_c; sa.vin[0] = ids_c;
+        sa.bases = sbases; sa.status = status; sa.tile_ctr = tile_ctr; sa.err = err; sa.n = m;
+        sa.slot = 79;  // its own ticket counter and lookback epoch (the sort passes use 0..)
+        sa.digit = 0; sa.src = 0; sa.last = 0; sa.split = split;
+        constexpr int IPT = (KB == 8) ? SWEEP_IPT64 : SWEEP_IPT32;
+        ++launches;
+        launch_one<KeyT, 7, IPT, SRC_SPLIT>(sa, st, rank_mode());
+      }
+      if (peer) {
+        // every rank's partition has landed before anyone reads its receive arrays
+        NCCLCHK(ncclAllReduce(barrier_w, barrier_w + 1, 1, ncclUint32, ncclSum, comm, st));
+      } else {
+        MGWAIT();  // the host needs the send / receive ranges
+        NcclGroup grp;
+        NCCLCHK(grp.start());
+        for (int d = 0; d < G; ++d) {
+          const uint32_t sc = h_left[d + 1] - h_left[d], rcn = h_srecv[2 * d + 1];
+          if (sc) {
+            NCCLCHK(ncclSend(send_k + h_left[d], sc, key_t, d, comm, st));
+            NCCLCHK(ncclSend(send_i + h_left[d], sc, ncclUint32, d, comm, st));
+          }
+          if (rcn) {
+            NCCLCHK(ncclRecv(recv_k + h_srecv[2 * d], rcn, key_t, d, comm, st));
+            NCCLCHK(ncclRecv(recv_i + h_srecv[2 * d], rcn, ncclUint32, d, comm, st));
+          }
+        }
+        NCCLCHK(grp.end());
+      }
+      rk = recv_k;
+      ri = recv_i;
+    } else {
+      rk = keys_c;  // one rank: the chunk is the whole list
+      ri = ids_c;
+    }
+
+    // ---- 7. stable local sort of the received runs (the global plan's digits; the bases
+    // from the local histogram)
+    if (cudaEventSynchronize(plan_ev) != cudaSuccess) { rc = PBIT_ERR_CUDA; goto done; }
+    {
+      uint32_t* ri_w = const_cast<uint32_t*>(ri);
+      KeyT* rk_w = const_cast<KeyT*>(rk);
+      fin = ri;
+      const Plan hp = h_plan;
+      if (m && hp.npasses) {
+        ++launches;
+        k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
+            rk, m, K, D, hist_r, err);
+        ++launches;
+        k_plan<<<1, 256, 0, st>>>(hist_r, bases_r, plan_r, D, K, m, err);
+        SweepArgs la{};
+        la.kin[0] = rk_w; la.kin[1] = kb1; la.vin[0] = ri_w; la.vin[1] = ib1;
+        la.kout[0] = rk_w; la.kout[1] = kb1; la.vout[0] = ri_w; la.vout[1] = ib1;
+        la.bases = bases_r; la.status = status; la.tile_ctr = tile_ctr; la.err = err; la.n = m;
+        launch_key_passes_k<KB>(K, la, hp, false, st, nullptr, 0, SRC_TMA);
+        launches += hp.npasses;
+        fin = (hp.npasses & 1u) ? ib1 : ri;
+      }
+    }
+
+    // ---- 8. stitch and relink: every rank's first and last sorted id (all-gather), then
+    // (v, successor[, predecessor]) routed to the owner of v
+    ++launches;
+    k_first_last_id<<<1, 1, 0, st>>>(fin, m, fl);
+    NCCLCHK(ncclAllGather(fl, fl_all, 2, ncclUint32, comm, st));
+    ++launches;
+    k_edges<<<1, 1, 0, st>>>(fl_all, (uint32_t)G, (uint32_t)r, edges);
+    {
+      const int pblocks = std::max(1, std::min((int)((m + 4095) / 4096), sms * 4));
+      const FastDiv fS = FastDiv::make(S);
+      PairDst pd{};
+      if (m) {
+        ++launches;
+        if (W == 3) k_pairs_owner<3><<<pblocks, 256, 0, st>>>(fin, m, edges, fS, G, pcnt, nullptr, nullptr, pd, 0, err);
+        else k_pairs_owner<2><<<pblocks, 256, 0, st>>>(fin, m, edges, fS, G, pcnt, nullptr, nullptr, pd, 0, err);
+      }
+      NCCLCHK(ncclAllGather(pcnt, pcntall, G, ncclUint32, comm, st));
+      ++launches;
+      k_pairs_plan<<<1, 32, 0, st>>>(pcntall, (uint32_t)G, (uint32_t)r, pbase, psbase, precv);
+      void* recvrec = peer ? (void*)(win->local + a_kn) : precvb;
+      for (int d = 0; d < G; ++d) pd.dst[d] = peer ? (void*)wk(d, a_kn) : psend;
+      if (m) {
+        ++launches;
+        if (W == 3)
+          k_pairs_owner<3><<<pblocks, 256, 0, st>>>(fin, m, edges, fS, G, nullptr, peer ? pbase : psbase, pfill, pd, 1, err);
+        else
+          k_pairs_owner<2><<<pblocks, 256, 0, st>>>(fin, m, edges, fS, G, nullptr, peer ? pbase : psbase, pfill, pd, 1, err);
+      }
+      if (peer) {
+        NCCLCHK(ncclAllReduce(barrier_w, barrier_w + 1, 1, ncclUint32, ncclSum, comm, st));
+      } else {
+        CUDACHK(cudaMemcpyAsync(h_prow, pcntall + (size_t)r * G, 4ull * G, cudaMemcpyDeviceToHost, st));
+        CUDACHK(cudaMemcpyAsync(h_psbase, psbase, 4ull * G, cudaMemcpyDeviceToHost, st));
+        CUDACHK(cudaMemcpyAsync(h_precv, precv, 8ull * G, cudaMemcpyDeviceToHost, st));
+        MGWAIT();
+        uint64_t racc = 0;
+        for (int d = 0; d < G; ++d) racc += h_precv[2 * d + 1];
+        // the counts come from an all-gather, so every rank sees the same totals and takes
+        // the same branch here (no rank is left waiting in the exchange below)
+        if (racc != n_local) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
+        NcclGroup grp;
+        NCCLCHK(grp.start());
+        for (int d = 0; d < G; ++d) {
+          if (h_prow[d])
+            NCCLCHK(ncclSend((uint32_t*)psend + (size_t)W * h_psbase[d], (size_t)W * h_prow[d], ncclUint32, d, comm, st));
+          if (h_precv[2 * d + 1])
+            NCCLCHK(ncclRecv((uint32_t*)precvb + (size_t)W * h_precv[2 * d], (size_t)W * h_precv[2 * d + 1], ncclUint32,
+                             d, comm, st));
+        }
+        NCCLCHK(grp.end());
+      }
+      // the received records (global v): out[v - lo] = succ (and pred) for every own id v
+      if (n_local)
+        launches += launch_relink(nullptr, recvrec, lo, n_local, rbuf0, rbuf1, cursors, out_next_local,
+                                  with_prev ? out_prev_local : nullptr, err, st, sms);
+    }
+    CUDACHK(cudaMemcpyAsync(&hb->err, err, 4, cudaMemcpyDeviceToHost, st));
+    CUDACHK(cudaMemcpyAsync(hb->res, edges, 12, cudaMemcpyDeviceToHost, st));
     MGWAIT();
     CUDACHK(cudaGetLastError());
-    if (h_err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
-    *out_head = h_firsts[0];  // rank 0 always holds sorted position 0 (n > 0)
+    if (hb->err & E_DYN_FULL) { rc = RC_DYN_OVERFLOW; goto done; }  // every rank sees it (all-reduced)
+    if (hb->err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
+    *out_head = hb->res[2];  // rank 0 always holds sorted position 0 (n > 0)
     if (launches_out) *launches_out = launches;
   }
 done:
+  if (plan_ev) cudaEventDestroy(plan_ev);
   cudaFreeAsync(base, st);
   if (rc != PBIT_ERR_NCCL) cudaStreamSynchronize(st);  // a stuck collective is released by the caller's abort
   return rc;
@@ -509,24 +753,36 @@ int pbit_mg_comm_init(void** comm_out, int nranks, const void* id, int rank) {
   return PBIT_OK;
 }
 
+static void release_window(void* comm) {
+  std::lock_guard<std::mutex> lk(g_win_mu);
+  auto it = g_wins.find(comm);
+  if (it != g_wins.end()) {
+    win_release(it->second);
+    g_wins.erase(it);
+  }
+}
+
 int pbit_mg_comm_abort(void* comm) {
   if (!comm) return PBIT_ERR_INVALID_ARG;
-  return ncclCommAbort((ncclComm_t)comm) == ncclSuccess ? PBIT_OK : PBIT_ERR_NCCL;
+  const int rc = ncclCommAbort((ncclComm_t)comm) == ncclSuccess ? PBIT_OK : PBIT_ERR_NCCL;
+  release_window(comm);
+  return rc;
 }
 
 int pbit_mg_comm_destroy(void* comm) {
   if (!comm) return PBIT_ERR_INVALID_ARG;
+  release_window(comm);
   return ncclCommDestroy((ncclComm_t)comm) == ncclSuccess ? PBIT_OK : PBIT_ERR_NCCL;
 }
 
 // Host-side plan of the exchange (step 5), exported so the multi-rank logic can be tested
-// without GPUs.  Every rank's chunk is sorted by (key, list position); splitter s sits at
-// global rank x_s = min(n, (s+1)*S) of the final order and has key k*_s.
-// lt[q*(G-1)+s] / le[q*(G-1)+s] = keys of rank q below / up to k*_s.  Elements below k*_s
-// go left of the split; of the t_s = x_s - sum_q lt ties that also go left, ranks take
-// theirs in rank order (= list-position order).  Rank r sends to d the contiguous range
-// [left_r(d-1), left_r(d)) of its sorted chunk and receives, in source-rank order, from
-// every q the range [left_q(r-1), left_q(r)).
+// without GPUs (k_split_plan is its device twin).  Every rank's chunk is sorted stably by
+// splitter bucket; splitter s sits at global rank x_s = min(n, (s+1)*S) of the final order
+// and has key k*_s.  lt[q*(G-1)+s] / le[q*(G-1)+s] = keys of rank q below / up to k*_s.
+// Elements below k*_s go left of the split; of the t_s = x_s - sum_q lt ties that also go
+// left, ranks take theirs in rank order (= list-position order).  Rank r sends to d the
+// contiguous range [left_r(d-1), left_r(d)) of its bucket order and receives, in
+// source-rank order, from every q the range [left_q(r-1), left_q(r)).
 void pbit_mg_exchange_plan(int G, int r, uint64_t n, uint64_t S, const uint64_t* lt, const uint64_t* le,
                            uint64_t* send_off, uint64_t* send_count, uint64_t* recv_off, uint64_t* recv_count) {
   const int NS = G - 1;
@@ -630,12 +886,13 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
       return PBIT_ERR_INVALID_ARG;
     return PBIT_OK;
   }();
-  // shared by all ranks: the list, the key format, the digit width.  out_prev: the ranks
-  // that own nodes must all pass it or none (flags: some rank with / without it)
-  const uint64_t shared[6] = {n_global, head, (uint64_t)key_bits, (uint64_t)K, (uint64_t)km.kind,
-                              (uint64_t)km.descending};
+  // shared by all ranks: the list, the key format, the digit width, the transport.
+  // out_prev: the ranks that own nodes must all pass it or none (flags: some rank with /
+  // without it)
+  const uint64_t shared[7] = {n_global, head, (uint64_t)key_bits, (uint64_t)K, (uint64_t)km.kind,
+                              (uint64_t)km.descending, (uint64_t)transport_request()};
   uint64_t flags[2] = {n_local && out_prev_local ? 1ull : 0ull, n_local && !out_prev_local ? 1ull : 0ull};
-  int rc = mg_agree(rc_local, shared, 6, flags, 2, comm, st);
+  int rc = mg_agree(rc_local, shared, 7, flags, 2, comm, st);
   if (rc) return rc;
   if (flags[0] && flags[1]) {
     set_last_error("pbit_sort_list_mg", "out_prev passed on some ranks but not on others");
@@ -647,16 +904,33 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
     *out_head = PBIT_NULL;
     return PBIT_OK;
   }
+  int transport = transport_request();
+  for (;;) {
 #define PBIT_RUN_MG(KB)                                                                                          \
-  run_mg<KB>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km, out_head,   \
-             out_next_local, out_prev_local, with_prev, comm, G, r, st, opts ? opts->launches : nullptr)
-  switch (key_bits) {
-    case 8: return PBIT_RUN_MG(1);
-    case 16: return PBIT_RUN_MG(2);
-    case 32: return PBIT_RUN_MG(4);
-    default: return PBIT_RUN_MG(8);
-  }
+    run_mg<KB>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km, out_head, \
+               out_next_local, out_prev_local, with_prev, comm, G, r, st, transport, opts ? opts->launches : nullptr)
+    switch (key_bits) {
+      case 8: rc = PBIT_RUN_MG(1); break;
+      case 16: rc = PBIT_RUN_MG(2); break;
+      case 32: rc = PBIT_RUN_MG(4); break;
+      default: rc = PBIT_RUN_MG(8); break;
+    }
 #undef PBIT_RUN_MG
+    // the peer transport is unavailable (some rank cannot map the others' memory), or its
+    // per-rank dynamic ruler table overflowed: every rank saw the same verdict -> NCCL
+    if (transport == T_PEER && (rc == PBIT_ERR_UNSUPPORTED || rc == RC_DYN_OVERFLOW)) {
+      transport = T_NCCL;
+      continue;
+    }
+    return rc;
+  }
+}
+
+int pbit_mg_transport(void* comm) {
+  if (!comm) return -1;
+  std::lock_guard<std::mutex> lk(g_win_mu);
+  auto it = g_wins.find(comm);
+  return (it != g_wins.end() && it->second.local) ? 0 : 1;
 }
 
 }  // extern "C"

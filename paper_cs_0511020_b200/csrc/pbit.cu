@@ -224,9 +224,11 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   size_t off = 0;
   auto take = [&](size_t bytes) { char* q = base ? base + off : nullptr; off += align_up(bytes); return (void*)q; };
   w->kn = take(n * rec);
-  w->slots = take(Rmax * p.cap * rec);  // also holds the relink pairs (dead slots by then)
-  for (int i = 0; i < 2; ++i)  // relink (v, succ) buffers: 2 x n x 8 B <= slot bytes
-    w->pairs[i] = base ? (uint2*)w->slots + i * align_up(n) : nullptr;
+  // the slots also hold the two relink record buffers (dead slots by then): n records of
+  // up to 12 B (v, succ, pred) each, plus the 16 B of padding the tile loads may read
+  const size_t rbuf = align_up(n * 12 + 16);
+  w->slots = take(std::max(Rmax * p.cap * rec, 2 * rbuf));
+  for (int i = 0; i < 2; ++i) w->pairs[i] = base ? (uint2*)((char*)w->slots + i * rbuf) : nullptr;
   w->seg = (uint2*)take(Rmax * 8);
   w->dist = (uint32_t*)take(Rmax * 4);
   const size_t nsub = (Rmax >> p.sub_log2) + 2;
@@ -326,7 +328,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   {
     static const int walk_occ = [] {  // resident walk CTAs per SM (one arch per process)
       int occ = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KB>, WALK_THREADS, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_walk<KB, false>, WALK_THREADS, 0);
       occ = std::max(occ, 1);
       if (int cap_occ = debug_env("PBIT_WALK_OCC")) occ = std::min(occ, cap_occ);  // experiments
       return occ;
@@ -335,7 +337,10 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t min_per = 4;
     if ((uint32_t)blocks * min_per > R_static) blocks = std::max(1u, (R_static + min_per - 1) / min_per);
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
-    launch_pdl(k_walk<KB>, blocks, WALK_THREADS, 0, st, (const RT*)w.kn, sel, R_static, head, (RT*)w.slots, p.cap,
+    KnSrc<RT> src{};
+    src.kn = (const RT*)w.kn;
+    const WalkMap wm{0u, p.R, head_is_ruler ? PBIT_NULL32 : p.R, R_static, R_static};  // slot(r) = r
+    launch_pdl(k_walk<KB, false>, blocks, WALK_THREADS, 0, st, src, sel, wm, head, (RT*)w.slots, p.cap,
                w.seg, w.dyn_count, p.dyn_cap, per_cta, w.err, debug_env("PBIT_DEBUG_WALK_NOWRITE"));
     ++launches;
   }
@@ -429,11 +434,9 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t* fin = w.ids[hplan.npasses & 1u];  // buffer holding the final ids
     launch_pdl(k_relink_head, 1, 1, 0, st, fin, w.d_head, w.err);
     ++launches;
-    launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_next, w.err, st, sms);
-    if (out_prev) {  // N2: the same binned relink of the pairs (ids[p], ids[p-1])
-      cudaMemsetAsync(w.cursors, 0, relink_cursor_words(n) * 4, st);
-      launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_prev, w.err, st, sms, -1);
-    }
+    // N2: with out_prev the records are (v, succ, pred): both outputs in one chain
+    launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_next, out_prev, w.err, st,
+                              sms);
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
 

@@ -69,7 +69,7 @@ def run_case(G, n, key_bits, keys, links, K, kind, desc, with_prev, seed):
                                         out_prev_local=prev)
                 st.synchronize()
                 res[r] = (h, out.cpu().numpy().view(np.uint32).copy(),
-                          prev.cpu().numpy().view(np.uint32).copy() if with_prev else None)
+                          prev.cpu().numpy().view(np.uint32).copy() if with_prev else None, p.mg_transport(comm))
                 p.mg_comm_destroy(comm)
         except Exception as e:  # noqa: BLE001  (reported by the main thread)
             errs[r] = e
@@ -88,6 +88,10 @@ def run_case(G, n, key_bits, keys, links, K, kind, desc, with_prev, seed):
     if any(errs):
         return False, f"rank errors: {[repr(e) for e in errs if e]}", False
     heads = {r_[0] for r_ in res}
+    used = {r_[3] for r_ in res}
+    want_t = os.environ.get("PBIT_MG_TRANSPORT", "peer")
+    if used != {want_t}:
+        return False, f"transport {used} != {want_t}", False
     oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4,
                               descending=desc, kind=kind)
     got = np.concatenate([r_[1] for r_ in res]) if n else np.zeros(0, np.uint32)
@@ -100,7 +104,7 @@ def run_case(G, n, key_bits, keys, links, K, kind, desc, with_prev, seed):
         gp = np.concatenate([r_[2] for r_ in res])
         if not np.array_equal(gp, oracle.repair_back(on, oh)):
             return False, "out_prev differs from the oracle's repair walk", False
-    return True, "ok", False
+    return True, f"ok ({want_t})", False
 
 
 def run_mismatch(G=3):

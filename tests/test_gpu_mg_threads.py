@@ -14,9 +14,14 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def test_mg_multi_rank_threads_vs_oracle(cuda_ok):
+@pytest.mark.parametrize("transport", ["peer", "nccl"])
+def test_mg_multi_rank_threads_vs_oracle(cuda_ok, transport):
+    """Both transports (N4 peer windows, and the NCCL reference) bit-exact with the oracle,
+    hence with each other."""
+    env = dict(os.environ, PBIT_MG_TRANSPORT=transport)
     r = subprocess.run([sys.executable, os.path.join(HERE, "fake_nccl", "run_mg_threads.py")],
-                       capture_output=True, text=True, timeout=900)
+                       capture_output=True, text=True, timeout=900, env=env)
     print(r.stdout[-4000:], r.stderr[-2000:])
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
     assert "cases bit-exact" in r.stdout and "FAILED" not in r.stdout
+    assert f"ok ({transport})" in r.stdout

@@ -142,16 +142,46 @@ def test_largest_n_fails_cleanly_with_oom(pbit):
     torch.cuda.empty_cache()
 
 
-def test_workspace_pool_trim(pbit):
-    """Workspace comes from the library's own pool (not the device's default pool) and
-    pbit_workspace_trim hands it back; sorting afterwards still works."""
+def test_workspace_released_after_each_call_by_default(pbit):
+    """Default: the workspace goes back to the device when the call ends (release
+    threshold 0, pbit.h); the device's free memory after a call is what it was before."""
     li = workloads.make_list(1 << 22, 32, seed=12, keys="uniform", device="cuda")
     want = _oracle(li)
-    _assert_same(_gpu_sort(pbit, li), want, "before trim")
+    torch.cuda.synchronize()
     free0 = torch.cuda.mem_get_info()[0]
+    got = _gpu_sort(pbit, li)   # allocates its output tensor (16 MB) from torch's cache
+    torch.cuda.synchronize()
+    assert torch.cuda.mem_get_info()[0] >= free0 - (64 << 20)   # ~250 MB of workspace returned
+    _assert_same(got, want, "default pool")
     pbit.workspace_trim(0)
-    assert torch.cuda.mem_get_info()[0] >= free0 + (100 << 20)  # ~250 MB of workspace released
     _assert_same(_gpu_sort(pbit, li), want, "after trim")
+
+
+KEEP_SNIPPET = """
+import torch, workloads, paper_cs_0511020_b200 as pbit
+li = workloads.make_list(1 << 22, 32, seed=12, keys="uniform", device="cuda")
+out = torch.empty_like(li.next)
+torch.cuda.synchronize(); f0 = torch.cuda.mem_get_info()[0]
+pbit.sort_list(li.keys, li.next, li.head, out_next=out); torch.cuda.synchronize()
+f1 = torch.cuda.mem_get_info()[0]
+pbit.workspace_trim(0); f2 = torch.cuda.mem_get_info()[0]
+print(f0, f1, f2)
+assert f1 <= f0 - (100 << 20), "PBIT_POOL_KEEP_GB: workspace should stay mapped"
+assert f2 >= f0 - (64 << 20), "pbit_workspace_trim(0) should release it"
+"""
+
+
+def test_workspace_kept_with_pool_keep_gb_and_trimmed(pbit):
+    """PBIT_POOL_KEEP_GB (opt-in) keeps the workspace mapped between calls;
+    pbit_workspace_trim hands it back (subprocess: the pool reads the variable once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PBIT_POOL_KEEP_GB="8", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", KEEP_SNIPPET], capture_output=True, text=True, env=env, cwd=root,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
 
 
 def test_all_equal_keys_runs_no_pass(pbit):

@@ -5,7 +5,8 @@ Each rank follows the steps of paper_cs_0511020_b200/csrc/mg.cu with numpy stand
 for the device kernels, and the product's own host-side exchange planner
 (`pbit_mg_exchange_plan`, `pbit_mg_slice` from libpbit.so) deciding what moves where:
   1 own id slice -> replica (all_gather)         4 chunk of own list positions
-  5 top non-trivial digit: stable local pass, count matrix (all_gather), planner,
+  5 exact splitters (8-bit radix refinement rounds over all_reduced histograms), one
+    stable partition by splitter bucket, per-rank counts (all_gather), the planner,
     point-to-point exchange, receive buffers concatenated in source-rank order
   6 stable local sort                              7 stitch (all_gather of first and last ids),
     (v, succ) and (v, pred) routed to the owner of v, applied to the owner's out_next /
@@ -105,29 +106,39 @@ def _rank_main(rank, G, port, n, key_bits, seed, keys_kind, links, K, out_q):
         hist = th.numpy()
         nontrivial = [d for d in range(D) if hist[d].max() != n]
         if nontrivial:
-            # 5a. stable local sort by the full key (chunk in list order -> (key, position))
-            perm = np.argsort(ck, kind="stable")
-            ck, ids = ck[perm], ids[perm]
             ck64 = ck.astype(np.uint64)
-            # 5b. splitters by radix refinement: global counts below candidate keys
+            # 5a. splitters by radix refinement, 8 bits per round from the top: histograms of
+            # the next digit among the keys matching each splitter's prefix, summed over the
+            # ranks (all_reduce); each prefix takes the largest digit c with
+            # below + #(prefix, digit < c) <= x_s (k_split_count / k_split_select)
             NS = G - 1
             prefix = [0] * NS
-            for i in range(D - 1, -1, -1):
-                wbits = M - K * (D - 1) if i == D - 1 else K
-                nc = 1 << wbits
-                q = np.array([[((prefix[sp] << wbits) | c) << (K * i) for c in range(nc)] for sp in range(NS)],
-                             dtype=np.uint64).reshape(-1)
-                cnt = torch.from_numpy(np.searchsorted(ck64, q, side="left").astype(np.int64))
-                dist.all_reduce(cnt)
-                cnt = cnt.numpy().reshape(max(NS, 1), nc) if NS else cnt.numpy()
+            below = [0] * NS
+            for i in range(key_bits // 8 - 1, -1, -1):
+                top = ck64 >> np.uint64(8 * i + 8) if 8 * i + 8 < 64 else np.zeros_like(ck64)
+                dig = ((ck64 >> np.uint64(8 * i)) & np.uint64(255)).astype(np.int64)
+                h = np.stack([np.bincount(dig[top == np.uint64(prefix[sp])], minlength=256) for sp in range(NS)]) \
+                    if NS else np.zeros((0, 256), np.int64)
+                th = torch.from_numpy(h.astype(np.int64))
+                dist.all_reduce(th)
+                h = th.numpy()
                 for sp in range(NS):
                     x = min(n, (sp + 1) * S)
-                    pick = max(c for c in range(nc) if cnt[sp, c] <= x)
-                    prefix[sp] = (prefix[sp] << wbits) | pick
-            # 5c. per-rank counts below / up to each splitter; the product's planner
+                    cum = np.concatenate([[0], np.cumsum(h[sp])])[:256]
+                    pick = max(c for c in range(256) if below[sp] + cum[c] <= x)
+                    below[sp] += int(cum[pick])
+                    prefix[sp] = (prefix[sp] << 8) | pick
+            # 5b. ONE stable partition by splitter bucket (2j + [key == k*_j]): key ranges in
+            # order, list order inside each bucket (the SRC_SPLIT pass)
             kst = np.array(prefix, dtype=np.uint64)
-            mine = np.concatenate([np.searchsorted(ck64, kst, side="left"),
-                                   np.searchsorted(ck64, kst, side="right")]).astype(np.int64)
+            jj = np.searchsorted(kst, ck64, side="left")
+            eq = (jj < NS) & (kst[np.minimum(jj, max(NS - 1, 0))] == ck64) if NS else np.zeros(len(ck64), bool)
+            perm = np.argsort(2 * jj + eq, kind="stable")
+            ck, ids = ck[perm], ids[perm]
+            # 5c. per-rank counts below / up to each splitter; the product's planner
+            mine = np.concatenate([(ck64[:, None] < kst[None, :]).sum(0),
+                                   (ck64[:, None] <= kst[None, :]).sum(0)]).astype(np.int64) \
+                if NS else np.zeros(0, np.int64)
             allm = [torch.empty(2 * NS, dtype=torch.int64) for _ in range(G)]
             dist.all_gather(allm, torch.from_numpy(mine))
             lt = np.stack([t_.numpy()[:NS] for t_ in allm])
