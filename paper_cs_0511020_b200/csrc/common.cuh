@@ -142,4 +142,33 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
   return m;
 }
 
+// ----------------------------------------------------------------------------- histograms
+// One count into a per-CTA shared-memory histogram, from every lane of a warp at once (the
+// whole warp must call it; `valid` masks lanes without an item).  SURVEY §8(a) a2:
+//   0  one shared atomic per lane;
+//   1  __match_any_sync groups the lanes holding the same bin; the lowest lane of each
+//      group adds the group's size (one atomic per distinct bin in the warp);
+//   2  __ballot_sync of the lanes sharing lane 0's bin: lane 0 adds them all, the others
+//      add 1 each (one extra ballot; pays off when one value dominates the warp).
+#ifndef PBIT_HIST_MODE
+#define PBIT_HIST_MODE 1
+#endif
+template <int MODE = PBIT_HIST_MODE>
+__device__ __forceinline__ void hist_add(uint32_t* __restrict__ h, uint32_t bin, bool valid) {
+  if constexpr (MODE == 0) {
+    if (valid) atomicAdd(h + bin, 1u);
+  } else if constexpr (MODE == 1) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, valid ? bin : 0xFFFFFFFFu);
+    if (valid && (peers & lanemask_lt()) == 0u) atomicAdd(h + bin, (uint32_t)__popc(peers));
+  } else {
+    const uint32_t b0 = __shfl_sync(0xffffffffu, bin, 0);
+    const uint32_t eq = __ballot_sync(0xffffffffu, valid && bin == b0);
+    if ((threadIdx.x & 31u) == 0u) {
+      if (eq) atomicAdd(h + b0, (uint32_t)__popc(eq));
+    } else if (valid && !((eq >> (threadIdx.x & 31u)) & 1u)) {
+      atomicAdd(h + bin, 1u);
+    }
+  }
+}
+
 }  // namespace pbit

@@ -63,7 +63,7 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 // write-out of the stable passes: 128-bit stores over 16 B-aligned groups of every digit
 // run (1), or one 4 B store per element, consecutive threads on consecutive elements (0)
 #ifndef PBIT_VEC_STORE
-#define PBIT_VEC_STORE 1
+#define PBIT_VEC_STORE 0
 #endif
 // per-warp digit counters of the pass ranking: u32 (one word per digit: no two digits
 // share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
@@ -104,18 +104,21 @@ struct KeyMap {
 
 // ============================================================================ a1/a2: pack
 // Reads key[v], next[v] (streaming, coalesced), writes the AoS record kn[v], and counts
-// every digit of every key into a per-CTA smem histogram (flushed once per CTA).
-// Four independent nodes per thread and iteration: 4x the loads in flight of one node
-// per thread, every access still lane-contiguous.
+// every digit of every key into a per-CTA smem histogram (hist_add: warp-aggregated,
+// flushed once per CTA).  Four independent nodes per thread and iteration: 4x the loads in
+// flight of one node per thread, every access still lane-contiguous.  The loop runs the
+// same trips on every lane of a warp (the histogram is a warp-wide operation).
 template <int KB>
-__device__ __forceinline__ void pack_one(unsigned long long k, uint32_t nx, uint32_t v, uint32_t n_ids,
+__device__ __forceinline__ void pack_one(unsigned long long k, uint32_t nx, uint32_t v, bool ok, uint32_t n_ids,
                                          typename Rec<KB>::T* __restrict__ kn, uint32_t* s_hist, int radix,
                                          uint32_t mask, int K, int D, const KeyMap& km, int& bad) {
-  bad |= (nx != PBIT_NULL32) & (nx >= n_ids);
-  if (!km.identity()) k = km(k, KB * 8);
-  if constexpr (KB == 8) kn[v] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), nx, 0u);
-  else kn[v] = make_uint2((uint32_t)k, nx);
-  for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
+  if (ok) {
+    bad |= (nx != PBIT_NULL32) & (nx >= n_ids);
+    if (!km.identity()) k = km(k, KB * 8);
+    if constexpr (KB == 8) kn[v] = make_uint4((uint32_t)k, (uint32_t)(k >> 32), nx, 0u);
+    else kn[v] = make_uint2((uint32_t)k, nx);
+  }
+  for (int d = 0; d < D; ++d) hist_add(s_hist + d * radix, (uint32_t)(k >> (d * K)) & mask, ok);
 }
 
 template <int KB>
@@ -136,21 +139,23 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
   int bad = 0;
   const KT* __restrict__ kp = reinterpret_cast<const KT*>(keys);
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-  uint32_t v = tid;
-  for (; (unsigned long long)v + (U - 1) * (unsigned long long)stride < n; v += U * stride) {
+  const uint32_t lane = threadIdx.x & 31u;
+  for (unsigned long long v0 = tid - lane; v0 < n; v0 += (unsigned long long)U * stride) {  // warp-uniform
     KT k[U];
     uint32_t nx[U];
+    bool ok[U];
 #pragma unroll
     for (int e = 0; e < U; ++e) {
-      k[e] = __ldcs(kp + v + e * stride);
-      nx[e] = __ldcs(next + v + e * stride);
+      const unsigned long long v = v0 + lane + (unsigned long long)e * stride;
+      ok[e] = v < n;
+      k[e] = ok[e] ? __ldcs(kp + v) : KT(0);
+      nx[e] = ok[e] ? __ldcs(next + v) : 0u;
     }
 #pragma unroll
     for (int e = 0; e < U; ++e)
-      pack_one<KB>((unsigned long long)k[e], nx[e], v + e * stride, n_ids, kn, s_hist, radix, mask, K, D, km, bad);
+      pack_one<KB>((unsigned long long)k[e], nx[e], (uint32_t)(v0 + lane + (unsigned long long)e * stride), ok[e],
+                   n_ids, kn, s_hist, radix, mask, K, D, km, bad);
   }
-  for (; v < n; v += stride)
-    pack_one<KB>((unsigned long long)kp[v], __ldcs(next + v), v, n_ids, kn, s_hist, radix, mask, K, D, km, bad);
   if (bad) atomicOr(err, E_BAD_INDEX);
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x)
@@ -1112,11 +1117,15 @@ k_array_prep(const void* __restrict__ keys, uint32_t n, typename KeyOf<KB>::T* _
   __syncthreads();
   const uint32_t mask = radix - 1;
   const KT* __restrict__ kp = reinterpret_cast<const KT*>(keys);
-  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-    unsigned long long k = __ldcs(kp + v);
+  const uint32_t lane = threadIdx.x & 31u;
+  for (unsigned long long v0 = blockIdx.x * blockDim.x + threadIdx.x - lane; v0 < n;
+       v0 += (unsigned long long)gridDim.x * blockDim.x) {  // warp-uniform trips (hist_add)
+    const unsigned long long v = v0 + lane;
+    const bool ok = v < n;
+    unsigned long long k = ok ? (unsigned long long)__ldcs(kp + v) : 0ull;
     if (!km.identity()) k = km(k, KB * 8);
-    kout[v] = (typename KeyOf<KB>::T)k;
-    for (int d = 0; d < D; ++d) atomicAdd(&s_hist[d * radix + (int)((k >> (d * K)) & mask)], 1u);
+    if (ok) kout[v] = (typename KeyOf<KB>::T)k;
+    for (int d = 0; d < D; ++d) hist_add(s_hist + d * radix, (uint32_t)(k >> (d * K)) & mask, ok);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < nb; i += blockDim.x)

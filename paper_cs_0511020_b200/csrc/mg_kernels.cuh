@@ -185,11 +185,9 @@ k_mg_gather(const __grid_constant__ PeerSlots ps, MgRulers mr, uint32_t cap, con
 }
 
 // ============================================================================ histograms
-// Histograms of every digit of m keys (a chunk in list order, or the received keys).
-// Warp-aggregated: the lanes holding the same digit value (__match_any_sync) add their
-// count with one shared atomic from the lowest lane (heavy duplicates -- C3's top key is
-// 12 % of the nodes -- otherwise serialise on one counter); per-CTA counters are flushed
-// to the global histogram once.
+// Histograms of every digit of m keys (a chunk in list order, or the received keys),
+// warp-aggregated by hist_add (common.cuh); per-CTA counters are flushed to the global
+// histogram once.
 template <typename KeyT>
 __global__ void __launch_bounds__(256)
 k_chunk_hist(const KeyT* __restrict__ keys, uint32_t m, int K, int D, uint32_t* __restrict__ hist,
@@ -204,11 +202,7 @@ k_chunk_hist(const KeyT* __restrict__ keys, uint32_t m, int K, int D, uint32_t* 
     const uint32_t p = p0 + threadIdx.x;
     const bool valid = p < m;
     const KeyT k = valid ? keys[p] : KeyT(0);
-    for (int d = 0; d < D; ++d) {
-      const uint32_t dig = (uint32_t)(k >> (d * K)) & (uint32_t)(radix - 1);
-      const uint32_t peers = __match_any_sync(0xffffffffu, valid ? dig : 0xFFFFFFFFu);
-      if (valid && (peers & lanemask_lt()) == 0u) atomicAdd(&s_hist[d * radix + (int)dig], (uint32_t)__popc(peers));
-    }
+    for (int d = 0; d < D; ++d) hist_add(s_hist + d * radix, (uint32_t)(k >> (d * K)) & (uint32_t)(radix - 1), valid);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < D * radix; i += blockDim.x)
@@ -278,7 +272,7 @@ static __global__ void k_split_select(uint32_t* __restrict__ hist, uint32_t NS, 
 }
 
 // Local bucket counts of the chunk (SplitTable buckets: 2*NS + 1 of them), warp-aggregated
-// like k_chunk_hist.  kstar is read from the split table's staging area.
+// by hist_add.  kstar is read from the split table's staging area.
 template <typename KeyT>
 __global__ void __launch_bounds__(256)
 k_split_buckets(const KeyT* __restrict__ keys, uint32_t m, const SplitTable* __restrict__ spt,
@@ -294,9 +288,8 @@ k_split_buckets(const KeyT* __restrict__ keys, uint32_t m, const SplitTable* __r
   for (uint32_t p0 = blockIdx.x * blockDim.x; p0 < m; p0 += stride) {
     const uint32_t p = p0 + threadIdx.x;
     const bool valid = p < m;
-    const uint32_t b = valid ? split_bucket(sp, (unsigned long long)keys[p]) : 0xFFFFFFFFu;
-    const uint32_t peers = __match_any_sync(0xffffffffu, b);
-    if (valid && (peers & lanemask_lt()) == 0u) atomicAdd(&s_cnt[b], (uint32_t)__popc(peers));
+    const uint32_t b = valid ? split_bucket(sp, (unsigned long long)keys[p]) : 0u;
+    hist_add(s_cnt, b, valid);
   }
   __syncthreads();
   if (threadIdx.x < 2 * sp.NS + 1 && s_cnt[threadIdx.x]) atomicAdd(&cnt[threadIdx.x], s_cnt[threadIdx.x]);

@@ -3,6 +3,7 @@ protocol's own cost on one GPU (no NVLink traffic)."""
 import os
 import sys
 
+os.environ.setdefault("PBIT_POOL_KEEP_GB", "96")  # as bench.py: workspace kept mapped between calls
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
@@ -25,5 +26,6 @@ for name, fn in (("single", lambda: pbit.sort_list(li.keys, li.next, li.head, ou
         fn()
     e1.record(st)
     torch.cuda.synchronize()
-    print(f"{cfg} {name}: {e0.elapsed_time(e1) / 5:.3f} ms")
+    print(f"{cfg} {name}: {e0.elapsed_time(e1) / 5:.3f} ms"
+          + (f" (transport {pbit.mg_transport(comm)})" if name.startswith("mg") else ""))
 pbit.mg_comm_destroy(comm)
