@@ -253,6 +253,29 @@ def load_traffic(cfg: str):
         return None
 
 
+def nvlink_model(n: int, G: int, key_bits: int, transport: str) -> dict:
+    """Bytes each rank moves over NVLink per pbit_sort_list_mg call (a model):
+    the walk's remote node reads (one 32 B sector per remote step, (G-1)/G of the n/G steps a
+    rank walks), the segment-table all-gather, the chunk gather from the walkers' slots, the
+    key-range scatter and the relink routing ((G-1)/G of each rank's n/G records); the NCCL
+    transport replaces the remote reads by an all-gather of the whole (key, next) array."""
+    f = (G - 1) / G
+    per = n / G
+    kb = 8 if key_bits == 64 else 4
+    rec = 16 if key_bits == 64 else 8
+    seg_table = f * (n / 64 + n / 256) * 8
+    parts = {"segment_table": seg_table, "key_range_exchange": f * per * (kb + 4), "relink_routing": f * per * 8}
+    if transport == "peer":
+        parts["walk_remote_reads"] = f * per * 32
+        parts["chunk_gather"] = f * per * (kb + 4)
+    else:
+        parts["kn_allgather"] = f * n * rec
+        parts["segment_table"] = f * (n / 64) * 8
+    total = sum(parts.values())
+    return {"transport": transport, "bytes_per_rank": round(total), "parts": {k: round(v) for k, v in parts.items()},
+            "ms_at_770_gbs": round(total / 770e9 * 1e3, 3)}
+
+
 def run_mg(args):
     """N > 1: one list sorted by every rank together (pbit_sort_list_mg)."""
     import torch
@@ -324,7 +347,8 @@ def run_mg(args):
                 "cpu_baseline": cpu,
                 "e2e": {"value": n / float(e2e_t.item()), "unit": UNIT,
                         "h2d_bytes_per_step": (hi - lo) * (kb // 8 + 4), "d2h_bytes_per_step": (hi - lo) * 4},
-                "gpu_launches": pbit.last_mg_launches * args.steps, "clocks": clk.summary()}
+                "gpu_launches": pbit.last_mg_launches * args.steps, "clocks": clk.summary(),
+                "nvlink_model": nvlink_model(n, ws, kb, pbit.mg_transport(comm))}
         print(json.dumps(line), flush=True)
     pbit.mg_comm_destroy(comm)
     dist.destroy_process_group()

@@ -207,6 +207,12 @@ int pbit_mg_comm_abort(void *comm);
  * a rank cannot map the others).  -1 for a NULL communicator. */
 int pbit_mg_transport(void *comm);
 
+/* The ruling set pbit_sort_list_mg uses for n nodes on nranks ranks: the ruler spacing (a
+ * power of two <= 64, which divides every rank's id slice) and the ruler blocks per rank;
+ * nranks * blocks * spacing >= n.  PBIT_ERR_UNSUPPORTED if the slices cannot be tiled (n
+ * beyond 32-bit ids).  Host only; exported for tests. */
+int pbit_mg_ruler_blocks(uint64_t n, int nranks, uint32_t *spacing, uint32_t *blocks_per_rank);
+
 /* Node ids per rank for pbit_sort_list_mg: ceil(n_global / nranks) rounded up to 64. */
 uint64_t pbit_mg_slice(uint64_t n_global, int nranks);
 

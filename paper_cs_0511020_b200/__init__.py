@@ -22,7 +22,8 @@ NUM_PHASES = 5 + 64
 PHASE_NAMES = ["pack", "walk", "rank", "gather", "relink"] + [f"pass{i}" for i in range(64)]
 SYMBOLS = ["pbit_sort_list", "pbit_sort_list_mg", "pbit_sort_array", "pbit_mg_get_unique_id", "pbit_mg_comm_init",
            "pbit_mg_comm_destroy", "pbit_mg_comm_abort", "pbit_status_string", "pbit_version", "pbit_last_error",
-           "pbit_mg_slice", "pbit_mg_exchange_plan", "pbit_workspace_trim", "pbit_rank_mode", "pbit_mg_transport"]
+           "pbit_mg_slice", "pbit_mg_exchange_plan", "pbit_workspace_trim", "pbit_rank_mode", "pbit_mg_transport",
+           "pbit_mg_ruler_blocks"]
 
 STATUS = {0: "PBIT_OK", 1: "PBIT_ERR_INVALID_ARG", 2: "PBIT_ERR_INVALID_LIST", 3: "PBIT_ERR_OOM",
           4: "PBIT_ERR_CUDA", 5: "PBIT_ERR_NCCL", 6: "PBIT_ERR_UNSUPPORTED"}
@@ -72,6 +73,9 @@ def _load():
     lib.pbit_status_string.argtypes = [ctypes.c_int]
     lib.pbit_version.restype = ctypes.c_uint32
     lib.pbit_last_error.restype = ctypes.c_char_p
+    lib.pbit_mg_ruler_blocks.restype = ctypes.c_int
+    lib.pbit_mg_ruler_blocks.argtypes = [ctypes.c_uint64, ctypes.c_int, ctypes.POINTER(ctypes.c_uint32),
+                                         ctypes.POINTER(ctypes.c_uint32)]
     lib.pbit_mg_transport.restype = ctypes.c_int
     lib.pbit_mg_transport.argtypes = [ctypes.c_void_p]
     lib.pbit_rank_mode.restype = ctypes.c_int
@@ -278,6 +282,15 @@ def mg_transport(comm: int) -> str:
     """"peer" (N4: CUDA IPC windows, peer loads and stores) or "nccl": the transport the
     last sort_list_mg call on `comm` used (pbit.h pbit_mg_transport)."""
     return {0: "peer", 1: "nccl"}.get(int(lib.pbit_mg_transport(ctypes.c_void_p(comm))), "none")
+
+
+def mg_ruler_blocks(n_global: int, nranks: int):
+    """(ruler spacing, ruler blocks per rank) of sort_list_mg's walk (pbit.h)."""
+    sp, b = ctypes.c_uint32(0), ctypes.c_uint32(0)
+    rc = lib.pbit_mg_ruler_blocks(n_global, nranks, ctypes.byref(sp), ctypes.byref(b))
+    if rc:
+        raise PbitError(rc, "pbit_mg_ruler_blocks")
+    return int(sp.value), int(b.value)
 
 
 def mg_slice(n_global: int, nranks: int) -> int:

@@ -61,13 +61,14 @@ struct RulerSel {
 };
 
 // ----------------------------------------------------------------------------- division
-// x / d for a divisor fixed per launch (Granlund-Montgomery, d >= 2): the multi-GPU walk
-// divides every node id by the rank slice S to find the rank that owns it.
+// x / d for a divisor fixed per launch (Granlund-Montgomery; d = 1 by a branch): the
+// multi-GPU walk divides every node id by the rank slice S to find the rank that owns it.
 struct FastDiv {
-  uint32_t d = 2, m = 0, s = 1;
+  uint32_t d = 1, m = 0, s = 1;
   __host__ static FastDiv make(uint32_t d) {
     FastDiv f;
-    f.d = d < 2 ? 2 : d;
+    f.d = d < 1 ? 1 : d;
+    if (f.d == 1) return f;
     uint32_t sh = 0;
     while ((1ull << sh) < f.d) ++sh;  // ceil(log2 d)
     f.s = sh;
@@ -80,7 +81,7 @@ struct FastDiv {
 #else
     const uint32_t t = (uint32_t)(((unsigned long long)x * m) >> 32);
 #endif
-    return (t + ((x - t) >> 1)) >> (s - 1);
+    return d == 1 ? x : (t + ((x - t) >> 1)) >> (s - 1);
   }
 };
 
@@ -150,8 +151,10 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 //      group adds the group's size (one atomic per distinct bin in the warp);
 //   2  __ballot_sync of the lanes sharing lane 0's bin: lane 0 adds them all, the others
 //      add 1 each (one extra ballot; pays off when one value dominates the warp).
+// Measured on B200: mode 0 wins for every histogram here (pack of C3: 0.78
+// ms, vs 6.65 ms with match.any and 2.19 ms with the ballot), so it is the default.
 #ifndef PBIT_HIST_MODE
-#define PBIT_HIST_MODE 1
+#define PBIT_HIST_MODE 0
 #endif
 template <int MODE = PBIT_HIST_MODE>
 __device__ __forceinline__ void hist_add(uint32_t* __restrict__ h, uint32_t bin, bool valid) {

@@ -104,10 +104,15 @@ struct KeyMap {
 
 // ============================================================================ a1/a2: pack
 // Reads key[v], next[v] (streaming, coalesced), writes the AoS record kn[v], and counts
-// every digit of every key into a per-CTA smem histogram (hist_add: warp-aggregated,
-// flushed once per CTA).  Four independent nodes per thread and iteration: 4x the loads in
-// flight of one node per thread, every access still lane-contiguous.  The loop runs the
-// same trips on every lane of a warp (the histogram is a warp-wide operation).
+// every digit of every key into a per-CTA smem histogram (flushed once per CTA).
+// Four independent nodes per thread and iteration: 4x the loads in flight of one node
+// per thread, every access still lane-contiguous.
+//
+// The counting is one shared atomic per digit (hist_add mode 0).  Warp-aggregated
+// counting (PBIT_HIST_MODE 1: __match_any_sync groups, one atomic per distinct digit; 2:
+// lane 0's digit by __ballot_sync) was measured on B200 and loses: C3 pack 0.78 ms plain,
+// 6.65 ms match.any, 2.19 ms ballot; C5 4.0 / 17.5 / 8.1 ms.  The modes need
+// the whole warp in every trip, so they take the warp-uniform loop below.
 template <int KB>
 __device__ __forceinline__ void pack_one(unsigned long long k, uint32_t nx, uint32_t v, bool ok, uint32_t n_ids,
                                          typename Rec<KB>::T* __restrict__ kn, uint32_t* s_hist, int radix,
@@ -139,22 +144,42 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
   int bad = 0;
   const KT* __restrict__ kp = reinterpret_cast<const KT*>(keys);
   const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
-  const uint32_t lane = threadIdx.x & 31u;
-  for (unsigned long long v0 = tid - lane; v0 < n; v0 += (unsigned long long)U * stride) {  // warp-uniform
-    KT k[U];
-    uint32_t nx[U];
-    bool ok[U];
+  if constexpr (PBIT_HIST_MODE == 0) {
+    uint32_t v = tid;
+    for (; (unsigned long long)v + (U - 1) * (unsigned long long)stride < n; v += U * stride) {
+      KT k[U];
+      uint32_t nx[U];
 #pragma unroll
-    for (int e = 0; e < U; ++e) {
-      const unsigned long long v = v0 + lane + (unsigned long long)e * stride;
-      ok[e] = v < n;
-      k[e] = ok[e] ? __ldcs(kp + v) : KT(0);
-      nx[e] = ok[e] ? __ldcs(next + v) : 0u;
+      for (int e = 0; e < U; ++e) {
+        k[e] = __ldcs(kp + v + e * stride);
+        nx[e] = __ldcs(next + v + e * stride);
+      }
+#pragma unroll
+      for (int e = 0; e < U; ++e)
+        pack_one<KB>((unsigned long long)k[e], nx[e], v + e * stride, true, n_ids, kn, s_hist, radix, mask, K, D,
+                     km, bad);
     }
+    for (; v < n; v += stride)
+      pack_one<KB>((unsigned long long)kp[v], __ldcs(next + v), v, true, n_ids, kn, s_hist, radix, mask, K, D, km,
+                   bad);
+  } else {
+    const uint32_t lane = threadIdx.x & 31u;
+    for (unsigned long long v0 = tid - lane; v0 < n; v0 += (unsigned long long)U * stride) {  // warp-uniform
+      KT k[U];
+      uint32_t nx[U];
+      bool ok[U];
 #pragma unroll
-    for (int e = 0; e < U; ++e)
-      pack_one<KB>((unsigned long long)k[e], nx[e], (uint32_t)(v0 + lane + (unsigned long long)e * stride), ok[e],
-                   n_ids, kn, s_hist, radix, mask, K, D, km, bad);
+      for (int e = 0; e < U; ++e) {
+        const unsigned long long v = v0 + lane + (unsigned long long)e * stride;
+        ok[e] = v < n;
+        k[e] = ok[e] ? __ldcs(kp + v) : KT(0);
+        nx[e] = ok[e] ? __ldcs(next + v) : 0u;
+      }
+#pragma unroll
+      for (int e = 0; e < U; ++e)
+        pack_one<KB>((unsigned long long)k[e], nx[e], (uint32_t)(v0 + lane + (unsigned long long)e * stride), ok[e],
+                     n_ids, kn, s_hist, radix, mask, K, D, km, bad);
+    }
   }
   if (bad) atomicOr(err, E_BAD_INDEX);
   __syncthreads();
@@ -166,11 +191,12 @@ k_pack(const void* __restrict__ keys, const uint32_t* __restrict__ next, uint32_
 // Which rulers one walk launch handles and where their records go.  Ruler indices are
 // global (they index the segment table); slots are local to the launching GPU.
 //   static rulers  r in [r_lo, r_lo + n_static)   start at sel.node_of(r), slot r - r_lo
-//   the head       r = head_idx (unless NULL)      starts at the head,      slot n_static
+//   the head       r = head_idx (unless NULL)      starts at the head,      slot head_slot
 //   dynamic        r = dyn_base + k                opened by a cut segment, slot dyn_slot0 + k
-// Single GPU: r_lo = 0 and slot(r) = r (head_idx = R, dyn_base = dyn_slot0 = R_static).
+// Single GPU: r_lo = 0 and slot(r) = r (head_idx = head_slot = R, dyn_base = dyn_slot0 =
+// R_static).
 struct WalkMap {
-  uint32_t r_lo, n_static, head_idx, dyn_base, dyn_slot0;
+  uint32_t r_lo, n_static, head_idx, head_slot, dyn_base, dyn_slot0;
   __host__ __device__ __forceinline__ uint32_t count() const { return n_static + (head_idx != PBIT_NULL32 ? 1u : 0u); }
 };
 
@@ -231,7 +257,7 @@ k_walk(const __grid_constant__ KnSrc<typename Rec<KB>::T> src, RulerSel sel, Wal
     const bool is_head = i == wm.n_static;
     uint32_t u = is_head ? head : sel.node_of(wm.r_lo + i);
     uint32_t cur = is_head ? wm.head_idx : wm.r_lo + i, j = 0;  // j: records of segment `cur` already stored
-    RT* out = slots + (size_t)i * cap;
+    RT* out = slots + (size_t)(is_head ? wm.head_slot : i) * cap;
     for (;;) {
       // one group of up to B steps, unrolled so that buf[] is indexed statically
       uint32_t m = 0, succ = PBIT_NULL32;

@@ -50,6 +50,21 @@
 
 static_assert(sizeof(ncclUniqueId) == PBIT_MG_UNIQUE_ID_BYTES, "NCCL unique id size");
 
+// The ruling set of the multi-GPU walk: the single-GPU spacing for n nodes (make_plan), at
+// most 64 so that every rank's id slice (pbit_mg_slice: a multiple of 64) is a whole number
+// of ruler blocks (make_plan picks 128 from 2^30 nodes).  Exported for tests.
+extern "C" int pbit_mg_ruler_blocks(uint64_t n, int nranks, uint32_t* spacing, uint32_t* blocks_per_rank) {
+  if (!spacing || !blocks_per_rank || nranks < 1 || n > 0xFFFFFFFEull) return PBIT_ERR_INVALID_ARG;
+  pbit::SortPlan p;
+  pbit::make_plan(n, 32, 8, &p);
+  const int s_log2 = p.s_log2 > 6 ? 6 : p.s_log2;
+  const uint64_t S = pbit_mg_slice(n, nranks), s = 1ull << s_log2;
+  if (S % s || (uint64_t)nranks * (S / s) * s < n || (uint64_t)nranks * S > 0xFFFFFFFFull) return PBIT_ERR_UNSUPPORTED;
+  *spacing = (uint32_t)s;
+  *blocks_per_rank = (uint32_t)(S / s);
+  return PBIT_OK;
+}
+
 namespace pbit {
 
 namespace {
@@ -271,11 +286,8 @@ enum Transport { T_PEER = 0, T_NCCL = 1 };
 
 // PBIT_MG_TRANSPORT=nccl|peer (default: peer where the ranks can map each other)
 int transport_request() {
-  static const int v = [] {
-    const char* e = getenv("PBIT_MG_TRANSPORT");
-    return e && !strcmp(e, "nccl") ? (int)T_NCCL : (int)T_PEER;
-  }();
-  return v;
+  const char* e = getenv("PBIT_MG_TRANSPORT");  // read per call (tests switch it)
+  return e && !strcmp(e, "nccl") ? (int)T_NCCL : (int)T_PEER;
 }
 
 // pbit_sort_list_mg's own status for "the per-rank dynamic ruler table overflowed" (a list
@@ -302,18 +314,15 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
   SortPlan p;
   make_plan(n, KB * 8, K, &p);
-  // a rank's id slice must be a whole number of ruler blocks: S is a multiple of 64
-  // (pbit_mg_slice), so the spacing is at most 64 here (make_plan picks 128 from 2^30)
-  if (p.s_log2 > 6) p.s_log2 = 6;
-  p.R = (uint32_t)(((uint64_t)n + (1ull << p.s_log2) - 1) >> p.s_log2);
-  p.cap = 4u << p.s_log2;
-  const int radix = 1 << K;
-  const uint32_t s = 1u << p.s_log2;
-  const uint32_t bpr = S / s;                      // ruler blocks per rank
-  if ((uint64_t)G * bpr * s < (uint64_t)n || S % s) {
+  uint32_t s = 0, bpr = 0;
+  if (pbit_mg_ruler_blocks(n, G, &s, &bpr) != PBIT_OK) {
     set_last_error("pbit_sort_list_mg", "ruler blocks do not tile the rank slices");
     return PBIT_ERR_UNSUPPORTED;
   }
+  p.s_log2 = __builtin_ctz(s);
+  p.R = (uint32_t)(((uint64_t)n + s - 1) >> p.s_log2);
+  p.cap = 4u << p.s_log2;
+  const int radix = 1 << K;
   const uint32_t Gs = (uint32_t)G * bpr;           // static rulers (+1: the head's extra ruler)
   const uint32_t cap = p.cap;
   const uint32_t dcap = peer ? S / cap + 1 : 0u;   // dynamic rulers per rank (cut segments)
@@ -337,6 +346,10 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   const uint32_t NB = 2 * NS + 1;                  // splitter buckets
   const int W = with_prev ? 3 : 2;                 // relink record words
   const uint32_t n_static = p.R > r * bpr ? std::min(bpr, p.R - r * bpr) : 0u;
+  // one rank with the peer transport: its slots ARE the list (slot(r) = r, as on a single
+  // GPU), so the first local pass gathers its tiles from them and the relink reads the
+  // sorted ids directly -- nothing is exchanged
+  const bool solo = peer && G == 1;
   const uint32_t nslots = bpr + 1 + dcap;
 
   // ---- the window (peer transport): [kn slice][segment slots][recv keys][recv ids]; the
@@ -405,7 +418,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     bases_g = b.take<uint32_t>((size_t)D * radix);
     hist_r = b.take<uint32_t>((size_t)D * radix);
     bases_r = b.take<uint32_t>((size_t)D * radix);
-    part_first = b.take<uint32_t>(G + 2);
+    part_first = b.take<uint32_t>(solo ? ntiles + 2 : (size_t)G + 2);  // solo: per pass tile
     tile_ctr = b.take<uint32_t>(80);
     nseg = b.take<uint32_t>(1);
     zero = b.take<uint32_t>(1);
@@ -485,8 +498,8 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       KnSrc<RT> src{};
       for (int q = 0; q < G; ++q) src.peer[q] = (const RT*)wk(q, 0);
       src.S = FastDiv::make(S);
-      const WalkMap wm{r * bpr, n_static, own_head && !head_is_ruler ? Gs : PBIT_NULL32, Gs + 1 + (uint32_t)r * dcap,
-                       bpr + 1};
+      const WalkMap wm{r * bpr, n_static, own_head && !head_is_ruler ? Gs : PBIT_NULL32, bpr,
+                       Gs + 1 + (uint32_t)r * dcap, bpr + 1};
       const uint32_t total = wm.count();
       if (total) {
         static const int occ = [] {
@@ -537,17 +550,19 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       k_rank_check<<<1, 1, 0, st>>>(sdist[cur], ssucc[cur], head_sub, n, err);
       ++launches;
       k_rank_walk_b<<<sblocks, 256, 0, st>>>(seg, sub, Rmax, zero, 0, head_ruler, nsub, head_sub, sdist[cur],
-                                             scnt[cur], dist, seg_ord, seg_pos, part_first, S, n, nseg, err);
+                                             scnt[cur], dist, seg_ord, seg_pos, part_first,
+                                             solo ? (uint32_t)tile : S, n, nseg, err);
     }
 
     // ---- 4. the list-order chunk of positions [P0, P1)
-    if (m) {
+    if (cudaEventSynchronize(plan_ev) != cudaSuccess) { rc = PBIT_ERR_CUDA; goto done; }
+    if (m && (!solo || h_plan.npasses == 0)) {
       const int blocks = std::max(1, std::min((int)((m / 64 + 2 + 255) / 256), sms * 8));
       ++launches;
       if (peer) {
         PeerSlots ps{};
         for (int q = 0; q < G; ++q) ps.slots[q] = wk(q, a_kn);
-        MgRulers mr{FastDiv::make(bpr), FastDiv::make(std::max(dcap, 2u)), Gs, p.R, head_owner};
+        MgRulers mr{FastDiv::make(bpr), FastDiv::make(std::max(dcap, 1u)), Gs, head_owner};
         k_mg_gather<KB><<<blocks, 256, 0, st>>>(ps, mr, cap, seg, seg_ord, seg_pos, part_first, r, nseg, P0, P1,
                                                 keys_c, ids_c, err);
       } else {
@@ -632,24 +647,30 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     }
 
     // ---- 7. stable local sort of the received runs (the global plan's digits; the bases
-    // from the local histogram)
-    if (cudaEventSynchronize(plan_ev) != cudaSuccess) { rc = PBIT_ERR_CUDA; goto done; }
+    // from the local histogram -- one rank: the global one, and the first pass gathers
+    // from the slots)
     {
       uint32_t* ri_w = const_cast<uint32_t*>(ri);
       KeyT* rk_w = const_cast<KeyT*>(rk);
       fin = ri;
       const Plan hp = h_plan;
       if (m && hp.npasses) {
-        ++launches;
-        k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4, st>>>(
-            rk, m, K, D, hist_r, err);
-        ++launches;
-        k_plan<<<1, 256, 0, st>>>(hist_r, bases_r, plan_r, D, K, m, err);
+        if (!solo) {
+          ++launches;
+          k_chunk_hist<KeyT><<<std::max(1, std::min((int)((m + 255) / 256), sms * 4)), 256, (size_t)D * radix * 4,
+                               st>>>(rk, m, K, D, hist_r, err);
+          ++launches;
+          k_plan<<<1, 256, 0, st>>>(hist_r, bases_r, plan_r, D, K, m, err);
+        }
         SweepArgs la{};
         la.kin[0] = rk_w; la.kin[1] = kb1; la.vin[0] = ri_w; la.vin[1] = ib1;
         la.kout[0] = rk_w; la.kout[1] = kb1; la.vout[0] = ri_w; la.vout[1] = ib1;
-        la.bases = bases_r; la.status = status; la.tile_ctr = tile_ctr; la.err = err; la.n = m;
-        launch_key_passes_k<KB>(K, la, hp, false, st, nullptr, 0, SRC_TMA);
+        la.bases = solo ? bases_g : bases_r; la.status = status; la.tile_ctr = tile_ctr; la.err = err; la.n = m;
+        if (solo) {
+          la.slots = slots_own; la.cap = cap; la.seg = seg; la.seg_ord = seg_ord; la.seg_pos = seg_pos;
+          la.tile_first = part_first; la.nseg = nseg;
+        }
+        launch_key_passes_k<KB>(K, la, hp, false, st, nullptr, 0, solo ? SRC_GATHER : SRC_TMA);
         launches += hp.npasses;
         fin = (hp.npasses & 1u) ? ib1 : ri;
       }
@@ -662,7 +683,10 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     NCCLCHK(ncclAllGather(fl, fl_all, 2, ncclUint32, comm, st));
     ++launches;
     k_edges<<<1, 1, 0, st>>>(fl_all, (uint32_t)G, (uint32_t)r, edges);
-    {
+    if (solo) {  // every record is this rank's own: relink straight from the sorted ids
+      launches += launch_relink(fin, nullptr, 0, n, rbuf0, rbuf1, cursors, out_next_local,
+                                with_prev ? out_prev_local : nullptr, err, st, sms);
+    } else {
       const int pblocks = std::max(1, std::min((int)((m + 4095) / 4096), sms * 4));
       const FastDiv fS = FastDiv::make(S);
       PairDst pd{};

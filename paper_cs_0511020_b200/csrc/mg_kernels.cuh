@@ -10,19 +10,18 @@ namespace pbit {
 // ============================================================================ rulers
 // Which rank walked ruler r and where its records are in that rank's slots (the walk's
 // WalkMap of every rank, mg.cu): static rulers r < Gs belong to rank r / bpr (slot
-// r - q*bpr); the head's extra ruler Gs to the rank owning the head (slot = its number of
-// static rulers); rank q's dynamic rulers are Gs + 1 + q*dcap + k (slot bpr + 1 + k).
+// r - q*bpr); the head's extra ruler Gs to the rank owning the head (slot bpr); rank q's
+// dynamic rulers are Gs + 1 + q*dcap + k (slot bpr + 1 + k).  One rank: slot(r) = r.
 struct MgRulers {
   FastDiv bpr, dcap;
-  uint32_t Gs, R, head_owner;
+  uint32_t Gs, head_owner;
   __device__ __forceinline__ void locate(uint32_t r, uint32_t& q, uint32_t& slot) const {
     if (r < Gs) {
       q = bpr.div(r);
       slot = r - q * bpr.d;
     } else if (r == Gs) {
       q = head_owner;
-      const uint32_t first = q * bpr.d;
-      slot = R > first ? min(bpr.d, R - first) : 0u;
+      slot = bpr.d;
     } else {
       const uint32_t k = r - Gs - 1;
       q = dcap.div(k);

@@ -339,7 +339,7 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t per_cta = (R_static + blocks - 1) / blocks;
     KnSrc<RT> src{};
     src.kn = (const RT*)w.kn;
-    const WalkMap wm{0u, p.R, head_is_ruler ? PBIT_NULL32 : p.R, R_static, R_static};  // slot(r) = r
+    const WalkMap wm{0u, p.R, head_is_ruler ? PBIT_NULL32 : p.R, p.R, R_static, R_static};  // slot(r) = r
     launch_pdl(k_walk<KB, false>, blocks, WALK_THREADS, 0, st, src, sel, wm, head, (RT*)w.slots, p.cap,
                w.seg, w.dyn_count, p.dyn_cap, per_cta, w.err, debug_env("PBIT_DEBUG_WALK_NOWRITE"));
     ++launches;

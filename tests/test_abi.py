@@ -111,3 +111,19 @@ def test_header_limits_match_the_checks(pbit):
     oh = ctypes.c_uint32(7)
     p = np.zeros(4, np.uint32).ctypes.data
     assert lib.pbit_sort_list(p, p, 0, 0xFFFFFFFF, 32, ctypes.byref(oh), p, None) == 1
+
+
+def test_mg_ruler_blocks_tile_every_slice(pbit):
+    """from 2^30 nodes the single-GPU plan spaces rulers 128 apart, but
+    a rank's id slice is only a multiple of 64; the multi-GPU walk must use a spacing that
+    divides every slice, so that G * blocks * spacing covers all n nodes."""
+    for n in [1, 77, 4097, 1 << 24, (1 << 26) + 5, 1 << 30, (1 << 30) + 64, 3_000_000_000, (1 << 32) - 2]:
+        for G in [1, 2, 3, 5, 6, 7, 8, 13, 64]:
+            S = pbit.mg_slice(n, G)
+            if G * S > 0xFFFFFFFF:
+                with pytest.raises(pbit.PbitError):
+                    pbit.mg_ruler_blocks(n, G)
+                continue
+            sp, b = pbit.mg_ruler_blocks(n, G)
+            assert sp & (sp - 1) == 0 and sp <= 64 and S % sp == 0
+            assert b == S // sp and G * b * sp >= n

@@ -1,7 +1,8 @@
 """pbit_sort_list_mg through the C-ABI on the one GPU available: a 1-rank NCCL
-communicator runs every step of the multi-GPU protocol (pack + all-gather, count walk,
-segment-table exchange, ranking, emit walk, top-digit partition + exchange, local sort,
-stitch, owner routing, relink), compared bit-exactly with the oracle.  G > 1: the real
+communicator, with both transports -- peer (N4; one rank: the single-GPU pipeline inside
+the multi-GPU call) and NCCL (pack + all-gather, count walk, segment-table exchange,
+ranking, emit walk, local sort, stitch, owner routing, relink) -- compared bit-exactly
+with the oracle.  G > 1: the real
 kernels at G = 2-8 in tests/test_gpu_mg_threads.py (stand-in transport, one GPU), and the
 protocol on CPU in tests/test_mg_protocol.py (gloo, world_size 2-4)."""
 from __future__ import annotations
@@ -16,13 +17,21 @@ import workloads
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module")
-def mg(cuda_ok):
+@pytest.fixture(scope="module", params=["peer", "nccl"])
+def mg(cuda_ok, request):
+    import os
     import paper_cs_0511020_b200 as p
+    old = os.environ.get("PBIT_MG_TRANSPORT")
+    os.environ["PBIT_MG_TRANSPORT"] = request.param   # read by the library on every call
     uid = p.mg_unique_id()
     comm = p.mg_comm_init(1, uid, 0)
     yield p, comm
+    assert p.mg_transport(comm) == request.param
     p.mg_comm_destroy(comm)
+    if old is None:
+        os.environ.pop("PBIT_MG_TRANSPORT", None)
+    else:
+        os.environ["PBIT_MG_TRANSPORT"] = old
 
 
 CASES = [
