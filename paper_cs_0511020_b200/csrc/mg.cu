@@ -713,7 +713,12 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         CUDACHK(cudaMemcpyAsync(h_prow, pcntall + (size_t)r * G, 4ull * G, cudaMemcpyDeviceToHost, st));
         CUDACHK(cudaMemcpyAsync(h_psbase, psbase, 4ull * G, cudaMemcpyDeviceToHost, st));
         CUDACHK(cudaMemcpyAsync(h_precv, precv, 8ull * G, cudaMemcpyDeviceToHost, st));
+        CUDACHK(cudaMemcpyAsync(&hb->err, err, 4, cudaMemcpyDeviceToHost, st));
         MGWAIT();
+        // an invalid list stopped every kernel after the ranking (the error word is the same
+        // on every rank: all-reduced after the walk, then the same redundant ranking)
+        if (hb->err & E_DYN_FULL) { rc = RC_DYN_OVERFLOW; goto done; }
+        if (hb->err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
         uint64_t racc = 0;
         for (int d = 0; d < G; ++d) racc += h_precv[2 * d + 1];
         // the counts come from an all-gather, so every rank sees the same totals and takes

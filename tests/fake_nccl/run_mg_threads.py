@@ -46,6 +46,9 @@ CASES = [
     (3, 123457, 16, "uniform", "identity", 5, "signed", False, True),
     (8, 1 << 20, 32, "uniform", "random", 0, "unsigned", False, True),
     (5, 65536, 8, "uniform", "random", 4, "unsigned", False, False),
+    (6, 1000, 32, "zipf", "push", 0, "unsigned", False, True),          # ruler blocks > rulers
+    (4, (1 << 22) + 37, 32, "zipf", "random", 0, "unsigned", False, False),
+    (7, 777777, 64, "uniform", "random", 11, "signed", True, True),
 ]
 
 
@@ -140,6 +143,44 @@ def run_mismatch(G=3):
     return ok
 
 
+def run_invalid(G=3):
+    """A cycle through the head: every rank must return INVALID_LIST (the error word is
+    all-reduced, so no rank is left in an exchange) and leave its out_next untouched."""
+    n = 30011
+    nx_all = torch.arange(1, n + 1, dtype=torch.int32, device="cuda")
+    nx_all[-1] = 0
+    keys_all = torch.arange(n, dtype=torch.int32, device="cuda")
+    S = p.mg_slice(n, G)
+    uid = p.mg_unique_id()
+    codes, kept = [None] * G, [None] * G
+
+    def rank(r):
+        torch.cuda.set_device(0)
+        st = torch.cuda.Stream()
+        lo, hi = min(n, r * S), min(n, (r + 1) * S)
+        with torch.cuda.stream(st):
+            comm = p.mg_comm_init(G, uid, r)
+            out = torch.full((hi - lo,), 7, dtype=torch.int32, device="cuda")
+            try:
+                p.sort_list_mg(keys_all[lo:hi], nx_all[lo:hi], 0, n, r * S, comm, stream=st, out_next_local=out)
+                codes[r] = 0
+            except p.PbitError as e:
+                codes[r] = e.code
+            st.synchronize()
+            kept[r] = bool((out == 7).all())
+            p.mg_comm_destroy(comm)
+
+    ts = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=60)
+    ok = not any(t.is_alive() for t in ts) and codes == [2] * G and all(kept)
+    print(f"G={G} invalid list (cycle): codes {codes}, out_next untouched {kept}: {'ok' if ok else 'FAILED'}",
+          flush=True)
+    return ok
+
+
 def main(argv):
     cases = CASES
     if argv:  # e.g. "3,250001,32,zipf,random,0,unsigned,0,1"
@@ -156,6 +197,8 @@ def main(argv):
             os._exit(1)
     print(f"{len(cases) - fails}/{len(cases)} cases bit-exact", flush=True)
     if not argv and not run_mismatch():
+        fails += 1
+    if not argv and not run_invalid():
         fails += 1
     return 1 if fails else 0
 
