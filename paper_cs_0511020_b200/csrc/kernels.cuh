@@ -1387,13 +1387,13 @@ template <bool FROM_IDS, int W>
 __global__ void __launch_bounds__(512)
 k_relink_apply(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* __restrict__ recs, uint32_t n,
                uint32_t v_off, uint32_t* __restrict__ out_next, uint32_t* __restrict__ out_prev,
-               const int* __restrict__ err) {
+               const int* __restrict__ err, uint32_t bin0 = 0) {
   using R = typename RelinkRec<W>::T;
   pdl_enter();
   extern __shared__ __align__(16) uint32_t s_win[];  // [W - 1][2^RELINK_FINE_SHIFT]
   uint32_t* s_prev = s_win + (1u << RELINK_FINE_SHIFT);
   if (*err) return;
-  const uint32_t f0 = blockIdx.x << RELINK_FINE_SHIFT;
+  const uint32_t f0 = (bin0 + blockIdx.x) << RELINK_FINE_SHIFT;  // launches may cover a range of bins
   const uint32_t cnt = min((uint32_t)(1u << RELINK_FINE_SHIFT), n - f0);
   for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) {
     if constexpr (FROM_IDS) {

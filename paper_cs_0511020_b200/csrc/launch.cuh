@@ -142,10 +142,22 @@ static inline size_t relink_cursor_words(uint32_t n) {
 // or records (`recs`, v - v_off = local id; pairs if out_prev is NULL, else triples).
 // rbuf[2]: n records each (+16 B of padding); when the source is records it must not be
 // rbuf[0] (level 0 writes rbuf[0]).  Returns the number of kernels launched.
+// Host-buffer calls (pbit_sort_list with host pointers): the apply kernel runs in `chunks`
+// launches over consecutive ranges of fine bins, and each range of out_next (out_prev) is
+// copied to the host on `copy` as soon as its launch is done, overlapping the D2H with the
+// rest of the apply.
+struct RelinkD2H {
+  int chunks = 0;
+  cudaStream_t copy = nullptr;
+  cudaEvent_t* ev = nullptr;  // chunks events
+  uint32_t* h_next = nullptr;
+  uint32_t* h_prev = nullptr;
+};
+
 template <int W>
 static uint32_t launch_relink_w(const uint32_t* ids, const void* recs, uint32_t v_off, uint32_t n, void* rbuf0,
                                 void* rbuf1, uint32_t* cursors, uint32_t* out_next, uint32_t* out_prev,
-                                const int* err, cudaStream_t st, int sms) {
+                                const int* err, cudaStream_t st, int sms, const RelinkD2H* d2h = nullptr) {
   using R = typename RelinkRec<W>::T;
   constexpr size_t WIN = (size_t)(W - 1) * (4u << RELINK_FINE_SHIFT);
   static std::atomic<unsigned long long> attr{0};
@@ -190,15 +202,32 @@ static uint32_t launch_relink_w(const uint32_t* ids, const void* recs, uint32_t 
   }
   // the relink kernels are launched plainly: with PDL the waiting apply CTAs would take
   // SM room from the persistent partition kernel (C3 relink +0.04 ms, measured)
-  k_relink_apply<false, W><<<nfine, 512, WIN, st>>>(nullptr, in, n, 0, out_next, out_prev, err);
-  return (uint32_t)lv.L + 1;
+  if (!d2h || d2h->chunks <= 1) {
+    k_relink_apply<false, W><<<nfine, 512, WIN, st>>>(nullptr, in, n, 0, out_next, out_prev, err);
+    return (uint32_t)lv.L + 1;
+  }
+  const uint32_t per = (nfine + d2h->chunks - 1) / d2h->chunks;
+  uint32_t launched = (uint32_t)lv.L;
+  for (int c = 0; c < d2h->chunks; ++c) {
+    const uint32_t b0 = c * per, b1 = std::min(nfine, b0 + per);
+    if (b0 >= b1) break;
+    k_relink_apply<false, W><<<b1 - b0, 512, WIN, st>>>(nullptr, in, n, 0, out_next, out_prev, err, b0);
+    ++launched;
+    cudaEventRecord(d2h->ev[c], st);
+    cudaStreamWaitEvent(d2h->copy, d2h->ev[c], 0);
+    const size_t v0 = (size_t)b0 << RELINK_FINE_SHIFT, v1 = std::min((size_t)n, (size_t)b1 << RELINK_FINE_SHIFT);
+    cudaMemcpyAsync(d2h->h_next + v0, out_next + v0, (v1 - v0) * 4, cudaMemcpyDeviceToHost, d2h->copy);
+    if (W == 3) cudaMemcpyAsync(d2h->h_prev + v0, out_prev + v0, (v1 - v0) * 4, cudaMemcpyDeviceToHost, d2h->copy);
+  }
+  return launched;
 }
 
 static inline uint32_t launch_relink(const uint32_t* ids, const void* recs, uint32_t v_off, uint32_t n, void* rbuf0,
                                      void* rbuf1, uint32_t* cursors, uint32_t* out_next, uint32_t* out_prev,
-                                     const int* err, cudaStream_t st, int sms) {
-  return out_prev ? launch_relink_w<3>(ids, recs, v_off, n, rbuf0, rbuf1, cursors, out_next, out_prev, err, st, sms)
-                  : launch_relink_w<2>(ids, recs, v_off, n, rbuf0, rbuf1, cursors, out_next, nullptr, err, st, sms);
+                                     const int* err, cudaStream_t st, int sms, const RelinkD2H* d2h = nullptr) {
+  return out_prev
+             ? launch_relink_w<3>(ids, recs, v_off, n, rbuf0, rbuf1, cursors, out_next, out_prev, err, st, sms, d2h)
+             : launch_relink_w<2>(ids, recs, v_off, n, rbuf0, rbuf1, cursors, out_next, nullptr, err, st, sms, d2h);
 }
 
 }  // namespace pbit

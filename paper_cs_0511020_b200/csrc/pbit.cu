@@ -258,11 +258,41 @@ static size_t carve(const SortPlan& p, char* base, Ws* w) {
   return off;
 }
 
+// ----------------------------------------------------------------------------- host buffers
+// pbit_sort_list on host buffers: the keys and successors go to the device in HOSTIO_CHUNKS
+// copies on a second stream, each chunk packed as soon as it has landed, and out_next
+// (out_prev) comes back in as many copies, each as soon as the relink's apply kernel has
+// written its range of ids -- the copies overlap the pack and the apply instead of
+// bracketing the whole call.
+constexpr int HOSTIO_CHUNKS = 8;
+struct HostIO {
+  const void* h_keys;
+  const uint32_t* h_next;
+  uint32_t* h_out;
+  uint32_t* h_prev;
+  cudaStream_t copy;
+  cudaEvent_t* ev;  // HOSTIO_CHUNKS events
+  bool results_copied = false;  // set once the relink has queued the result copies
+};
+static void hostio_resources(cudaStream_t* copy, cudaEvent_t** ev) {
+  static thread_local cudaStream_t cs[64] = {};
+  static thread_local cudaEvent_t evs[64][HOSTIO_CHUNKS] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!cs[dev]) {
+    cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking);
+    for (int i = 0; i < HOSTIO_CHUNKS; ++i) cudaEventCreateWithFlags(&evs[dev][i], cudaEventDisableTiming);
+  }
+  *copy = cs[dev];
+  *ev = evs[dev];
+}
+
 // ----------------------------------------------------------------------------- the device path
 template <int KB>
 static int run_device(const void* keys, const uint32_t* next, uint32_t head, const SortPlan& p, uint32_t* out_next,
                       uint32_t* out_prev, uint32_t* out_head, cudaStream_t st, int sms, float* phase_ms,
-                      uint32_t* passes_run, uint32_t* launches_out) {
+                      uint32_t* passes_run, uint32_t* launches_out, HostIO* hio = nullptr) {
   using RT = typename Rec<KB>::T;
   Ws w;
   const size_t bytes = carve(p, nullptr, &w);
@@ -299,8 +329,28 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const size_t smem = (size_t)p.D * radix * 4;
     const int blocks = full_wave(k_pack<KB>, PACK_THREADS, smem, sms, (n + PACK_THREADS - 1) / PACK_THREADS);
     const KeyMap km{p.key_kind, p.descending};
-    launch_pdl(k_pack<KB>, blocks, PACK_THREADS, smem, st, keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
-    ++launches;
+    if (!hio) {
+      launch_pdl(k_pack<KB>, blocks, PACK_THREADS, smem, st, keys, next, n, n, (RT*)w.kn, w.hist, p.K, p.D, w.err, km);
+      ++launches;
+    } else {  // copy chunk c on the copy stream, pack it on st once it has landed
+      cudaEventRecord(hio->ev[0], st);  // the staging buffers were allocated on st
+      cudaStreamWaitEvent(hio->copy, hio->ev[0], 0);
+      const uint32_t per = (uint32_t)((((uint64_t)n + HOSTIO_CHUNKS - 1) / HOSTIO_CHUNKS + 255) & ~255ull);
+      for (int c = 0; c < HOSTIO_CHUNKS; ++c) {
+        const uint32_t v0 = c * per;
+        if (v0 >= n) break;
+        const uint32_t cnt = std::min(per, n - v0);
+        cudaMemcpyAsync((char*)keys + (size_t)v0 * KB, (const char*)hio->h_keys + (size_t)v0 * KB, (size_t)cnt * KB,
+                        cudaMemcpyHostToDevice, hio->copy);
+        cudaMemcpyAsync((uint32_t*)next + v0, hio->h_next + v0, (size_t)cnt * 4, cudaMemcpyHostToDevice, hio->copy);
+        cudaEventRecord(hio->ev[c], hio->copy);
+        cudaStreamWaitEvent(st, hio->ev[c], 0);
+        const int cb = full_wave(k_pack<KB>, PACK_THREADS, smem, sms, (cnt + PACK_THREADS - 1) / PACK_THREADS);
+        k_pack<KB><<<cb, PACK_THREADS, smem, st>>>((const char*)keys + (size_t)v0 * KB, next + v0, cnt, n,
+                                                    (RT*)w.kn + v0, w.hist, p.K, p.D, w.err, km);
+        ++launches;
+      }
+    }
   }
 #if PBIT_EARLY_PLAN
   // a3, early: the bucket bases and the pass plan depend only on the histograms, complete
@@ -385,6 +435,10 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
                (uint32_t)sweep_tile(p.key_bits), n, w.nseg, w.err);
     launches += 2;
     if (timing) cudaEventRecord(ev[PBIT_PHASE_RANK], st);
+    if (hio) {  // the error word is final once the ranking has validated the list
+      cudaMemcpyAsync(&hb->err, w.err, 4, cudaMemcpyDeviceToHost, st);
+      cudaEventRecord(hio->ev[HOSTIO_CHUNKS - 1], st);
+    }
   }
   // the host reads the pass plan once, so every pass gets its digit and parity as kernel
   // parameters and trivial digits are not launched
@@ -429,14 +483,31 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   nvtxRangePop();
   // a5: relink: (v, succ) pairs grouped by v's fine bin (MSD partition levels), then
   // each 2^14-id bin applied in a shared-memory window
-  if (ok && !sa.debug_no_lookback) {
+  // host buffers: the results are copied to the caller's arrays while the apply runs, so an
+  // invalid list must be known before the relink is queued (out_next is never touched
+  // then); the host waits for the ranking here while the passes run
+  const bool valid_for_copy = !hio || (cudaEventSynchronize(hio->ev[HOSTIO_CHUNKS - 1]) == cudaSuccess && hb->err == 0);
+  if (ok && valid_for_copy && !sa.debug_no_lookback) {
     NvtxRange nv("pbit.relink");
     const uint32_t* fin = w.ids[hplan.npasses & 1u];  // buffer holding the final ids
     launch_pdl(k_relink_head, 1, 1, 0, st, fin, w.d_head, w.err);
     ++launches;
     // N2: with out_prev the records are (v, succ, pred): both outputs in one chain
+    RelinkD2H d2h;
+    if (hio && RelinkLevels(n).L > 0) {
+      d2h.chunks = HOSTIO_CHUNKS;
+      d2h.copy = hio->copy;
+      d2h.ev = hio->ev;
+      d2h.h_next = hio->h_out;
+      d2h.h_prev = hio->h_prev;
+      hio->results_copied = true;
+    }
     launches += launch_relink(fin, nullptr, 0, n, w.pairs[0], w.pairs[1], w.cursors, out_next, out_prev, w.err, st,
-                              sms);
+                              sms, hio ? &d2h : nullptr);
+    if (hio && hio->results_copied) {  // the workspace and the staging buffers outlive the copies
+      cudaEventRecord(hio->ev[0], hio->copy);
+      cudaStreamWaitEvent(st, hio->ev[0], 0);
+    }
   }
   if (timing) cudaEventRecord(ev[PBIT_PHASE_RELINK], st);
 
@@ -536,14 +607,14 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
 
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
                 int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
-                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches) {
+                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches, HostIO* hio) {
   NvtxRange nv("pbit_sort_list");
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
   int sms = 0;
   if (int rc = device_info(dev, &sms)) return rc;
   init_rank_mode(st);
-  if (n <= SMALL_N && (K == 4 || K == 8) && rank_mode() == RANK_ATOMIC && !small_path_disabled()) {
+  if (n <= SMALL_N && (K == 4 || K == 8) && rank_mode() == RANK_ATOMIC && !small_path_disabled() && !hio) {
     const KeyMap km{key_kind, descending ? 1 : 0};
     const uint32_t n32 = (uint32_t)n;
     switch (key_bits) {
@@ -558,10 +629,10 @@ int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t 
   p.key_kind = key_kind;
   p.descending = descending ? 1 : 0;
   switch (key_bits) {
-    case 8: return run_device<1>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
-    case 16: return run_device<2>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
-    case 32: return run_device<4>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
-    default: return run_device<8>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches);
+    case 8: return run_device<1>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
+    case 16: return run_device<2>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
+    case 32: return run_device<4>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
+    default: return run_device<8>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
   }
 }
 
@@ -763,14 +834,22 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   if (ws_alloc((void**)&d, a + 3 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   uint32_t* d_prev = out_prev ? (uint32_t*)(d + a + 2 * b) : nullptr;
   int rc = PBIT_OK;
-  if (cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ||
-      cudaMemcpyAsync(d + a, next, nbytes, cudaMemcpyHostToDevice, st))
+  const bool small = n <= SMALL_N;  // the single-cluster path: plain copies around one launch
+  HostIO hio{keys, next, out_next, out_prev, nullptr, nullptr};
+  if (!small) {
+    int sms = 0;
+    if (device_info(dev, &sms)) rc = PBIT_ERR_CUDA;
+    hostio_resources(&hio.copy, &hio.ev);
+  } else if (cudaMemcpyAsync(d, keys, kbytes, cudaMemcpyHostToDevice, st) ||
+             cudaMemcpyAsync(d + a, next, nbytes, cudaMemcpyHostToDevice, st)) {
     rc = PBIT_ERR_CUDA;
+  }
   if (!rc) rc = sort_device(d, (const uint32_t*)(d + a), head, n, key_bits, K, key_kind, descending, out_head,
-                            (uint32_t*)(d + a + b), d_prev, st,
-                            phase_ms, passes_run, launches);
-  if (!rc && cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
-  if (!rc && out_prev && cudaMemcpyAsync(out_prev, d_prev, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+                            (uint32_t*)(d + a + b), d_prev, st, phase_ms, passes_run, launches, small ? nullptr : &hio);
+  if (!rc && !hio.results_copied) {
+    if (cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+    if (!rc && out_prev && cudaMemcpyAsync(out_prev, d_prev, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+  }
   cudaFreeAsync(d, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = PBIT_ERR_CUDA;
   cudaGetLastError();

@@ -282,6 +282,20 @@ def test_invalid_list_rejected_and_out_untouched(pbit, name, n, K):
         oracle.pbit_sort(keys.cpu().numpy().view(np.uint32), nx.cpu().numpy().view(np.uint32), 0, 32, 4)
 
 
+@pytest.mark.parametrize("name", ["cycle_through_head", "short", "index_ge_n", "two_predecessors"])
+def test_invalid_list_host_buffers_untouched(pbit, name):
+    """Host buffers (the e2e path copies results back while the relink runs): an invalid
+    list must leave the caller's host out_next untouched."""
+    n = 200003
+    nx = _bad_lists(n)[name].numpy().view(np.uint32)
+    keys = workloads.uniform_u32(nx.shape[0], 1, 1).numpy().astype(np.uint32)
+    out = np.full(nx.shape[0], 0x1234, np.uint32)
+    with pytest.raises(pbit.PbitError) as e:
+        pbit.sort_list(keys, nx, 0, out_next=out)
+    assert e.value.code == 2
+    assert (out == 0x1234).all(), "host out_next modified on INVALID_LIST"
+
+
 def test_invalid_args(pbit):
     k = torch.zeros(4, dtype=torch.int32, device="cuda")
     nx = torch.tensor([1, 2, 3, -1], dtype=torch.int32, device="cuda")
