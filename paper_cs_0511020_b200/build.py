@@ -48,16 +48,17 @@ def _newer(target, deps):
     return not os.path.exists(target) or any(os.path.getmtime(d) > os.path.getmtime(target) for d in deps)
 
 
-def objects(force: bool = False, verbose: bool = False) -> list:
+def objects(force: bool = False, verbose: bool = False, extra=(), objdir: str = OBJDIR) -> list:
     """Compile each source to build/obj/<name>.o, in parallel (the two sources take about
-    the same time); shared by libpbit.so and the tests' fake-NCCL build."""
-    os.makedirs(OBJDIR, exist_ok=True)
+    the same time); shared by libpbit.so and the tests' fake-NCCL build.  `extra` flags
+    (e.g. -DPBIT_BOUNDS_CHECK=1) go with their own objdir."""
+    os.makedirs(objdir, exist_ok=True)
     objs, procs = [], []
     for src in SOURCES:
-        obj = os.path.join(OBJDIR, os.path.splitext(src)[0] + ".o")
+        obj = os.path.join(objdir, os.path.splitext(src)[0] + ".o")
         objs.append(obj)
         if force or _newer(obj, _deps()):
-            cmd = ["nvcc", *_common_flags(), "-c", os.path.join(CSRC, src), "-o", obj + f".tmp{os.getpid()}"]
+            cmd = ["nvcc", *_common_flags(), *extra, "-c", os.path.join(CSRC, src), "-o", obj + f".tmp{os.getpid()}"]
             if verbose:
                 print(" ".join(cmd), file=sys.stderr)
             procs.append((obj, subprocess.Popen(cmd)))

@@ -3,8 +3,30 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #define PBIT_NULL32 0xFFFFFFFFu
+
+// Device-side bounds checks (compute-sanitizer is closed on this GPU pool): a build with
+// -DPBIT_BOUNDS_CHECK=1 traps on any index outside its buffer at the places where the
+// kernels compute addresses from data (slot offsets, scatter targets, window offsets, peer
+// ranks); the GPU test suite runs against that build too (tools/build_variants.py bounds=
+// -DPBIT_BOUNDS_CHECK=1, PBIT_LIB_PATH).  Compiled out otherwise.
+#ifndef PBIT_BOUNDS_CHECK
+#define PBIT_BOUNDS_CHECK 0
+#endif
+#if PBIT_BOUNDS_CHECK
+#define PBIT_ASSERT(cond)                                                                      \
+  do {                                                                                         \
+    if (!(cond)) {                                                                             \
+      printf("pbit bounds check failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,    \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                                     \
+      __trap();                                                                                \
+    }                                                                                          \
+  } while (0)
+#else
+#define PBIT_ASSERT(cond) do { } while (0)
+#endif
 
 namespace pbit {
 

@@ -276,6 +276,7 @@ k_walk(const __grid_constant__ KnSrc<typename Rec<KB>::T> src, RulerSel sel, Wal
           u = v;
         }
       }
+      PBIT_ASSERT(j + m <= cap);
       if (!no_writes) {
         uint4* o = reinterpret_cast<uint4*>(out + j);
         const uint4* bb = reinterpret_cast<const uint4*>(buf);
@@ -764,6 +765,7 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
       const uint32_t sr = __shfl_sync(0xffffffffu, r, q);
       const uint32_t sl = __shfl_sync(0xffffffffu, len, q);
       const uint32_t lo = max(P, sp), hi = min(E, sp + sl);
+      PBIT_ASSERT(hi <= lo || (hi - P <= (uint32_t)TILE && sl <= cap));
       if constexpr (!WIDE && PBIT_GATHER_BULK) {
         // a segment starting at an even list position has its records at the same 16 B
         // alignment in the slot and in the tile (slots and tiles start 16 B-aligned): one
@@ -1066,6 +1068,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
       const uint32_t g = sm.goff[split_bucket(sp, (unsigned long long)k)] + j;
       const uint32_t d = split_dest(sp, g);
       const uint32_t at = g + sp.dst_off[d];
+      PBIT_ASSERT(g < n && d < sp.G);
       reinterpret_cast<KeyT*>(sp.dst_k[d])[at] = k;
       sp.dst_i[d][at] = sm.iout[j];
     }
@@ -1113,6 +1116,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
       const KeyT k = sm.k[j];
       const uint32_t g = sm.goff[(uint32_t)(k >> shift) & (RADIX - 1)] + j;
+      PBIT_ASSERT(g < n);
       kout[g] = k;
       iout[g] = sm.iout[j];
     }
@@ -1120,6 +1124,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 #pragma unroll 4
     for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) {
       const uint32_t g = sm.goff[(uint32_t)sm.k[j]] + j;
+      PBIT_ASSERT(g < n);
       iout[g] = sm.iout[j];
     }
   }
@@ -1366,6 +1371,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* 
     for (uint32_t j = t; j < cnt; j += PART_THREADS) {
       const R p = sm.stage[j];
       const uint32_t b = (p.x >> shift) & mask;
+      PBIT_ASSERT(sm.gofs[b] + j < n);
       if constexpr (W == 2) __stcs(pout + (sm.gofs[b] + j), p);
       else pout[sm.gofs[b] + j] = p;
     }
@@ -1403,6 +1409,7 @@ k_relink_apply(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T*
       R p;
       if constexpr (W == 2) p = __ldcs(recs + f0 + i); else p = recs[f0 + i];
       const uint32_t v = p.x - v_off - f0;
+      PBIT_ASSERT(v < (1u << RELINK_FINE_SHIFT));
       s_win[v] = p.y;
       if constexpr (W == 3) s_prev[v] = p.z;
     }

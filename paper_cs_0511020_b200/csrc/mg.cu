@@ -562,7 +562,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       if (peer) {
         PeerSlots ps{};
         for (int q = 0; q < G; ++q) ps.slots[q] = wk(q, a_kn);
-        MgRulers mr{FastDiv::make(bpr), FastDiv::make(std::max(dcap, 1u)), Gs, head_owner};
+        MgRulers mr{FastDiv::make(bpr), FastDiv::make(std::max(dcap, 1u)), Gs, head_owner, cap};
         k_mg_gather<KB><<<blocks, 256, 0, st>>>(ps, mr, cap, seg, seg_ord, seg_pos, part_first, r, nseg, P0, P1,
                                                 keys_c, ids_c, err);
       } else {

@@ -14,7 +14,7 @@ namespace pbit {
 // dynamic rulers are Gs + 1 + q*dcap + k (slot bpr + 1 + k).  One rank: slot(r) = r.
 struct MgRulers {
   FastDiv bpr, dcap;
-  uint32_t Gs, head_owner;
+  uint32_t Gs, head_owner, cap;
   __device__ __forceinline__ void locate(uint32_t r, uint32_t& q, uint32_t& slot) const {
     if (r < Gs) {
       q = bpr.div(r);
@@ -151,6 +151,7 @@ k_mg_gather(const __grid_constant__ PeerSlots ps, MgRulers mr, uint32_t cap, con
         const uint32_t r = seg_ord[k], p = seg_pos[k], len = seg[r].x;
         uint32_t owner, slot;
         mr.locate(r, owner, slot);
+        PBIT_ASSERT(owner < 64 && len <= mr.cap);
         src[q] = reinterpret_cast<const RT*>(ps.slots[owner]) + (size_t)slot * cap;
         pos[q] = p;
         lo[q] = max(p, P0) - p;             // overlap with [P0, P1), relative to the segment
@@ -438,6 +439,7 @@ k_pairs_owner(const uint32_t* __restrict__ ids, uint32_t m, const uint32_t* __re
       rec.x = ids[p];
       rec.y = p + 1 < m ? ids[p + 1] : e_next;
       if constexpr (W == 3) rec.z = p > 0 ? ids[p - 1] : e_prev;
+      PBIT_ASSERT(o < G);
       reinterpret_cast<R*>(pd.dst[o])[s_base[o] + at] = rec;
     }
   }

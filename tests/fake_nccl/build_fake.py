@@ -22,16 +22,21 @@ def _product_build():
 
 
 def build(force: bool = False) -> str:
+    """PBIT_BOUNDS_CHECK=1 in the environment: the objects with device-side bounds checks
+    (their own objdir and library)."""
     b = _product_build()
-    objs = b.objects()  # the product's own objects (compiled once, shared with libpbit.so)
-    if not force and not b._newer(OUT, objs + [FAKE, __file__]):
-        return OUT
+    bounds = os.environ.get("PBIT_BOUNDS_CHECK") == "1"
+    out = OUT.replace(".so", "_bounds.so") if bounds else OUT
+    objs = (b.objects(extra=["-DPBIT_BOUNDS_CHECK=1"], objdir=b.OBJDIR + "_bounds") if bounds
+            else b.objects())  # the product's own objects (compiled once, shared with libpbit.so)
+    if not force and not b._newer(out, objs + [FAKE, __file__]):
+        return out
     inc, _ = b.nccl_dirs()
     fobj = os.path.join(b.OBJDIR, "fake_nccl.o")
     subprocess.check_call(["g++", "-std=c++17", "-O2", "-fPIC", f"-I{inc}", "-I/usr/local/cuda/include",
                            "-c", FAKE, "-o", fobj])
-    b.link(OUT, objs + [fobj], link_nccl=False, extra=["-Xlinker", "-Bsymbolic"])
-    return OUT
+    b.link(out, objs + [fobj], link_nccl=False, extra=["-Xlinker", "-Bsymbolic"])
+    return out
 
 
 if __name__ == "__main__":
