@@ -227,7 +227,8 @@ def run_reference(args):
             "scaling": "strong", "vs_baseline": None, "dtype": "u32" if c["key_bits"] <= 32 else "u64",
             "data": "synthetic",
             "config": dict(bench_config(args.config, sample_n, args.digit_bits or c["digit_bits"], args.gpus),
-                           sample_of_n=c["n"] if args.n is None else args.n),
+                           sample_of_n=c["n"] if args.n is None else args.n,
+                           parallelism="one host thread (the oracle, K=4)"),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "cpu": cpu_model(),
                              "host_threads": os.cpu_count(),
                              "sample": f"each step: a bounded sample of the workload, a {args.config}-shaped list "

@@ -1072,6 +1072,9 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
       reinterpret_cast<KeyT*>(sp.dst_k[d])[at] = k;
       sp.dst_i[d][at] = sm.iout[j];
     }
+    // the stores may go to other GPUs' memory (peer transport): make them visible at
+    // system scope before this kernel completes and the ranks' barrier collective runs
+    __threadfence_system();
   } else if (VEC && ((((uintptr_t)iout | (last ? 0 : (uintptr_t)kout)) & 15u) == 0)) {
     // 128-bit stores: every digit run is cut at 16 B boundaries of the OUTPUT arrays into
     // groups of 4 slots; thread q takes group q (its digit by binary search over the group

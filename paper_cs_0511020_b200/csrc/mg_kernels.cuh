@@ -443,6 +443,7 @@ k_pairs_owner(const uint32_t* __restrict__ ids, uint32_t m, const uint32_t* __re
       reinterpret_cast<R*>(pd.dst[o])[s_base[o] + at] = rec;
     }
   }
+  __threadfence_system();  // peer stores (the owner's window): visible before the barrier collective
 }
 
 // The routing plan of the relink records from the all-gathered counts (cntall[q][d] =
