@@ -202,9 +202,12 @@ int pbit_mg_comm_abort(void *comm);
 
 /* The transport pbit_sort_list_mg used on this communicator in its last call: 0 = peer
  * (N4: every rank maps the others' windows through CUDA IPC; the walk reads remote nodes
- * with peer loads and the exchanges are stores into the destination's memory), 1 = NCCL
- * (kn replica + ncclSend/ncclRecv; PBIT_MG_TRANSPORT=nccl forces it; also the fallback when
- * a rank cannot map the others).  -1 for a NULL communicator. */
+ * with peer loads and the exchanges are stores into the destination's memory), 2 = hybrid
+ * (PBIT_MG_TRANSPORT=hybrid: the peer transport with a kn replica by ncclAllGather walked
+ * locally), 1 = NCCL (kn replica + ncclSend/ncclRecv; PBIT_MG_TRANSPORT=nccl forces it; also
+ * the fallback when
+ * a rank cannot map the others, or when the peer transport's per-rank table of cut
+ * segments overflows).  -1 for a NULL communicator or one without a call yet. */
 int pbit_mg_transport(void *comm);
 
 /* The ruling set pbit_sort_list_mg uses for n nodes on nranks ranks: the ruler spacing (a

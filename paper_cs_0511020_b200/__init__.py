@@ -279,9 +279,10 @@ def mg_comm_abort(comm: int) -> None:
 
 
 def mg_transport(comm: int) -> str:
-    """"peer" (N4: CUDA IPC windows, peer loads and stores) or "nccl": the transport the
-    last sort_list_mg call on `comm` used (pbit.h pbit_mg_transport)."""
-    return {0: "peer", 1: "nccl"}.get(int(lib.pbit_mg_transport(ctypes.c_void_p(comm))), "none")
+    """"peer" (N4: CUDA IPC windows, peer loads and stores), "hybrid" (peer stores, a kn
+    replica walked locally) or "nccl": the transport the last sort_list_mg call on `comm`
+    used (pbit.h pbit_mg_transport)."""
+    return {0: "peer", 1: "nccl", 2: "hybrid"}.get(int(lib.pbit_mg_transport(ctypes.c_void_p(comm))), "none")
 
 
 def mg_ruler_blocks(n_global: int, nranks: int):

@@ -187,6 +187,7 @@ struct PeerWin {
 };
 std::mutex g_win_mu;
 std::map<void*, PeerWin> g_wins;
+std::map<void*, int> g_last_transport;  // the transport of each communicator's last call
 
 void win_release(PeerWin& w) {
   for (int q = 0; q < 64; ++q) {
@@ -282,12 +283,16 @@ int peer_window(ncclComm_t comm, int G, int r, size_t need, cudaStream_t st, Pee
   return PBIT_OK;
 }
 
-enum Transport { T_PEER = 0, T_NCCL = 1 };
+enum Transport { T_PEER = 0, T_NCCL = 1, T_HYBRID = 2 };
 
-// PBIT_MG_TRANSPORT=nccl|peer (default: peer where the ranks can map each other)
+// PBIT_MG_TRANSPORT=peer|hybrid|nccl (default: peer where the ranks can map each other).
+// hybrid = the peer transport with a kn replica (ncclAllGather) walked locally instead of
+// remote node reads -- for fabrics where small random peer reads are slow.
 int transport_request() {
   const char* e = getenv("PBIT_MG_TRANSPORT");  // read per call (tests switch it)
-  return e && !strcmp(e, "nccl") ? (int)T_NCCL : (int)T_PEER;
+  if (e && !strcmp(e, "nccl")) return T_NCCL;
+  if (e && !strcmp(e, "hybrid")) return T_HYBRID;
+  return T_PEER;
 }
 
 // pbit_sort_list_mg's own status for "the per-rank dynamic ruler table overflowed" (a list
@@ -304,7 +309,8 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   using KeyT = typename KeyOf<KB>::T;
   constexpr int REC_WORDS = sizeof(RT) / 4;
   const ncclDataType_t key_t = KB == 8 ? ncclUint64 : ncclUint32;
-  const bool peer = transport == T_PEER;
+  const bool peer = transport != T_NCCL;       // windows, slot walk, peer stores
+  const bool replica = transport != T_PEER;    // a kn replica by ncclAllGather (NCCL, hybrid)
   uint32_t launches = 0;
   int rc = PBIT_OK;
   int dev = 0, sms = 148;
@@ -387,7 +393,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   int* err = nullptr;
   size_t ctl_off = 0, ctl_end = 0;
   auto carve = [&]() {
-    if (!peer) kn_rep = b.take<RT>((size_t)G * S);
+    if (replica) kn_rep = b.take<RT>((size_t)G * S);
     seg = b.take<uint2>(Rmax);
     dist = b.take<uint32_t>(Rmax);
     seg_ord = b.take<uint32_t>(Rmax);
@@ -462,6 +468,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   MgBox* hb = mg_box();
   const Plan& h_plan = hb->plan;
   uint32_t h_left[66] = {}, h_srecv[128] = {}, h_prow[64] = {}, h_psbase[64] = {}, h_precv[128] = {};
+  std::vector<uint32_t> h_pall((size_t)G * G);
   SplitTable h_split{};
   cudaEvent_t plan_ev = nullptr;
   const KeyT* rk = nullptr;
@@ -474,7 +481,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
     // ---- 1. pack the own slice; histograms of every digit of every key
     {
-      RT* kn_own = peer ? (RT*)win->local : kn_rep + lo;
+      RT* kn_own = replica ? kn_rep + lo : (RT*)win->local;
       if (n_local) {
         const int blocks = full_wave(k_pack<KB>, PACK_THREADS, (size_t)D * radix * 4, sms,
                                      (n_local + PACK_THREADS - 1) / PACK_THREADS);
@@ -482,7 +489,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         k_pack<KB><<<blocks, PACK_THREADS, (size_t)D * radix * 4, st>>>(keys_local, next_local, n_local, n, kn_own,
                                                                          hist_l, K, D, err, km);
       }
-      if (!peer) NCCLCHK(ncclAllGather(kn_rep + lo, kn_rep, (size_t)S * REC_WORDS, ncclUint32, comm, st));
+      if (replica) NCCLCHK(ncclAllGather(kn_rep + lo, kn_rep, (size_t)S * REC_WORDS, ncclUint32, comm, st));
       NCCLCHK(ncclAllReduce(hist_l, hist_g, (size_t)D * radix, ncclUint32, ncclSum, comm, st));
       // the global pass plan (a digit trivial globally is trivial on every rank): read by
       // the host while the walk, the ranking and the exchange run
@@ -498,6 +505,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       KnSrc<RT> src{};
       for (int q = 0; q < G; ++q) src.peer[q] = (const RT*)wk(q, 0);
       src.S = FastDiv::make(S);
+      src.kn = kn_rep;  // hybrid: the replica, read locally
       const WalkMap wm{r * bpr, n_static, own_head && !head_is_ruler ? Gs : PBIT_NULL32, bpr,
                        Gs + 1 + (uint32_t)r * dcap, bpr + 1};
       const uint32_t total = wm.count();
@@ -511,8 +519,12 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         if ((uint32_t)blocks * 4 > total) blocks = std::max(1u, (total + 3) / 4);
         const uint32_t per = (total + blocks - 1) / blocks;
         ++launches;
-        k_walk<KB, true><<<blocks, WALK_THREADS, 0, st>>>(src, sel, wm, head, slots_own, cap, seg, dyn_count, dcap,
-                                                          per, err, 0);
+        if (replica)
+          k_walk<KB, false><<<blocks, WALK_THREADS, 0, st>>>(src, sel, wm, head, slots_own, cap, seg, dyn_count, dcap,
+                                                             per, err, 0);
+        else
+          k_walk<KB, true><<<blocks, WALK_THREADS, 0, st>>>(src, sel, wm, head, slots_own, cap, seg, dyn_count, dcap,
+                                                            per, err, 0);
       }
     } else {
       const uint32_t b_lo = r * bpr, b_hi = (r + 1) * bpr;
@@ -710,6 +722,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       if (peer) {
         NCCLCHK(ncclAllReduce(barrier_w, barrier_w + 1, 1, ncclUint32, ncclSum, comm, st));
       } else {
+        CUDACHK(cudaMemcpyAsync(h_pall.data(), pcntall, 4ull * G * G, cudaMemcpyDeviceToHost, st));
         CUDACHK(cudaMemcpyAsync(h_prow, pcntall + (size_t)r * G, 4ull * G, cudaMemcpyDeviceToHost, st));
         CUDACHK(cudaMemcpyAsync(h_psbase, psbase, 4ull * G, cudaMemcpyDeviceToHost, st));
         CUDACHK(cudaMemcpyAsync(h_precv, precv, 8ull * G, cudaMemcpyDeviceToHost, st));
@@ -719,11 +732,14 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
         // on every rank: all-reduced after the walk, then the same redundant ranking)
         if (hb->err & E_DYN_FULL) { rc = RC_DYN_OVERFLOW; goto done; }
         if (hb->err) { rc = PBIT_ERR_INVALID_LIST; goto done; }
-        uint64_t racc = 0;
-        for (int d = 0; d < G; ++d) racc += h_precv[2 * d + 1];
-        // the counts come from an all-gather, so every rank sees the same totals and takes
-        // the same branch here (no rank is left waiting in the exchange below)
-        if (racc != n_local) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
+        // every rank checks EVERY rank's receive total against its node count, from the same
+        // all-gathered matrix, so all take the same branch (none is left in the exchange)
+        for (int d = 0; d < G; ++d) {
+          uint64_t racc = 0;
+          for (int q = 0; q < G; ++q) racc += h_pall[(size_t)q * G + d];
+          const uint64_t lo_d = std::min<uint64_t>(n, (uint64_t)d * S), hi_d = std::min<uint64_t>(n, (uint64_t)(d + 1) * S);
+          if (racc != hi_d - lo_d) { set_last_error("pbit_sort_list_mg", "relink routing mismatch"); rc = PBIT_ERR_CUDA; goto done; }
+        }
         NcclGroup grp;
         NCCLCHK(grp.start());
         for (int d = 0; d < G; ++d) {
@@ -784,6 +800,7 @@ int pbit_mg_comm_init(void** comm_out, int nranks, const void* id, int rank) {
 
 static void release_window(void* comm) {
   std::lock_guard<std::mutex> lk(g_win_mu);
+  g_last_transport.erase(comm);
   auto it = g_wins.find(comm);
   if (it != g_wins.end()) {
     win_release(it->second);
@@ -947,9 +964,13 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
 #undef PBIT_RUN_MG
     // the peer transport is unavailable (some rank cannot map the others' memory), or its
     // per-rank dynamic ruler table overflowed: every rank saw the same verdict -> NCCL
-    if (transport == T_PEER && (rc == PBIT_ERR_UNSUPPORTED || rc == RC_DYN_OVERFLOW)) {
+    if (transport != T_NCCL && (rc == PBIT_ERR_UNSUPPORTED || rc == RC_DYN_OVERFLOW)) {
       transport = T_NCCL;
       continue;
+    }
+    {
+      std::lock_guard<std::mutex> lk(g_win_mu);
+      g_last_transport[(void*)comm] = transport;
     }
     return rc;
   }
@@ -958,8 +979,8 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
 int pbit_mg_transport(void* comm) {
   if (!comm) return -1;
   std::lock_guard<std::mutex> lk(g_win_mu);
-  auto it = g_wins.find(comm);
-  return (it != g_wins.end() && it->second.local) ? 0 : 1;
+  auto it = g_last_transport.find(comm);
+  return it == g_last_transport.end() ? -1 : it->second;
 }
 
 }  // extern "C"

@@ -181,6 +181,75 @@ def run_invalid(G=3):
     return ok
 
 
+def _is_ruler(v, n, s_log2):
+    """The ruling-set selection of the product (common.cuh RulerSel), restated to BUILD an
+    adversarial input (not to check an output)."""
+    M = 0xFFFFFFFF
+    r = v >> s_log2
+    x = r ^ 0x6A09E667
+    x ^= x >> 16
+    x = (x * 0x21F0AAAD) & M
+    x ^= x >> 15
+    x = (x * 0x735A2D97) & M
+    x ^= x >> 15
+    s = 1 << s_log2
+    span = n - (r << s_log2)
+    off = (x & (s - 1)) if span >= s else x % span
+    return (v & (s - 1)) == off
+
+
+def run_dyn_overflow(G=2, n=120011):
+    """A list whose rank-0 rulers head two segments covering almost every other node: rank
+    0 must cut far more segments than its dynamic-ruler table holds (peer transport), the
+    ranks see the overflow in the all-reduced error word and redo the call on the NCCL
+    transport -- still bit-exact."""
+    spacing, _ = p.mg_ruler_blocks(n, G)
+    s_log2 = spacing.bit_length() - 1
+    S = p.mg_slice(n, G)
+    rul = np.array([_is_ruler(v, n, s_log2) for v in range(n)])
+    ids = np.arange(n)
+    A = ids[(ids < S) & rul]
+    B = ids[(ids >= S) & rul]
+    C0 = ids[(ids < S) & ~rul]
+    C1 = ids[(ids >= S) & ~rul]
+    order = np.concatenate([A[:1], C1, A[1:], C0, B]).astype(np.int64)
+    assert len(order) == n and len(np.unique(order)) == n
+    nxt = np.full(n, 0xFFFFFFFF, np.uint32)
+    nxt[order[:-1]] = order[1:]
+    keys = (np.arange(n, dtype=np.uint64) * 2654435761 % 1000).astype(np.uint32)
+    kd = torch.from_numpy(keys.view(np.int32)).cuda()
+    nd = torch.from_numpy(nxt.view(np.int32)).cuda()
+    head = int(order[0])
+    uid = p.mg_unique_id()
+    res, errs = [None] * G, [None] * G
+
+    def rank(r):
+        try:
+            torch.cuda.set_device(0)
+            st = torch.cuda.Stream()
+            lo, hi = min(n, r * S), min(n, (r + 1) * S)
+            with torch.cuda.stream(st):
+                comm = p.mg_comm_init(G, uid, r)
+                h, out = p.sort_list_mg(kd[lo:hi], nd[lo:hi], head, n, r * S, comm, key_bits=32, stream=st)
+                st.synchronize()
+                res[r] = (h, out.cpu().numpy().view(np.uint32).copy(), p.mg_transport(comm))
+                p.mg_comm_destroy(comm)
+        except Exception as e:  # noqa: BLE001
+            errs[r] = e
+
+    ts = [threading.Thread(target=rank, args=(r,), daemon=True) for r in range(G)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout=120)
+    oh, on = oracle.pbit_sort(keys, nxt, head, 32, 4)
+    ok = (not any(t.is_alive() for t in ts) and not any(errs) and {x[0] for x in res} == {oh}
+          and np.array_equal(np.concatenate([x[1] for x in res]), on) and {x[2] for x in res} == {"nccl"})
+    print(f"G={G} dynamic-ruler overflow on the peer transport: {'ok (fell back to nccl)' if ok else 'FAILED'} "
+          f"{[repr(e) for e in errs if e]} {[x[2] for x in res if x]}", flush=True)
+    return ok
+
+
 def main(argv):
     cases = CASES
     if argv:  # e.g. "3,250001,32,zipf,random,0,unsigned,0,1"
@@ -199,6 +268,8 @@ def main(argv):
     if not argv and not run_mismatch():
         fails += 1
     if not argv and not run_invalid():
+        fails += 1
+    if not argv and os.environ.get("PBIT_MG_TRANSPORT", "peer") in ("peer", "hybrid") and not run_dyn_overflow():
         fails += 1
     return 1 if fails else 0
 

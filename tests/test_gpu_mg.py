@@ -17,7 +17,7 @@ import workloads
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(scope="module", params=["peer", "nccl"])
+@pytest.fixture(scope="module", params=["peer", "hybrid", "nccl"])
 def mg(cuda_ok, request):
     import os
     import paper_cs_0511020_b200 as p

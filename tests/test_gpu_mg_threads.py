@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-@pytest.mark.parametrize("transport", ["peer", "nccl"])
+@pytest.mark.parametrize("transport", ["peer", "hybrid", "nccl"])
 def test_mg_multi_rank_threads_vs_oracle(cuda_ok, transport):
     """Both transports (N4 peer windows, and the NCCL reference) bit-exact with the oracle,
     hence with each other."""
