@@ -58,7 +58,7 @@ def _input_sha(li):
 
 def test_golden_files_complete():
     """Every BASELINE config and the extra large cases have an oracle golden (CPU test)."""
-    for name in ["C1", "C2", "C3", "C4", "C5", "X26", "X26u64"]:
+    for name in ["C1", "C2", "C3", "C4", "C5", "X26", "X26u64", "ctx"]:
         assert name in GOLD, f"missing tests/golden/config_{name}.json (run tools/make_goldens.py {name})"
         g = GOLD[name]
         assert g["oracle_K"] == 4 and len(g["out_next_sha256"]) == 64
@@ -75,8 +75,9 @@ def test_golden_c1_matches_oracle_here():
 
 # every config at its BASELINE digit width; the extra cases also at the paper's K = 4 and
 # at a width that does not divide the key (K = 11 as 8-bit sub-passes, reading Q7)
-CASES = [(c, None) for c in ["C1", "C2", "C3", "C4", "C5", "X26", "X26u64"]] + [
-    ("X26", 4), ("X26", 6), ("X26u64", 11), ("C3", 4)]
+CASES = [(c, None) for c in ["C1", "C2", "C3", "C4", "C5", "X26", "X26u64", "ctx"]] + [
+    ("X26", 4), ("X26", 6), ("X26u64", 11), ("C3", 4),
+    ("ctx", 8), ("ctx", 16)]  # the paper's own workload at its K = 4 (default), 8 and 16
 
 
 @pytest.mark.gpu
@@ -100,3 +101,25 @@ def test_full_size_bit_exact_vs_oracle_golden(cuda_ok, name, K):
         order = oracle.list_order(on, h)
         seq = payload.cpu().numpy()[order]
         assert hashlib.sha256(seq.tobytes()).hexdigest() == g["payload_seq_sha256"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("transport", ["peer", "hybrid", "nccl"])
+def test_mg_one_rank_full_size_c3_vs_oracle_golden(cuda_ok, transport, monkeypatch):
+    """pbit_sort_list_mg on a real 1-rank NCCL communicator, every transport, on the full
+    C3 list: the oracle's bytes."""
+    import paper_cs_0511020_b200 as pbit
+    monkeypatch.setenv("PBIT_MG_TRANSPORT", transport)   # read by the library on every call
+    g = GOLD["C3"]
+    li = _make("C3", g, "cuda")
+    comm = pbit.mg_comm_init(1, pbit.mg_unique_id(), 0)
+    try:
+        h, out = pbit.sort_list_mg(li.keys, li.next, li.head, li.n, 0, comm, digit_bits=8)
+        torch.cuda.synchronize()
+        assert pbit.mg_transport(comm) == transport
+    finally:
+        pbit.mg_comm_destroy(comm)
+    on = out.cpu().numpy().view(np.uint32)
+    del li, out
+    torch.cuda.empty_cache()
+    assert h == g["out_head"] and hashlib.sha256(on.tobytes()).hexdigest() == g["out_next_sha256"]
