@@ -62,6 +62,11 @@ constexpr int SWEEP_IPT32 = PBIT_SWEEP_IPT;                       // items per t
 constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 // write-out of the stable passes: 128-bit stores over 16 B-aligned groups of every digit
 // run (1), or one 4 B store per element, consecutive threads on consecutive elements (0)
+// in-warp ranking: branch on the warp-uniform "all lanes share one digit" test (1) or
+// select the addend per lane and skip zero addends (0)
+#ifndef PBIT_RANK_UNIBRANCH
+#define PBIT_RANK_UNIBRANCH 1
+#endif
 #ifndef PBIT_VEC_STORE
 #define PBIT_VEC_STORE 0
 #endif
@@ -689,8 +694,30 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
       // share one digit (equal-key runs) lets lane 0 add 32 instead of serialising.
       const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
       const bool uni = __all_sync(0xffffffffu, d == d0 && valid);
-      const uint32_t add = uni ? (lane == 0 ? 32u : 0u) : (valid ? 1u : 0u);
       uint32_t r = 0;
+#if PBIT_RANK_UNIBRANCH
+      // `uni` is warp-uniform: branch on it, so that a full tile's common case (every lane
+      // adds 1) issues its atomic without a per-lane predicate or reconvergence barrier
+      if (uni) {
+        if (lane == 0) {
+          if constexpr (sizeof(WCnt) == 4) {
+            r = atomicAdd(reinterpret_cast<uint32_t*>(wrow + d), 32u);
+          } else {
+            const uint32_t sh = (d & 1u) << 4;
+            r = (atomicAdd(reinterpret_cast<uint32_t*>(wrow) + (d >> 1), 32u << sh) >> sh) & 0xFFFFu;
+          }
+        }
+        r = __shfl_sync(0xffffffffu, r, 0) + lane;
+      } else if (FULL || valid) {
+        if constexpr (sizeof(WCnt) == 4) {
+          r = atomicAdd(reinterpret_cast<uint32_t*>(wrow + d), 1u);
+        } else {
+          const uint32_t sh = (d & 1u) << 4;
+          r = (atomicAdd(reinterpret_cast<uint32_t*>(wrow) + (d >> 1), 1u << sh) >> sh) & 0xFFFFu;
+        }
+      }
+#else
+      const uint32_t add = uni ? (lane == 0 ? 32u : 0u) : (valid ? 1u : 0u);
       if constexpr (sizeof(WCnt) == 4) {
         if (add) r = atomicAdd(reinterpret_cast<uint32_t*>(wrow + d), add);
       } else {  // two u16 counters per word
@@ -700,6 +727,7 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
       }
       const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0);
       r = uni ? r0 + lane : r;
+#endif
       rd[i] = r | (d << 16);
     } else {
       const uint32_t vmask = FULL ? 0xffffffffu : __ballot_sync(0xffffffffu, valid);
