@@ -190,8 +190,15 @@ def cpu_baseline(cfg: str, sample_n: int, reps: int = 1):
         oracle.pbit_sort(keys, nxt, li.head, c["key_bits"], 4)
         ts.append(time.perf_counter() - t0)
     t = statistics.mean(ts)
+    # SURVEY §8(d)'s optional variant: the recursion below the first two levels on every
+    # host core (bit-identical to the serial oracle, tests/test_oracle.py)
+    nthr = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oracle.pbit_sort_par(keys, nxt, li.head, c["key_bits"], 4, nthr)
+    tp = time.perf_counter() - t0
     return {"value": sample_n / t, "unit": UNIT, "cores": 1, "kind": "oracle",
             "cpu": cpu_model(), "host_threads": os.cpu_count(),
+            "subtree_parallel": {"value": sample_n / tp, "unit": UNIT, "cores": nthr, "seconds": round(tp, 2)},
             "sample": f"{cfg}-shaped list, n={sample_n} of the config's {c['n']} (seed {c['seed']}), "
                       f"paper-literal Pbit K=4, mean of {reps} run(s), {t:.2f} s each, single thread",
             "full_size": full_size_oracle(cfg)}

@@ -15,6 +15,7 @@ from .oracle import (  # noqa: F401
     list_order,
     memory_bound_T,
     pbit_sort,
+    pbit_sort_par,
     repair_back,
     split_once,
     validate_list,

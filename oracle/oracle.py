@@ -44,7 +44,7 @@ def build(force: bool = False) -> str:
     """Compile liboracle.so with gcc (-O2, plain C11) if missing or stale."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", tmp, _SRC])
+        subprocess.check_call(["gcc", "-O2", "-std=gnu11", "-fPIC", "-shared", "-pthread", "-o", tmp, _SRC])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -70,6 +70,9 @@ def _load():
                                               ctypes.c_uint64, ctypes.c_uint, ctypes.c_void_p]
             lib.oracle_validate_list.restype = ctypes.c_int
             lib.oracle_validate_list.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64]
+            lib.oracle_pbit_sort_par.restype = ctypes.c_int
+            lib.oracle_pbit_sort_par.argtypes = [ctypes.c_void_p, ctypes.c_int, ctypes.c_void_p, ctypes.c_uint32,
+                                                 ctypes.c_uint64, ctypes.c_uint, ctypes.c_int, u32p, ctypes.c_void_p]
             lib.oracle_list_order.restype = ctypes.c_int
             lib.oracle_list_order.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_void_p]
             lib.oracle_bits.restype = ctypes.c_uint64
@@ -121,6 +124,22 @@ def pbit_sort(keys, next_, head: int, key_bits: int, K: int = 4, descending: boo
         raise OracleError(rc)
     res = (int(oh.value), out[:n])
     return res + (c.as_dict(),) if with_counters else res
+
+
+def pbit_sort_par(keys, next_, head: int, key_bits: int, K: int = 4, threads: int = 0):
+    """The same ascending sort with the recursion below the first two levels on `threads`
+    host threads (0 = every core); bit-identical to pbit_sort.  Returns (out_head, out_next)."""
+    lib = _load()
+    nxt = np.ascontiguousarray(next_, dtype=np.uint32)
+    n = int(nxt.shape[0])
+    k = _keys(keys, key_bits) if n else np.zeros(1, _KEY_DTYPES.get(key_bits, np.uint8))
+    out = np.empty(max(n, 1), np.uint32)
+    oh = ctypes.c_uint32(0)
+    rc = lib.oracle_pbit_sort_par(k.ctypes.data, key_bits, nxt.ctypes.data if n else None, head & 0xFFFFFFFF, n, K,
+                                  threads, ctypes.byref(oh), out.ctypes.data)
+    if rc:
+        raise OracleError(rc)
+    return int(oh.value), out[:n]
 
 
 def repair_back(next_, head: int):

@@ -21,9 +21,11 @@
  * direction duality and the reverse-stability of odd M/K (Q1).
  * Nothing here is "parity unpinned".
  */
+#include <pthread.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
+#include <unistd.h>
 
 #define ORACLE_NULL 0xFFFFFFFFu
 
@@ -188,6 +190,134 @@ int oracle_pbit_sort(const void *keys, int key_bits, const uint32_t *next, uint3
     free(x.tabs);
     if (counters) *counters = x.c;
     return ORACLE_OK;
+}
+
+/* ---------------------------------------------------------------- subtree-parallel baseline
+ * The same sort on several host threads (an optional CPU baseline on nproc
+ * threads whose output must be bit-identical).  The first two levels of the recursion run
+ * exactly as Pbit runs them -- the split loop of P:351-353 at M-K, then at M-2K on every
+ * bucket -- which leaves Omega^2 independent sublists, in list order (b1, b2) ascending
+ * (the ascending loops of P:379-380 put bucket 0 first).  Each sublist's own recursion
+ * Pbit(L, M-2K, NULL) runs on one of the threads: Pbit(L, M, P) is Pbit(L, M, NULL)
+ * followed by P (the end marker is only ever spliced behind the last node), so
+ * linking every sorted sublist's tail to the next one's head reproduces the serial result
+ * node for node.  Ascending unsigned keys only (the cpu_baseline's sort). */
+typedef struct {
+    const ctx_t *proto;      /* keys, K, omega, next */
+    unsigned M2;             /* bits left below the first two levels */
+    const uint32_t *tab1;    /* the level-1 buckets */
+    uint32_t *lists;         /* Omega^2 sublist heads (level-2 buckets) */
+    uint32_t *heads, *tails; /* per sublist: sorted head and tail */
+    int phase;               /* 0: split the level-1 buckets; 1: sort the sublists */
+    uint32_t njobs;
+    uint32_t next_job;       /* shared job counter */
+    pthread_mutex_t mu;
+    int oom;
+} par_t;
+
+static void *par_worker(void *arg) {
+    par_t *w = (par_t *)arg;
+    ctx_t x = *w->proto;
+    memset(&x.c, 0, sizeof x.c);
+    x.depth = x.live = 0;
+    unsigned levels = w->M2 / x.K + 1;
+    x.tabs = (uint32_t *)malloc((size_t)levels * x.omega * sizeof(uint32_t));
+    for (;;) {
+        pthread_mutex_lock(&w->mu);
+        uint32_t j = w->next_job++;
+        if (!x.tabs) w->oom = 1;
+        pthread_mutex_unlock(&w->mu);
+        if (j >= w->njobs || !x.tabs) break;
+        if (w->phase == 0) {  /* level 2: the split loop on level-1 bucket j, M2 = M - 2K */
+            uint32_t *tab2 = w->lists + (size_t)j * x.omega;
+            for (uint32_t b = 0; b < x.omega; ++b) tab2[b] = ORACLE_NULL;
+            for (uint32_t i, L = w->tab1[j]; (i = L) != ORACLE_NULL; ) {
+                uint32_t *in = tab2 + oracle_bits(key_of(&x, L), w->M2, x.K);
+                L = x.next[L];
+                x.next[i] = *in; *in = i;
+            }
+            continue;
+        }
+        uint32_t L = w->lists[j];
+        uint32_t h = (w->M2 && L != ORACLE_NULL) ? Pbit(&x, L, w->M2, ORACLE_NULL, 0) : L;
+        uint32_t t = h;
+        if (t != ORACLE_NULL)
+            while (x.next[t] != ORACLE_NULL) t = x.next[t];
+        w->heads[j] = h;
+        w->tails[j] = t;
+    }
+    free(x.tabs);
+    return NULL;
+}
+
+static int par_run(par_t *w, pthread_t *th, int nthreads) {
+    w->next_job = 0;
+    int started = 0;
+    for (int t = 0; t < nthreads; ++t)
+        if (pthread_create(&th[t], NULL, par_worker, w) == 0) ++started;
+    if (!started) par_worker(w);
+    for (int t = 0; t < started; ++t) pthread_join(th[t], NULL);
+    return w->oom ? ORACLE_ERR_OOM : ORACLE_OK;
+}
+
+int oracle_pbit_sort_par(const void *keys, int key_bits, const uint32_t *next, uint32_t head, uint64_t n,
+                         unsigned K, int nthreads, uint32_t *out_head, uint32_t *out_next) {
+    if (!out_head || (n && (!keys || !next || !out_next))) return ORACLE_ERR_ARG;
+    if (key_bits != 8 && key_bits != 16 && key_bits != 32 && key_bits != 64) return ORACLE_ERR_ARG;
+    if (K < 1 || K > 8 || (key_bits % K) != 0 || (unsigned)key_bits < 2 * K) return ORACLE_ERR_ARG;
+    if (n > 0xFFFFFFFFull) return ORACLE_ERR_ARG;
+    int rc = oracle_validate_list(next, head, n);
+    if (rc) return rc;
+    if (nthreads <= 0) nthreads = (int)sysconf(_SC_NPROCESSORS_ONLN);
+    if (nthreads < 1) nthreads = 1;
+    ctx_t x;
+    memset(&x, 0, sizeof x);
+    x.key = (const uint8_t *)keys;
+    x.key_bytes = key_bits / 8;
+    x.K = K;
+    x.omega = 1u << K;
+    x.fmask = ~(uint64_t)0;
+    if (out_next != next && n) memcpy(out_next, next, (size_t)n * sizeof(uint32_t));
+    x.next = out_next;
+    const uint32_t om = x.omega, nj = om * om;
+    uint32_t *tab1 = (uint32_t *)malloc(sizeof(uint32_t) * om);
+    uint32_t *lists = (uint32_t *)malloc(sizeof(uint32_t) * nj);
+    uint32_t *heads = (uint32_t *)malloc(sizeof(uint32_t) * nj);
+    uint32_t *tails = (uint32_t *)malloc(sizeof(uint32_t) * nj);
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)nthreads);
+    if (!tab1 || !lists || !heads || !tails || !th) { rc = ORACLE_ERR_OOM; goto out; }
+    {
+        /* level 1: the split loop on the whole list, M1 = M - K */
+        const unsigned M1 = (unsigned)key_bits - K, M2 = M1 - K;
+        for (uint32_t b = 0; b < om; ++b) tab1[b] = ORACLE_NULL;
+        for (uint32_t i, L = head; (i = L) != ORACLE_NULL; ) {
+            uint32_t *in = tab1 + oracle_bits(key_of(&x, L), M1, K);
+            L = x.next[L];
+            x.next[i] = *in; *in = i;
+        }
+        /* level 2 (the same split on every level-1 bucket, M2 = M - 2K), then the
+         * independent sublists, both on the threads */
+        par_t w;
+        memset(&w, 0, sizeof w);
+        w.proto = &x; w.M2 = M2; w.tab1 = tab1; w.lists = lists; w.heads = heads; w.tails = tails;
+        pthread_mutex_init(&w.mu, NULL);
+        w.phase = 0; w.njobs = om;
+        rc = par_run(&w, th, nthreads);
+        if (!rc) { w.phase = 1; w.njobs = nj; rc = par_run(&w, th, nthreads); }
+        pthread_mutex_destroy(&w.mu);
+        if (rc) goto out;
+        /* concatenate in list order: every sorted sublist's tail -> the next one's head */
+        uint32_t first = ORACLE_NULL, prev_tail = ORACLE_NULL;
+        for (uint32_t j = 0; j < nj; ++j) {
+            if (heads[j] == ORACLE_NULL) continue;
+            if (prev_tail == ORACLE_NULL) first = heads[j]; else x.next[prev_tail] = heads[j];
+            prev_tail = tails[j];
+        }
+        *out_head = first;
+    }
+out:
+    free(tab1); free(lists); free(heads); free(tails); free(th);
+    return rc;
 }
 
 /* ---------------------------------------------------------------- key kinds

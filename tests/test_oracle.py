@@ -458,3 +458,18 @@ def test_list_order_rejects_invalid():
     with pytest.raises(oracle.OracleError):
         oracle.list_order(np.array([1, 0], np.uint32), 0)   # cycle
     assert oracle.list_order(np.zeros(0, np.uint32), oracle.ORACLE_NULL).shape == (0,)
+
+
+@pytest.mark.parametrize("n,key_bits,keys,links,K,threads", [
+    (0, 32, "uniform", "random", 4, 2), (1, 8, "uniform", "random", 4, 3), (2, 16, "equal", "push", 8, 2),
+    (5000, 8, "uniform", "random", 4, 4), (50001, 32, "zipf", "random", 4, 8), (70001, 64, "runs4096", "random", 8, 3),
+    (30000, 16, "equal", "push", 4, 5), (100003, 32, "uniform", "identity", 8, 1), (65537, 32, "sorted", "random", 2, 4)])
+def test_subtree_parallel_oracle_is_bit_identical(n, key_bits, keys, links, K, threads):
+    """SURVEY §8(d)'s optional subtree-parallel CPU baseline: the first two levels of the
+    recursion as Pbit runs them, the rest on threads, the sorted sublists linked in list
+    order -- the serial oracle's bytes (Pbit(L, M, P) = Pbit(L, M, NULL) followed by P)."""
+    li = workloads.make_list(n, key_bits, seed=n + K, keys=keys, links=links)
+    k, nx = workloads.keys_numpy(li), workloads.next_numpy(li)
+    a = oracle.pbit_sort(k, nx, li.head, key_bits, K)
+    b = oracle.pbit_sort_par(k, nx, li.head, key_bits, K, threads)
+    assert a[0] == b[0] and np.array_equal(a[1], b[1])
