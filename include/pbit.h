@@ -112,6 +112,15 @@ typedef struct {
                         repair.  Same memory kind as out_next, must not
                         alias it; pbit_sort_list_mg: this rank's n_local predecessors
                         (device).  NULL = singly-linked.                           */
+    uint32_t *out_order; /* optional (NEXT row N3, record materialisation): the n node ids
+                        in sorted order, out_order[i] = w_i (the walk of the sorted list
+                        from *out_head).  Same memory kind as out_next.  pbit_sort_list
+                        only (pbit_sort_list_mg: PBIT_ERR_UNSUPPORTED).             */
+    void *out_keys;  /* optional: the n keys in sorted order, out_keys[i] = keys[w_i]
+                        (the input bit patterns, key_bits/8 bytes each).  Same memory
+                        kind as out_next; pbit_sort_list only.  With a payload array,
+                        payload[out_order[i]] materialises the sorted records.
+                        Neither is written when the list is invalid.                */
 } pbit_opts;
 
 enum { PBIT_KEY_UNSIGNED = 0, PBIT_KEY_SIGNED = 1, PBIT_KEY_FLOAT = 2 };

@@ -39,7 +39,8 @@ class _Opts(ctypes.Structure):
     _fields_ = [("digit_bits", ctypes.c_int), ("stream", ctypes.c_void_p), ("validate", ctypes.c_int),
                 ("phase_ms", ctypes.POINTER(ctypes.c_float)), ("passes_run", ctypes.POINTER(ctypes.c_uint32)),
                 ("launches", ctypes.POINTER(ctypes.c_uint32)), ("key_kind", ctypes.c_int),
-                ("descending", ctypes.c_int), ("out_prev", ctypes.c_void_p)]
+                ("descending", ctypes.c_int), ("out_prev", ctypes.c_void_p), ("out_order", ctypes.c_void_p),
+                ("out_keys", ctypes.c_void_p)]
 
 
 KEY_KINDS = {"unsigned": 0, "signed": 1, "float": 2}  # pbit.h PBIT_KEY_*
@@ -161,7 +162,7 @@ def _stream_handle(stream, on_cuda: bool):
 
 def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: int = 0, out_next=None,
               stream=None, timing: bool = False, key_kind: str | None = None, descending: bool = False,
-              out_prev=None):
+              out_prev=None, out_order=None, out_keys=None):
     """Stable sort of the list (head, next_) by keys; returns (head, out_next) (plus a
     dict of device ms per phase when timing=True).
 
@@ -171,7 +172,8 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
     "signed" or "float" (how the key bits order, pbit.h PBIT_KEY_*; None: inferred, see
     _key_kind); descending: order.
     out_prev (same kind as out_next): also filled with the predecessors of the sorted list
-    (doubly-linked lists, pbit.h pbit_opts.out_prev)."""
+    (doubly-linked lists, pbit.h pbit_opts.out_prev).  out_order / out_keys (same kind as
+    out_next): also filled with the node ids / the keys in sorted order (N3 records)."""
     if key_bits is None:
         key_bits = _KEY_BITS[keys.dtype] if isinstance(keys, torch.Tensor) else keys.dtype.itemsize * 8
     key_kind = _key_kind(keys, key_kind)
@@ -191,6 +193,10 @@ def sort_list(keys, next_, head: int, key_bits: int | None = None, digit_bits: i
               key_kind, descending)
     if out_prev is not None and n:
         o.out_prev = ctypes.c_void_p(_ptr(out_prev))
+    if out_order is not None and n:
+        o.out_order = ctypes.c_void_p(_ptr(out_order))
+    if out_keys is not None and n:
+        o.out_keys = ctypes.c_void_p(_ptr(out_keys))
     rc = lib.pbit_sort_list(_ptr(keys) if n else None, _ptr(next_) if n else None, head & 0xFFFFFFFF, n, key_bits,
                             ctypes.byref(oh), _ptr(out_next) if n else None, ctypes.byref(o))
     if rc:

@@ -1212,6 +1212,27 @@ k_array_finish(const typename KeyOf<KB>::T* __restrict__ ksorted, uint32_t n, vo
   }
 }
 
+// ============================================================================ N3: records
+// Materialise the sorted order (pbit_opts.out_order / out_keys): the final ids, and the
+// final sort keys mapped back to the input bit patterns.  Skipped for an invalid list.
+template <int KB>
+__global__ void __launch_bounds__(256)
+k_materialize(const uint32_t* __restrict__ ids, const typename KeyOf<KB>::T* __restrict__ ksorted, uint32_t n,
+              uint32_t* __restrict__ out_order, void* __restrict__ out_keys, KeyMap km, const int* __restrict__ err) {
+  using KT = std::conditional_t<KB == 1, uint8_t, std::conditional_t<KB == 2, uint16_t,
+             std::conditional_t<KB == 4, uint32_t, unsigned long long>>>;
+  pdl_enter();
+  if (*err) return;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+    if (out_order) out_order[v] = ids[v];
+    if (out_keys) {
+      unsigned long long k = ksorted[v];
+      if (!km.identity()) k = km.inverse(k, KB * 8);
+      reinterpret_cast<KT*>(out_keys)[v] = (KT)k;
+    }
+  }
+}
+
 // ============================================================================ a5: relink
 // out_next[ids[p]] = ids[p+1], out_next[ids[n-1]] = NULL, head = ids[0]: the paper's
 // end-splice merge of sorted fragments, one write per node; with out_prev (N2,

@@ -918,6 +918,7 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
     if (out_prev_local && out_prev_local == out_next_local) return PBIT_ERR_INVALID_ARG;
     if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
     if (G > 64) return PBIT_ERR_UNSUPPORTED;
+    if (opts && (opts->out_order || opts->out_keys)) return PBIT_ERR_UNSUPPORTED;  // pbit.h: single GPU only
     const uint64_t want_lo = (uint64_t)r * S;
     const uint64_t want_n = n_global > want_lo ? std::min<uint64_t>(S, n_global - want_lo) : 0;
     if (node_lo != want_lo || n_local != want_n) return PBIT_ERR_UNSUPPORTED;

@@ -292,7 +292,8 @@ static void hostio_resources(cudaStream_t* copy, cudaEvent_t** ev) {
 template <int KB>
 static int run_device(const void* keys, const uint32_t* next, uint32_t head, const SortPlan& p, uint32_t* out_next,
                       uint32_t* out_prev, uint32_t* out_head, cudaStream_t st, int sms, float* phase_ms,
-                      uint32_t* passes_run, uint32_t* launches_out, HostIO* hio = nullptr) {
+                      uint32_t* passes_run, uint32_t* launches_out, HostIO* hio = nullptr,
+                      uint32_t* out_order = nullptr, void* out_keys = nullptr) {
   using RT = typename Rec<KB>::T;
   Ws w;
   const size_t bytes = carve(p, nullptr, &w);
@@ -474,7 +475,9 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
   sa.tile_first = w.tile_first; sa.nseg = w.nseg;
   { const char* e = getenv("PBIT_DEBUG_NO_LOOKBACK"); sa.debug_no_lookback = e ? atoi(e) : 0; }
   if (ok) {
-    launch_key_passes_k<KB>(p.K, sa, hplan, false, st, timing ? ev : nullptr, PBIT_PHASE_PASS0, SRC_GATHER);
+    // out_keys (N3 records): the last pass keeps the keys too
+    launch_key_passes_k<KB>(p.K, sa, hplan, out_keys != nullptr, st, timing ? ev : nullptr, PBIT_PHASE_PASS0,
+                            SRC_GATHER);
     launches += hplan.npasses;
   }
   if (timing)
@@ -492,6 +495,13 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
     const uint32_t* fin = w.ids[hplan.npasses & 1u];  // buffer holding the final ids
     launch_pdl(k_relink_head, 1, 1, 0, st, fin, w.d_head, w.err);
     ++launches;
+    if (out_order || out_keys) {  // N3: the sorted records (skipped for an invalid list)
+      const int mb = full_wave(k_materialize<KB>, 256, 0, sms, (n + 255) / 256);
+      const KeyMap km{p.key_kind, p.descending};
+      launch_pdl(k_materialize<KB>, mb, 256, 0, st, fin, (const typename KeyOf<KB>::T*)w.keys[hplan.npasses & 1u], n,
+                 out_order, out_keys, km, w.err);
+      ++launches;
+    }
     // N2: with out_prev the records are (v, succ, pred): both outputs in one chain
     RelinkD2H d2h;
     if (hio && RelinkLevels(n).L > 0) {
@@ -607,14 +617,16 @@ static int run_small(const void* keys, const uint32_t* next, uint32_t head, uint
 
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
                 int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
-                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches, HostIO* hio) {
+                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches, HostIO* hio,
+                uint32_t* out_order, void* out_keys) {
   NvtxRange nv("pbit_sort_list");
   int dev = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return PBIT_ERR_CUDA;
   int sms = 0;
   if (int rc = device_info(dev, &sms)) return rc;
   init_rank_mode(st);
-  if (n <= SMALL_N && (K == 4 || K == 8) && rank_mode() == RANK_ATOMIC && !small_path_disabled() && !hio) {
+  if (n <= SMALL_N && (K == 4 || K == 8) && rank_mode() == RANK_ATOMIC && !small_path_disabled() && !hio &&
+      !out_order && !out_keys) {
     const KeyMap km{key_kind, descending ? 1 : 0};
     const uint32_t n32 = (uint32_t)n;
     switch (key_bits) {
@@ -629,10 +641,14 @@ int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t 
   p.key_kind = key_kind;
   p.descending = descending ? 1 : 0;
   switch (key_bits) {
-    case 8: return run_device<1>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
-    case 16: return run_device<2>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
-    case 32: return run_device<4>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
-    default: return run_device<8>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio);
+    case 8: return run_device<1>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio,
+                                 out_order, out_keys);
+    case 16: return run_device<2>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio,
+                                 out_order, out_keys);
+    case 32: return run_device<4>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio,
+                                 out_order, out_keys);
+    default: return run_device<8>(keys, next, head, p, out_next, out_prev, out_head, st, sms, phase_ms, passes_run, launches, hio,
+                                 out_order, out_keys);
   }
 }
 
@@ -804,6 +820,8 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   if (!key_kind_ok(key_kind, key_bits)) return PBIT_ERR_INVALID_ARG;
   uint32_t* out_prev = opts ? opts->out_prev : nullptr;
   if (out_prev && out_prev == out_next) return PBIT_ERR_INVALID_ARG;
+  uint32_t* out_order = opts ? opts->out_order : nullptr;
+  void* out_keys = opts ? opts->out_keys : nullptr;
   cudaStream_t st = opts ? (cudaStream_t)opts->stream : (cudaStream_t)0;
   float* phase_ms = opts ? opts->phase_ms : nullptr;
   uint32_t* passes_run = opts ? opts->passes_run : nullptr;
@@ -821,18 +839,22 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
   if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
   const int kk = pointer_kind(keys, dev), kn = pointer_kind(next, dev), ko = pointer_kind(out_next, dev);
   const int kp = out_prev ? pointer_kind(out_prev, dev) : ko;
-  if (kk < 0 || kn < 0 || ko < 0 || kp < 0) return PBIT_ERR_INVALID_ARG;
-  if (kk == 1 && kn == 1 && ko == 1 && kp == 1)
+  const int kr = out_order ? pointer_kind(out_order, dev) : ko;
+  const int ky = out_keys ? pointer_kind(out_keys, dev) : ko;
+  if (kk < 0 || kn < 0 || ko < 0 || kp < 0 || kr < 0 || ky < 0) return PBIT_ERR_INVALID_ARG;
+  if (kk == 1 && kn == 1 && ko == 1 && kp == 1 && kr == 1 && ky == 1)
     return sort_device(keys, next, head, n, key_bits, K, key_kind, descending, out_head, out_next, out_prev, st,
-                       phase_ms, passes_run, launches);
-  if (kk != 0 || kn != 0 || ko != 0 || kp != 0) return PBIT_ERR_INVALID_ARG;  // mixed host/device
+                       phase_ms, passes_run, launches, nullptr, out_order, out_keys);
+  if (kk != 0 || kn != 0 || ko != 0 || kp != 0 || kr != 0 || ky != 0) return PBIT_ERR_INVALID_ARG;  // mixed
 
   // host buffers: stage through device memory inside the call
   const size_t kbytes = n * (size_t)(key_bits / 8), nbytes = n * 4;
   char* d = nullptr;
   const size_t a = align_up(kbytes), b = align_up(nbytes);
-  if (ws_alloc((void**)&d, a + 3 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
+  if (ws_alloc((void**)&d, 2 * a + 4 * b, st) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_OOM; }
   uint32_t* d_prev = out_prev ? (uint32_t*)(d + a + 2 * b) : nullptr;
+  uint32_t* d_order = out_order ? (uint32_t*)(d + a + 3 * b) : nullptr;
+  void* d_keys = out_keys ? (void*)(d + a + 4 * b) : nullptr;
   int rc = PBIT_OK;
   const bool small = n <= SMALL_N;  // the single-cluster path: plain copies around one launch
   HostIO hio{keys, next, out_next, out_prev, nullptr, nullptr};
@@ -845,11 +867,15 @@ int pbit_sort_list(const void* keys, const uint32_t* next, uint32_t head, uint64
     rc = PBIT_ERR_CUDA;
   }
   if (!rc) rc = sort_device(d, (const uint32_t*)(d + a), head, n, key_bits, K, key_kind, descending, out_head,
-                            (uint32_t*)(d + a + b), d_prev, st, phase_ms, passes_run, launches, small ? nullptr : &hio);
+                            (uint32_t*)(d + a + b), d_prev, st, phase_ms, passes_run, launches, small ? nullptr : &hio,
+                            d_order, d_keys);
   if (!rc && !hio.results_copied) {
     if (cudaMemcpyAsync(out_next, d + a + b, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
     if (!rc && out_prev && cudaMemcpyAsync(out_prev, d_prev, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
   }
+  // the sorted records (a valid list only: rc is PBIT_OK here)
+  if (!rc && out_order && cudaMemcpyAsync(out_order, d_order, nbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
+  if (!rc && out_keys && cudaMemcpyAsync(out_keys, d_keys, kbytes, cudaMemcpyDeviceToHost, st)) rc = PBIT_ERR_CUDA;
   cudaFreeAsync(d, st);
   if (cudaStreamSynchronize(st) != cudaSuccess && !rc) rc = PBIT_ERR_CUDA;
   cudaGetLastError();

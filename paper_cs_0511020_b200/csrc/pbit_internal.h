@@ -41,7 +41,8 @@ void init_rank_mode(cudaStream_t st); // runs the atomic-order self-test once
 struct HostIO;  // pbit.cu: host-buffer staging overlapped with the pack and the apply
 int sort_device(const void* keys, const uint32_t* next, uint32_t head, uint64_t n, int key_bits, int K,
                 int key_kind, int descending, uint32_t* out_head, uint32_t* out_next, uint32_t* out_prev,
-                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches, HostIO* hio = nullptr);
+                cudaStream_t st, float* phase_ms, uint32_t* passes_run, uint32_t* launches, HostIO* hio = nullptr,
+                uint32_t* out_order = nullptr, void* out_keys = nullptr);
 // key_kind / key_bits combination accepted by the ABI (PBIT_KEY_*, pbit.h)
 bool key_kind_ok(int key_kind, int key_bits);
 

@@ -581,3 +581,46 @@ def test_concurrent_host_threads_on_own_streams(pbit):
     assert not errors, errors
     for i in range(len(lists)):
         _assert_same(got[i], want[i], f"thread {i}")
+
+
+# ---------------------------------------------------------------- N3: sorted records (out_order, out_keys)
+@pytest.mark.parametrize("n,key_bits,keys,links,kind,desc", [
+    (1, 32, "uniform", "random", "unsigned", False), (1000, 8, "uniform", "random", "unsigned", False),
+    (65537, 16, "uniform", "push", "signed", True), (100003, 32, "zipf", "random", "unsigned", False),
+    (250001, 64, "runs4096", "random", "float", False), (300007, 32, "equal", "random", "unsigned", False)])
+def test_sorted_records_materialised(pbit, n, key_bits, keys, links, kind, desc):
+    """out_order[i] = the i-th node of the oracle's sorted list, out_keys[i] = its key (input
+    bits); device and host buffers; the payload follows through out_order (reading Q11)."""
+    li = workloads.make_list(n, key_bits, seed=n * 7 + key_bits, keys=keys, links=links, device="cuda")
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4,
+                              descending=desc, kind=kind)
+    order = oracle.list_order(on, oh)
+    order_d = torch.empty(n, dtype=torch.int32, device="cuda")
+    keys_d = torch.empty_like(li.keys)
+    h, out = pbit.sort_list(li.keys, li.next, li.head, key_bits=key_bits, key_kind=kind, descending=desc,
+                            out_order=order_d, out_keys=keys_d)
+    torch.cuda.synchronize()
+    assert h == oh and np.array_equal(out.cpu().numpy().view(np.uint32), on)
+    assert np.array_equal(order_d.cpu().numpy().view(np.uint32), order)
+    assert np.array_equal(workloads.keys_numpy(li)[order], keys_d.cpu().numpy().view(workloads.keys_numpy(li).dtype))
+    if li.payload is not None:  # sorted records (key, payload) through out_order
+        assert np.array_equal(li.payload[order_d.long()].cpu().numpy(), li.payload.cpu().numpy()[order])
+    # host buffers
+    kh, nh = workloads.keys_numpy(li), workloads.next_numpy(li)
+    oh2, ko2 = np.empty(n, np.uint32), np.empty_like(kh)
+    h2, out2 = pbit.sort_list(kh, nh, li.head, key_bits=key_bits, key_kind=kind, descending=desc,
+                              out_order=oh2, out_keys=ko2)
+    assert h2 == oh and np.array_equal(out2, on) and np.array_equal(oh2, order) and np.array_equal(ko2, kh[order])
+
+
+def test_sorted_records_untouched_on_invalid_list(pbit):
+    n = 100003
+    nx = _bad_lists(n)["cycle_through_head"].cuda()
+    keys = workloads.uniform_u32(n, 1, 1).to(torch.int32).cuda()
+    order = torch.full((n,), 5, dtype=torch.int32, device="cuda")
+    ko = torch.full((n,), 9, dtype=torch.int32, device="cuda")
+    with pytest.raises(pbit.PbitError) as e:
+        pbit.sort_list(keys, nx, 0, out_order=order, out_keys=ko)
+    assert e.value.code == 2
+    torch.cuda.synchronize()
+    assert bool((order == 5).all()) and bool((ko == 9).all())
