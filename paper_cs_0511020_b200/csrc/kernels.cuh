@@ -10,10 +10,12 @@
 //   k_plan      a3     exclusive scans of the digit histograms -> bucket bases, pass plan
 //   k_onesweep  a3/a4  one stable LSD pass: TMA tile loads, in-warp ranking (lane-ordered
 //                      shared atomics, or ballots), decoupled lookback, smem-staged
-//                      coalesced scatter
+//                      coalesced scatter; SRC_SPLIT: the multi-GPU key-range partition,
+//                      stored straight into the destination ranks' arrays
+//   k_materialize N3   the sorted node ids / keys (pbit_opts.out_order / out_keys)
 //   k_relink_*  a5     out_next (and out_prev, N2) from the sorted ids (the paper's merge,
-//                      P:273-280): (v, succ) pairs binned by v in MSD partition levels,
-//                      applied in shared-memory windows
+//                      P:273-280): (v, succ[, pred]) records binned by v in MSD partition
+//                      levels, applied in shared-memory windows
 //   k_array_*   N3     pbit_sort_array's prep (key map + histograms) and finish
 //
 // Paper anchors: the split loop is the stable scatter; the end-marker

@@ -5,8 +5,9 @@
 //   -> k_walk -> k_rank_walk_a, k_rank_jump^r (or k_rank_jump_block), k_rank_walk_b
 //   -> k_onesweep per non-trivial digit (the first gathers from the walk's slots;
 //      k_gather only when no pass runs) -> k_relink_part per level -> k_relink_apply
-// then one small D2H of {head, error, passes} and a stream sync.  pbit_sort_array
-// (the "table" of P:1118-1177) runs k_array_prep -> k_plan -> the passes.
+// then one small D2H of {head, error, passes} and a stream sync.  Host buffers: the copies
+// run on a second stream in chunks, overlapped with the pack and the apply (HostIO).
+// pbit_sort_array (the "table" of P:1118-1177) runs k_array_prep -> k_plan -> the passes.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
