@@ -42,6 +42,7 @@ GOLD = _goldens()
 
 
 def _make(name, g, device):
+    name = g.get("config", name)  # key-kind goldens ("C3_float") sort a config's list
     if name in workloads.CONFIGS:
         return workloads.make_config(name, device=device)
     e = EXTRA[name]
@@ -63,6 +64,8 @@ def test_golden_files_complete():
         g = GOLD[name]
         assert g["oracle_K"] == 4 and len(g["out_next_sha256"]) == 64
     assert "payload_seq_sha256" in GOLD["C4"]
+    for name in ["C3_float", "C3_unsigned_desc", "C4_signed_desc"]:  # N1 at full size
+        assert name in GOLD and GOLD[name]["config"] == name.split("_")[0]
 
 
 def test_golden_c1_matches_oracle_here():
@@ -77,7 +80,9 @@ def test_golden_c1_matches_oracle_here():
 # at a width that does not divide the key (K = 11 as 8-bit sub-passes, reading Q7)
 CASES = [(c, None) for c in ["C1", "C2", "C3", "C4", "C5", "X26", "X26u64", "ctx"]] + [
     ("X26", 4), ("X26", 6), ("X26u64", 11), ("C3", 4),
-    ("ctx", 8), ("ctx", 16)]  # the paper's own workload at its K = 4 (default), 8 and 16
+    ("ctx", 8), ("ctx", 16),  # the paper's own workload at its K = 4 (default), 8 and 16
+    # key kinds and the descending order at full size (N1: P:371-372)
+    ("C3_float", None), ("C3_unsigned_desc", None), ("C4_signed_desc", None)]
 
 
 @pytest.mark.gpu
@@ -88,9 +93,11 @@ def test_full_size_bit_exact_vs_oracle_golden(cuda_ok, name, K):
     li = _make(name, g, "cuda")
     assert li.n == g["n"]
     assert _input_sha(li) == g["input_sha256"], "device generator differs from the host generator"
-    K = K or (workloads.CONFIGS[name]["digit_bits"] if name in workloads.CONFIGS else 8)
+    cfg = g.get("config", name)
+    K = K or (workloads.CONFIGS[cfg]["digit_bits"] if cfg in workloads.CONFIGS else 8)
     payload = li.payload
-    h, out = pbit.sort_list(li.keys, li.next, li.head, key_bits=li.key_bits, digit_bits=K)
+    h, out = pbit.sort_list(li.keys, li.next, li.head, key_bits=li.key_bits, digit_bits=K,
+                            key_kind=g.get("kind", "unsigned"), descending=g.get("descending", False))
     torch.cuda.synchronize()
     on = out.cpu().numpy().view(np.uint32)
     del li, out

@@ -18,7 +18,7 @@ tests/golden/config_<name>.json:
 
 No value here comes from the CUDA path: this script imports only oracle/ and workloads.py.
 
-  python tools/make_goldens.py C1 C2 X26 C3 C4 C5
+  python tools/make_goldens.py C1 C2 X26 C3 C4 C5 C3:float C4:signed:desc
 """
 from __future__ import annotations
 
@@ -80,7 +80,10 @@ def cpu_model() -> str:
 
 
 def main(names):
-    for name in names:
+    for spec in names:
+        # "<config>[:<kind>[:desc]]" -- key kinds and the descending order (N1) at full size
+        parts = spec.split(":")
+        name, kind, desc = parts[0], parts[1] if len(parts) > 1 else "unsigned", len(parts) > 2 and parts[2] == "desc"
         t0 = time.time()
         li, c = make(name)
         keys = workloads.keys_numpy(li)
@@ -91,7 +94,7 @@ def main(names):
         t_gen = time.time() - t0
         ih = input_sha256(keys, nxt, head)
         t1 = time.time()
-        oh, on = oracle.pbit_sort(keys, nxt, head, c["key_bits"], 4)
+        oh, on = oracle.pbit_sort(keys, nxt, head, c["key_bits"], 4, descending=desc, kind=kind)
         t_or = time.time() - t1
         rec = {"n": int(nxt.shape[0]), "key_bits": c["key_bits"], "seed": c["seed"], "desc": c["desc"],
                "input_sha256": ih, "out_head": int(oh), "out_next_sha256": hashlib.sha256(on.tobytes()).hexdigest(),
@@ -102,9 +105,10 @@ def main(names):
             rec["payload_seq_sha256"] = hashlib.sha256(payload[order].tobytes()).hexdigest()
             del order
         del on, keys, nxt, payload
-        rec["name"] = name
-        print(name, json.dumps(rec), flush=True)
-        out = os.path.join(GOLDEN_DIR, f"config_{name}.json")
+        gname = name if (kind == "unsigned" and not desc) else f"{name}_{kind}{'_desc' if desc else ''}"
+        rec.update(name=gname, config=name, kind=kind, descending=desc)
+        print(gname, json.dumps(rec), flush=True)
+        out = os.path.join(GOLDEN_DIR, f"config_{gname}.json")
         with open(out + ".tmp", "w") as f:
             json.dump(rec, f, indent=1, sort_keys=True)
             f.write("\n")
