@@ -23,6 +23,7 @@
 #pragma once
 #include "common.cuh"
 
+#include <cooperative_groups.h>
 #include <type_traits>
 
 namespace pbit {
@@ -361,6 +362,44 @@ static __global__ void k_rank_jump(const unsigned long long* __restrict__ d_in, 
     d_out[r] = d;
     c_out[r] = c;
     s_out[r] = s2;
+  }
+}
+
+// All pointer-jumping rounds in ONE cooperative launch (grid-wide barrier between rounds)
+// instead of one launch per round: the rounds are ~8 us each, mostly launch latency even
+// with programmatic dependent launch.  The blocks of this one launch wait on each other
+// at the barrier (cooperative launch: all of them are resident).  Ends with the check of
+// k_rank_check; the result is in buffer (rounds & 1).
+static __global__ void __launch_bounds__(256)
+k_rank_jump_grid(unsigned long long* __restrict__ d0, uint32_t* __restrict__ c0, uint32_t* __restrict__ s0,
+                 unsigned long long* __restrict__ d1, uint32_t* __restrict__ c1, uint32_t* __restrict__ s1, uint32_t m,
+                 int rounds, uint32_t head_sub, uint32_t n, int* __restrict__ err) {
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  if (*err) return;  // written by earlier kernels only: the same value in every block
+  for (int r = 0; r < rounds; ++r) {
+    const bool odd = r & 1;
+    const unsigned long long* d_in = odd ? d1 : d0;
+    const uint32_t* c_in = odd ? c1 : c0;
+    const uint32_t* s_in = odd ? s1 : s0;
+    unsigned long long* d_out = odd ? d0 : d1;
+    uint32_t* c_out = odd ? c0 : c1;
+    uint32_t* s_out = odd ? s0 : s1;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+      const uint32_t sx = s_in[i];
+      unsigned long long d = d_in[i];
+      uint32_t c = c_in[i], s2 = sx;
+      if (sx != PBIT_NULL32) { d += d_in[sx]; c += c_in[sx]; s2 = s_in[sx]; }
+      d_out[i] = d;
+      c_out[i] = c;
+      s_out[i] = s2;
+    }
+    grid.sync();
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const bool odd = rounds & 1;
+    const uint32_t* s = odd ? s1 : s0;
+    const unsigned long long* d = odd ? d1 : d0;
+    if (s[head_sub] != PBIT_NULL32 || d[head_sub] != (unsigned long long)n) atomicOr(err, E_CHAIN);
   }
 }
 

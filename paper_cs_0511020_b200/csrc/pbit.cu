@@ -148,6 +148,13 @@ static int debug_env(const char* name) {
   return e ? atoi(e) : 0;
 }
 
+// the pointer jumping of the ranking in one cooperative launch (default), or one launch
+// per round (PBIT_RANK_GRID=0, experiments)
+static bool rank_grid_enabled() {
+  static const bool v = [] { const char* e = getenv("PBIT_RANK_GRID"); return !(e && atoi(e) == 0); }();
+  return v;
+}
+
 // PBIT_SMALL=0 sends small lists through the general path too (experiments, tests)
 static bool small_path_disabled() {
   static const bool v = [] { const char* e = getenv("PBIT_SMALL"); return e && atoi(e) == 0; }();
@@ -422,6 +429,31 @@ static int run_device(const void* keys, const uint32_t* next, uint32_t head, con
       });
       launch_pdl(k_rank_jump_block, 1, 1024, RANK_SMALL * 32, st, w.sdist[0], w.scnt[0], w.ssucc[0], nsub, rounds,
                  head_sub, n, w.err);
+      launches += 1;
+    } else if (rank_grid_enabled()) {  // every round in one cooperative launch
+      static std::atomic<unsigned long long> attr{0};
+      static int occ = 1;
+      once_per_device(attr, [] {
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, k_rank_jump_grid, 256, 0) != cudaSuccess) {
+          cudaGetLastError();
+          o = 1;
+        }
+        occ = std::max(o, 1);
+      });
+      const int gblocks = std::max(1, std::min(sblocks, sms * occ));
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = gblocks;
+      cfg.blockDim = 256;
+      cfg.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, k_rank_jump_grid, w.sdist[0], w.scnt[0], w.ssucc[0], w.sdist[1], w.scnt[1],
+                         w.ssucc[1], nsub, rounds, head_sub, n, w.err);
+      cur = rounds & 1;
       launches += 1;
     } else {
       for (int i = 0; i < rounds; ++i) {
