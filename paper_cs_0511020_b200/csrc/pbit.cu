@@ -148,10 +148,11 @@ static int debug_env(const char* name) {
   return e ? atoi(e) : 0;
 }
 
-// the pointer jumping of the ranking in one cooperative launch (default), or one launch
-// per round (PBIT_RANK_GRID=0, experiments)
+// the pointer jumping of the ranking as one launch per round chained by programmatic
+// dependent launch (default), or all rounds in one cooperative launch (PBIT_RANK_GRID=1:
+// measured slower -- the grid barrier costs more than a PDL-chained launch)
 static bool rank_grid_enabled() {
-  static const bool v = [] { const char* e = getenv("PBIT_RANK_GRID"); return !(e && atoi(e) == 0); }();
+  static const bool v = [] { const char* e = getenv("PBIT_RANK_GRID"); return e && atoi(e) == 1; }();
   return v;
 }
 
