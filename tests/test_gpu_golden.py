@@ -79,7 +79,7 @@ def test_golden_c1_matches_oracle_here():
 # every config at its BASELINE digit width; the extra cases also at the paper's K = 4 and
 # at a width that does not divide the key (K = 11 as 8-bit sub-passes, reading Q7)
 CASES = [(c, None) for c in ["C1", "C2", "C3", "C4", "C5", "X26", "X26u64", "ctx"]] + [
-    ("X26", 4), ("X26", 6), ("X26u64", 11), ("C3", 4),
+    ("X26", 4), ("X26", 6), ("X26u64", 11), ("C3", 4), ("C4", 4), ("C5", 4), ("C2", 3),
     ("ctx", 8), ("ctx", 16),  # the paper's own workload at its K = 4 (default), 8 and 16
     # key kinds and the descending order at full size (N1: P:371-372)
     ("C3_float", None), ("C3_unsigned_desc", None), ("C4_signed_desc", None)]
