@@ -434,6 +434,27 @@ def run_ours(args):
     if ws > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = n * ws / float(e2e_t.item())
+    # the PCIe bound of a synchronous host-buffer call: the same bytes copied alone (pinned
+    # H2D of keys + next, D2H of out_next), measured here with plain device copies
+    dk, dn = torch.empty_like(keys), torch.empty_like(nxt)
+    torch.cuda.synchronize()
+    c0 = time.perf_counter()
+    for _ in range(3):
+        dk.copy_(kh, non_blocking=True)
+        dn.copy_(nh, non_blocking=True)
+        torch.cuda.synchronize()
+    h2d_s = (time.perf_counter() - c0) / 3
+    c0 = time.perf_counter()
+    for _ in range(3):
+        oh.copy_(dn, non_blocking=True)
+        torch.cuda.synchronize()
+    d2h_s = (time.perf_counter() - c0) / 3
+    del dk, dn
+    pcie = {"h2d_gbs": round(n * (kb // 8 + 4) / h2d_s / 1e9, 1), "d2h_gbs": round(n * 4 / d2h_s / 1e9, 1),
+            "copies_alone_ms": round((h2d_s + d2h_s) * 1e3, 2),
+            "bound_nodes_per_s": n / (h2d_s + d2h_s + ms_max / 1e3),
+            "note": "copies alone + the device-timed call: what a synchronous call moving these bytes "
+                    "over PCIe can reach without overlap; the call overlaps the pack and the apply"}
 
     # ---- roofline of the dominant kernel
     bpn = phase_bytes_per_node(kb)
@@ -517,7 +538,7 @@ def run_ours(args):
                 "hbm_gbs_method": round(method_bytes_per_node(kb) * n * ws / (ms_max / 1e3) / 1e9, 1),
                 "roofline": roofline, "whole_call_dram": whole, "array_sort": array_ctx, "cpu_baseline": cpu,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n * (kb // 8 + 4),
-                        "d2h_bytes_per_step": n * 4 + 4},
+                        "d2h_bytes_per_step": n * 4 + 4, "pcie": pcie},
                 "gpu_launches": launches * args.steps, "clocks": clocks}
         print(json.dumps(line), flush=True)
     if ws > 1:
