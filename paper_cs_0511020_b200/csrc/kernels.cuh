@@ -1353,7 +1353,8 @@ template <bool FROM_IDS, int W>
 __global__ void __launch_bounds__(PART_THREADS, 2)
 k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* __restrict__ pin,
               typename RelinkRec<W>::T* __restrict__ pout, uint32_t n, uint32_t v_off, int shift, int bits,
-              uint32_t* __restrict__ cursor, const int* __restrict__ err) {
+              uint32_t* __restrict__ cursor, const int* __restrict__ err, uint32_t lo = 0) {
+  // records [lo, n) of the input (lo: a whole bin of the previous level; 0 for FROM_IDS)
   using R = typename RelinkRec<W>::T;
   constexpr int TILE = PartCfg<W>::TILE;
   constexpr int IPT = PartCfg<W>::IPT;
@@ -1363,9 +1364,9 @@ k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* 
   if (*err) return;
   const uint32_t t = threadIdx.x, lane = t & 31, w = t >> 5;
   const uint32_t nb = 1u << bits, mask = nb - 1;
-  const uint32_t ntiles = (n + TILE - 1) / TILE;
+  const uint32_t ntiles = (n - lo + TILE - 1) / TILE;
   auto issue = [&](uint32_t tile, int buf) {  // thread 0: TMA bulk load of one tile
-    const uint32_t base = tile * (uint32_t)TILE;
+    const uint32_t base = lo + tile * (uint32_t)TILE;
     const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[buf]);
     uint32_t bytes;
     const void* src;
@@ -1405,7 +1406,7 @@ k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* 
                      : "=r"(done) : "r"(m), "r"(par) : "memory");
     }
     __syncthreads();
-    const uint32_t base = tile * (uint32_t)TILE;
+    const uint32_t base = lo + tile * (uint32_t)TILE;
     const uint32_t cnt = min((uint32_t)TILE, n - base);
     R x[IPT];
     uint32_t r[IPT];

@@ -189,6 +189,34 @@ static uint32_t launch_relink_w(const uint32_t* ids, const void* recs, uint32_t 
   const size_t psm = sizeof(PartSmem<W>);
   const R* in = (const R*)recs;
   R* buf[2] = {(R*)rbuf0, (R*)rbuf1};
+  if (d2h && d2h->chunks > 1 && lv.L == 2 && ids) {
+    // host buffers, two levels: level 0 on everything, then per group of level-0 bins its
+    // level-1 partition, its apply and the copy of its ids' results -- the copies start
+    // after the first group instead of after the whole level 1
+    k_relink_part<true, W><<<grid, PART_THREADS, psm, st>>>(ids, nullptr, buf[0], n, 0, lv.shift[0], lv.bits[0],
+                                                            cursors, err);
+    uint32_t* cur1 = cursors + RelinkLevels::cursors(n, lv.shift[0]);
+    const uint32_t nb0 = ((n - 1) >> lv.shift[0]) + 1;
+    const uint32_t per = (nb0 + d2h->chunks - 1) / d2h->chunks;
+    uint32_t launched = 1;
+    for (int c = 0; c < d2h->chunks; ++c) {
+      const uint32_t b0 = c * per, b1 = std::min(nb0, b0 + per);
+      if (b0 >= b1) break;
+      const uint32_t lo = b0 << lv.shift[0];
+      const uint32_t hi = (uint32_t)std::min<uint64_t>(n, (uint64_t)b1 << lv.shift[0]);
+      const uint32_t g1 = std::min<uint32_t>((hi - lo + TILE - 1) / TILE, (uint32_t)(sms * part_occ));
+      k_relink_part<false, W><<<g1, PART_THREADS, psm, st>>>(nullptr, buf[0], buf[1], hi, 0u, lv.shift[1],
+                                                             lv.bits[1], cur1, err, lo);
+      const uint32_t f0 = lo >> RELINK_FINE_SHIFT, f1 = (hi + (1u << RELINK_FINE_SHIFT) - 1) >> RELINK_FINE_SHIFT;
+      k_relink_apply<false, W><<<f1 - f0, 512, WIN, st>>>(nullptr, buf[1], n, 0, out_next, out_prev, err, f0);
+      launched += 2;
+      cudaEventRecord(d2h->ev[c], st);
+      cudaStreamWaitEvent(d2h->copy, d2h->ev[c], 0);
+      cudaMemcpyAsync(d2h->h_next + lo, out_next + lo, (size_t)(hi - lo) * 4, cudaMemcpyDeviceToHost, d2h->copy);
+      if (W == 3) cudaMemcpyAsync(d2h->h_prev + lo, out_prev + lo, (size_t)(hi - lo) * 4, cudaMemcpyDeviceToHost, d2h->copy);
+    }
+    return launched;
+  }
   for (int l = 0; l < lv.L; ++l) {
     R* out = buf[l & 1];
     if (l == 0 && ids)
