@@ -127,3 +127,15 @@ def test_mg_ruler_blocks_tile_every_slice(pbit):
             sp, b = pbit.mg_ruler_blocks(n, G)
             assert sp & (sp - 1) == 0 and sp <= 64 and S % sp == 0
             assert b == S // sp and G * b * sp >= n
+
+
+def test_header_is_plain_c_and_the_example_links(pbit, tmp_path):
+    """include/pbit.h compiles as C99 and a plain C program links against libpbit.so
+    (examples/sort_list.c; it runs on a GPU box: tests/test_gpu_parity.py)."""
+    import subprocess
+    exe = tmp_path / "sort_list"
+    libdir = os.path.dirname(pbit.LIB_PATH)
+    r = subprocess.run(["cc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
+                        os.path.join(ROOT, "examples", "sort_list.c"), "-L", libdir, "-l:libpbit.so",
+                        f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr

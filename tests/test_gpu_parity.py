@@ -624,3 +624,18 @@ def test_sorted_records_untouched_on_invalid_list(pbit):
     assert e.value.code == 2
     torch.cuda.synchronize()
     assert bool((order == 5).all()) and bool((ko == 9).all())
+
+
+def test_plain_c_example_prints_the_papers_worked_example(pbit, tmp_path):
+    """examples/sort_list.c: the C-ABI from a plain C program on host arrays, the worked
+    example of P:84-98 (3 3 14 21 47 156 209 214)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = tmp_path / "sort_list"
+    libdir = os.path.dirname(pbit.LIB_PATH)
+    subprocess.run(["cc", "-std=c99", "-I", os.path.join(root, "include"), os.path.join(root, "examples", "sort_list.c"),
+                    "-L", libdir, "-l:libpbit.so", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+    r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stderr
+    assert r.stdout.split() == ["3", "3", "14", "21", "47", "156", "209", "214"]
