@@ -284,17 +284,28 @@ struct HostIO {
   bool results_copied = false;  // set once the relink has queued the result copies
 };
 static void hostio_resources(cudaStream_t* copy, cudaEvent_t** ev) {
-  static thread_local cudaStream_t cs[64] = {};
-  static thread_local cudaEvent_t evs[64][HOSTIO_CHUNKS] = {};
+  // one copy stream and its events per (host thread, device), released when the thread ends
+  struct Res {
+    cudaStream_t cs[64] = {};
+    cudaEvent_t evs[64][HOSTIO_CHUNKS] = {};
+    ~Res() {
+      for (int d = 0; d < 64; ++d) {
+        if (!cs[d]) continue;
+        cudaStreamDestroy(cs[d]);
+        for (int i = 0; i < HOSTIO_CHUNKS; ++i) cudaEventDestroy(evs[d][i]);
+      }
+    }
+  };
+  static thread_local Res r;
   int dev = 0;
   cudaGetDevice(&dev);
   dev &= 63;
-  if (!cs[dev]) {
-    cudaStreamCreateWithFlags(&cs[dev], cudaStreamNonBlocking);
-    for (int i = 0; i < HOSTIO_CHUNKS; ++i) cudaEventCreateWithFlags(&evs[dev][i], cudaEventDisableTiming);
+  if (!r.cs[dev]) {
+    cudaStreamCreateWithFlags(&r.cs[dev], cudaStreamNonBlocking);
+    for (int i = 0; i < HOSTIO_CHUNKS; ++i) cudaEventCreateWithFlags(&r.evs[dev][i], cudaEventDisableTiming);
   }
-  *copy = cs[dev];
-  *ev = evs[dev];
+  *copy = r.cs[dev];
+  *ev = r.evs[dev];
 }
 
 // ----------------------------------------------------------------------------- the device path
