@@ -191,6 +191,17 @@ int pbit_sort_array(const void *keys, uint64_t n, int key_bits, uint32_t *out_in
  * Rank r returns the successors of its own nodes; the sorted positions it computed
  * internally are [r*S, r*S + S) (key-range sharding: exact splitters of the global
  * (key, list position) order, so the shards are equal in size even under heavy duplicates).
+ * opts->out_order / out_keys are not supported here (PBIT_ERR_UNSUPPORTED).
+ *
+ * Transport (PBIT_MG_TRANSPORT, read at every call; pbit_mg_transport reports the one
+ * used): "peer" (default) -- every rank maps the others' device memory through CUDA IPC:
+ * the walk reads remote nodes with peer loads, the key-range partition and the relink
+ * routing store straight into the destination rank's memory, NCCL carries only small
+ * collectives; "hybrid" -- the same with a kn replica (ncclAllGather) walked locally;
+ * "nccl" -- replica + ncclSend/ncclRecv.  Every transport gives the same bytes.  If a rank
+ * cannot map the others, the ranks agree on it and the call runs on "nccl".  The peer
+ * windows (cudaMalloc, about 5-6 B per node of the slice plus the slots) are kept per
+ * communicator and freed by pbit_mg_comm_destroy / pbit_mg_comm_abort.
  */
 int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32_t head,
                       uint64_t n_global, uint64_t node_lo, uint64_t n_local, int key_bits,
