@@ -200,7 +200,7 @@ int pbit_sort_array(const void *keys, uint64_t n, int key_bits, uint32_t *out_in
  * collectives; "hybrid" -- the same with a kn replica (ncclAllGather) walked locally;
  * "nccl" -- replica + ncclSend/ncclRecv.  Every transport gives the same bytes.  If a rank
  * cannot map the others, the ranks agree on it and the call runs on "nccl".  The peer
- * windows (cudaMalloc, about 5-6 B per node of the slice plus the slots) are kept per
+ * windows (cudaMalloc; ~56 B per node of the slice for 32-bit keys, mostly segment slots) are kept per
  * communicator and freed by pbit_mg_comm_destroy / pbit_mg_comm_abort.
  */
 int pbit_sort_list_mg(const void *keys_local, const uint32_t *next_local, uint32_t head,
