@@ -639,3 +639,34 @@ def test_plain_c_example_prints_the_papers_worked_example(pbit, tmp_path):
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert r.stdout.split() == ["3", "3", "14", "21", "47", "156", "209", "214"]
+
+
+RANK_SNIPPET = """
+import numpy as np, torch, oracle, workloads, paper_cs_0511020_b200 as pbit
+assert pbit.rank_mode() == {mode}, pbit.rank_mode()
+for n, kb, keys, links, K in [(100003, 32, "zipf", "random", 8), (65537, 8, "uniform", "push", 4),
+                               (250001, 64, "runs4096", "random", 8), (1000003, 32, "uniform", "random", 0),
+                               (77777, 16, "equal", "identity", 5), (4097, 32, "sorted", "random", 3)]:
+    li = workloads.make_list(n, kb, seed=n, keys=keys, links=links, device="cuda")
+    h, out = pbit.sort_list(li.keys, li.next, li.head, key_bits=kb, digit_bits=K)
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, kb, 4)
+    assert h == oh and np.array_equal(out.cpu().numpy().view(np.uint32), on), (n, kb, keys, K)
+    idx, _ = pbit.sort_array(li.keys, key_bits=kb, digit_bits=K)
+    assert np.array_equal(idx.cpu().numpy().view(np.uint32), np.argsort(workloads.keys_numpy(li), kind="stable"))
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("mode,code", [("ballot", 0), ("match", 1)])
+def test_fallback_rankings_vs_oracle(pbit, mode, code):
+    """The in-warp rankings other than the lane-ordered atomics: the ballot peer masks run
+    if a device's atomic-order self-test ever fails (pbit_rank_mode), match.any on request;
+    both must give the oracle's bytes (subprocess: the mode is decided once per device)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PBIT_RANK=mode, PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", RANK_SNIPPET.format(mode=code)], capture_output=True, text=True,
+                       env=env, cwd=root, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout[-2000:] + r.stderr[-2000:]
