@@ -465,6 +465,15 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   }
 
   // host-side state (declared before the first goto)
+  // NVTX ranges (SURVEY §5 tracing): the call, and each protocol step inside it; the stack
+  // is unwound at `done` whatever step a failure left
+  int nvtx_depth = 1;
+  nvtxRangePushA("pbit_sort_list_mg");
+  auto nvtx_step = [&](const char* name) {
+    if (nvtx_depth > 1) { nvtxRangePop(); --nvtx_depth; }
+    nvtxRangePushA(name);
+    ++nvtx_depth;
+  };
   MgBox* hb = mg_box();
   const Plan& h_plan = hb->plan;
   uint32_t h_left[66] = {}, h_srecv[128] = {}, h_prow[64] = {}, h_psbase[64] = {}, h_precv[128] = {};
@@ -480,6 +489,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     CUDACHK(cudaMemsetAsync(status, 0, ntiles * 256 * 8, st));
 
     // ---- 1. pack the own slice; histograms of every digit of every key
+    nvtx_step("pbit.mg.pack");
     {
       RT* kn_own = replica ? kn_rep + lo : (RT*)win->local;
       if (n_local) {
@@ -501,6 +511,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     }
 
     // ---- 2. walk the own rulers; share the segment table
+    nvtx_step("pbit.mg.walk");
     if (peer) {
       KnSrc<RT> src{};
       for (int q = 0; q < G; ++q) src.peer[q] = (const RT*)wk(q, 0);
@@ -543,6 +554,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     NCCLCHK(ncclAllReduce(err, err, 1, ncclInt32, ncclMax, comm, st));
 
     // ---- 3. rank the ruler list (identical on every rank)
+    nvtx_step("pbit.mg.rank");
     {
       const int sblocks = full_wave(k_rank_walk_a, 256, 0, sms, (nsub + 255) / 256);
       ++launches;
@@ -567,6 +579,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     }
 
     // ---- 4. the list-order chunk of positions [P0, P1)
+    nvtx_step("pbit.mg.chunk");
     if (cudaEventSynchronize(plan_ev) != cudaSuccess) { rc = PBIT_ERR_CUDA; goto done; }
     if (m && (!solo || h_plan.npasses == 0)) {
       const int blocks = std::max(1, std::min((int)((m / 64 + 2 + 255) / 256), sms * 8));
@@ -585,6 +598,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
     if (G > 1) {
       // ---- 5. splitters, bucket counts, exchange plan -- all on the device
+      nvtx_step("pbit.mg.splitters");
       h_split.G = (uint32_t)G;
       h_split.NS = NS;
       for (int d = 0; d < G; ++d) {
@@ -621,6 +635,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       }
 
       // ---- 6. one stable partition pass by splitter bucket, scattered to the destinations
+      nvtx_step("pbit.mg.exchange");
       if (m) {
         SweepArgs sa{};
         sa.kin[0] = keys_c; sa.vin[0] = ids_c;
@@ -661,6 +676,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     // ---- 7. stable local sort of the received runs (the global plan's digits; the bases
     // from the local histogram -- one rank: the global one, and the first pass gathers
     // from the slots)
+    nvtx_step("pbit.mg.local_sort");
     {
       uint32_t* ri_w = const_cast<uint32_t*>(ri);
       KeyT* rk_w = const_cast<KeyT*>(rk);
@@ -690,6 +706,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
 
     // ---- 8. stitch and relink: every rank's first and last sorted id (all-gather), then
     // (v, successor[, predecessor]) routed to the owner of v
+    nvtx_step("pbit.mg.relink");
     ++launches;
     k_first_last_id<<<1, 1, 0, st>>>(fin, m, fl);
     NCCLCHK(ncclAllGather(fl, fl_all, 2, ncclUint32, comm, st));
@@ -766,6 +783,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
     if (launches_out) *launches_out = launches;
   }
 done:
+  while (nvtx_depth-- > 0) nvtxRangePop();
   if (plan_ev) cudaEventDestroy(plan_ev);
   cudaFreeAsync(base, st);
   if (rc != PBIT_ERR_NCCL) cudaStreamSynchronize(st);  // a stuck collective is released by the caller's abort
