@@ -134,8 +134,8 @@ def test_header_is_plain_c_and_the_example_links(pbit, tmp_path):
     (examples/sort_list.c; it runs on a GPU box: tests/test_gpu_parity.py)."""
     import subprocess
     exe = tmp_path / "sort_list"
-    libdir = os.path.dirname(pbit.LIB_PATH)
+    libdir = os.path.dirname(os.path.abspath(pbit.LIB_PATH))
     r = subprocess.run(["cc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(ROOT, "include"),
-                        os.path.join(ROOT, "examples", "sort_list.c"), "-L", libdir, "-l:libpbit.so",
+                        os.path.join(ROOT, "examples", "sort_list.c"), os.path.abspath(pbit.LIB_PATH),
                         f"-Wl,-rpath,{libdir}", "-o", str(exe)], capture_output=True, text=True)
     assert r.returncode == 0, r.stderr

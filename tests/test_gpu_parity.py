@@ -633,9 +633,9 @@ def test_plain_c_example_prints_the_papers_worked_example(pbit, tmp_path):
     import subprocess
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     exe = tmp_path / "sort_list"
-    libdir = os.path.dirname(pbit.LIB_PATH)
+    libdir = os.path.dirname(os.path.abspath(pbit.LIB_PATH))
     subprocess.run(["cc", "-std=c99", "-I", os.path.join(root, "include"), os.path.join(root, "examples", "sort_list.c"),
-                    "-L", libdir, "-l:libpbit.so", f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
+                    os.path.abspath(pbit.LIB_PATH), f"-Wl,-rpath,{libdir}", "-o", str(exe)], check=True)
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert r.stdout.split() == ["3", "3", "14", "21", "47", "156", "209", "214"]
