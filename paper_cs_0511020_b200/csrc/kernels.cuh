@@ -65,6 +65,11 @@ constexpr int SWEEP_IPT32 = PBIT_SWEEP_IPT;                       // items per t
 constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 // write-out of the stable passes: 128-bit stores over 16 B-aligned groups of every digit
 // run (1), or one 4 B store per element, consecutive threads on consecutive elements (0)
+// decoupled lookback: ns to sleep when the nearest predecessor has published nothing new
+// (0 = poll again at once)
+#ifndef PBIT_LB_SLEEP
+#define PBIT_LB_SLEEP 0
+#endif
 // in-warp ranking: branch on the warp-uniform "all lanes share one digit" test (1) or
 // select the addend per lane and skip zero addends (0)
 #ifndef PBIT_RANK_UNIBRANCH
@@ -1102,6 +1107,11 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
         }
         if (done) break;
         hi -= q;
+#if PBIT_LB_SLEEP
+        // nothing new from the nearest predecessor yet: back off instead of re-polling at
+        // once, leaving the issue slots to the other CTA's warps on this SM
+        if (q == 0) __nanosleep(PBIT_LB_SLEEP);
+#endif
       }
       st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (2ull << 32) | (excl + total));
     }
