@@ -114,11 +114,11 @@ typedef struct {
                         (device).  NULL = singly-linked.                           */
     uint32_t *out_order; /* optional (NEXT row N3, record materialisation): the n node ids
                         in sorted order, out_order[i] = w_i (the walk of the sorted list
-                        from *out_head).  Same memory kind as out_next.  pbit_sort_list
-                        only (pbit_sort_list_mg: PBIT_ERR_UNSUPPORTED).             */
+                        from *out_head).  Same memory kind as out_next.
+                        pbit_sort_list_mg: this rank's sorted positions (below).    */
     void *out_keys;  /* optional: the n keys in sorted order, out_keys[i] = keys[w_i]
                         (the input bit patterns, key_bits/8 bytes each).  Same memory
-                        kind as out_next; pbit_sort_list only.  With a payload array,
+                        kind as out_next.  With a payload array,
                         payload[out_order[i]] materialises the sorted records.
                         Neither is written when the list is invalid.                */
 } pbit_opts;
@@ -191,7 +191,9 @@ int pbit_sort_array(const void *keys, uint64_t n, int key_bits, uint32_t *out_in
  * Rank r returns the successors of its own nodes; the sorted positions it computed
  * internally are [r*S, r*S + S) (key-range sharding: exact splitters of the global
  * (key, list position) order, so the shards are equal in size even under heavy duplicates).
- * opts->out_order / out_keys are not supported here (PBIT_ERR_UNSUPPORTED).
+ * opts->out_order / out_keys (device, n_local entries each): this rank's share of the
+ * sorted records -- the node ids and keys at the sorted positions [r*S, r*S + n_local)
+ * (the same count as its node slice); the ranks that own nodes pass them all or none.
  *
  * Transport (PBIT_MG_TRANSPORT, read at every call; pbit_mg_transport reports the one
  * used): "peer" (default) -- every rank maps the others' device memory through CUDA IPC:

@@ -323,7 +323,8 @@ def mg_exchange_plan(nranks: int, rank: int, n: int, slice_: int, lt, le):
 
 def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int, comm: int,
                  key_bits: int | None = None, digit_bits: int = 0, out_next_local=None, stream=None,
-                 key_kind: str | None = None, descending: bool = False, out_prev_local=None):
+                 key_kind: str | None = None, descending: bool = False, out_prev_local=None,
+                 out_order_local=None, out_keys_local=None):
     """Sort one list sharded over the ranks of `comm` (see include/pbit.h).  Returns
     (head, out_next_local)."""
     if key_bits is None:
@@ -337,6 +338,10 @@ def sort_list_mg(keys_local, next_local, head: int, n_global: int, node_lo: int,
     o = _opts(digit_bits, _stream_handle(stream, True), None, None, ctypes.pointer(launches), key_kind, descending)
     if out_prev_local is not None and n_local:
         o.out_prev = ctypes.c_void_p(_ptr(out_prev_local))
+    if out_order_local is not None and n_local:
+        o.out_order = ctypes.c_void_p(_ptr(out_order_local))
+    if out_keys_local is not None and n_local:
+        o.out_keys = ctypes.c_void_p(_ptr(out_keys_local))
     rc = lib.pbit_sort_list_mg(_ptr(keys_local) if n_local else None, _ptr(next_local) if n_local else None,
                                head & 0xFFFFFFFF, n_global, node_lo, n_local, key_bits, ctypes.byref(oh),
                                _ptr(out_next_local) if n_local else None, ctypes.c_void_p(comm), ctypes.byref(o))

@@ -304,7 +304,7 @@ template <int KB>
 int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, uint32_t n, uint32_t S,
            uint32_t n_local, int K, KeyMap km, uint32_t* out_head, uint32_t* out_next_local,
            uint32_t* out_prev_local, bool with_prev, ncclComm_t comm, int G, int r, cudaStream_t st,
-           int transport, uint32_t* launches_out) {
+           int transport, uint32_t* launches_out, uint32_t* out_order_local = nullptr, void* out_keys_local = nullptr) {
   using RT = typename Rec<KB>::T;
   using KeyT = typename KeyOf<KB>::T;
   constexpr int REC_WORDS = sizeof(RT) / 4;
@@ -483,6 +483,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
   const KeyT* rk = nullptr;
   const uint32_t* ri = nullptr;
   const uint32_t* fin = nullptr;
+  const KeyT* fin_k = nullptr;
   {
     CUDACHK(cudaMemsetAsync(base + ctl_off, 0, ctl_end - ctl_off, st));
     CUDACHK(cudaMemsetAsync(seg, 0, sizeof(uint2) * Rmax, st));
@@ -681,6 +682,7 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
       uint32_t* ri_w = const_cast<uint32_t*>(ri);
       KeyT* rk_w = const_cast<KeyT*>(rk);
       fin = ri;
+      fin_k = rk;
       const Plan hp = h_plan;
       if (m && hp.npasses) {
         if (!solo) {
@@ -698,10 +700,20 @@ int run_mg(const void* keys_local, const uint32_t* next_local, uint32_t head, ui
           la.slots = slots_own; la.cap = cap; la.seg = seg; la.seg_ord = seg_ord; la.seg_pos = seg_pos;
           la.tile_first = part_first; la.nseg = nseg;
         }
-        launch_key_passes_k<KB>(K, la, hp, false, st, nullptr, 0, solo ? SRC_GATHER : SRC_TMA);
+        // the last pass keeps the keys when the sorted keys are asked for (N3 records)
+        launch_key_passes_k<KB>(K, la, hp, out_keys_local != nullptr, st, nullptr, 0, solo ? SRC_GATHER : SRC_TMA);
         launches += hp.npasses;
         fin = (hp.npasses & 1u) ? ib1 : ri;
+        fin_k = (hp.npasses & 1u) ? kb1 : rk;
       }
+    }
+
+    // N3 records: this rank's sorted positions [P0, P1) -- ids and keys (skipped for an
+    // invalid list, like every later kernel)
+    if (m && (out_order_local || out_keys_local)) {
+      ++launches;
+      k_materialize<KB><<<std::max(1, std::min((int)((m + 255) / 256), sms * 8)), 256, 0, st>>>(
+          fin, fin_k, m, out_order_local, out_keys_local, km, err);
     }
 
     // ---- 8. stitch and relink: every rank's first and last sorted id (all-gather), then
@@ -936,7 +948,6 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
     if (out_prev_local && out_prev_local == out_next_local) return PBIT_ERR_INVALID_ARG;
     if (!key_kind_ok(km.kind, key_bits)) return PBIT_ERR_INVALID_ARG;
     if (G > 64) return PBIT_ERR_UNSUPPORTED;
-    if (opts && (opts->out_order || opts->out_keys)) return PBIT_ERR_UNSUPPORTED;  // pbit.h: single GPU only
     const uint64_t want_lo = (uint64_t)r * S;
     const uint64_t want_n = n_global > want_lo ? std::min<uint64_t>(S, n_global - want_lo) : 0;
     if (node_lo != want_lo || n_local != want_n) return PBIT_ERR_UNSUPPORTED;
@@ -947,7 +958,9 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
     if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return PBIT_ERR_CUDA; }
     if (n_local && (pointer_kind(keys_local, dev) != 1 || pointer_kind(next_local, dev) != 1 ||
                     pointer_kind(out_next_local, dev) != 1 ||
-                    (out_prev_local && pointer_kind(out_prev_local, dev) != 1)))
+                    (out_prev_local && pointer_kind(out_prev_local, dev) != 1) ||
+                    (opts && opts->out_order && pointer_kind(opts->out_order, dev) != 1) ||
+                    (opts && opts->out_keys && pointer_kind(opts->out_keys, dev) != 1)))
       return PBIT_ERR_INVALID_ARG;
     return PBIT_OK;
   }();
@@ -956,11 +969,15 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
   // without it)
   const uint64_t shared[7] = {n_global, head, (uint64_t)key_bits, (uint64_t)K, (uint64_t)km.kind,
                               (uint64_t)km.descending, (uint64_t)transport_request()};
-  uint64_t flags[2] = {n_local && out_prev_local ? 1ull : 0ull, n_local && !out_prev_local ? 1ull : 0ull};
-  int rc = mg_agree(rc_local, shared, 7, flags, 2, comm, st);
+  uint32_t* out_order_local = opts ? opts->out_order : nullptr;
+  void* out_keys_local = opts ? opts->out_keys : nullptr;
+  uint64_t flags[6] = {n_local && out_prev_local ? 1ull : 0ull, n_local && !out_prev_local ? 1ull : 0ull,
+                       n_local && out_order_local ? 1ull : 0ull, n_local && !out_order_local ? 1ull : 0ull,
+                       n_local && out_keys_local ? 1ull : 0ull, n_local && !out_keys_local ? 1ull : 0ull};
+  int rc = mg_agree(rc_local, shared, 7, flags, 6, comm, st);
   if (rc) return rc;
-  if (flags[0] && flags[1]) {
-    set_last_error("pbit_sort_list_mg", "out_prev passed on some ranks but not on others");
+  if ((flags[0] && flags[1]) || (flags[2] && flags[3]) || (flags[4] && flags[5])) {
+    set_last_error("pbit_sort_list_mg", "out_prev / out_order / out_keys passed on some ranks but not on others");
     return PBIT_ERR_INVALID_ARG;
   }
   const bool with_prev = flags[0] != 0;
@@ -973,7 +990,8 @@ int pbit_sort_list_mg(const void* keys_local, const uint32_t* next_local, uint32
   for (;;) {
 #define PBIT_RUN_MG(KB)                                                                                          \
     run_mg<KB>(keys_local, next_local, head, (uint32_t)n_global, (uint32_t)S, (uint32_t)n_local, K, km, out_head, \
-               out_next_local, out_prev_local, with_prev, comm, G, r, st, transport, opts ? opts->launches : nullptr)
+               out_next_local, out_prev_local, with_prev, comm, G, r, st, transport, opts ? opts->launches : nullptr, \
+               out_order_local, out_keys_local)
     switch (key_bits) {
       case 8: rc = PBIT_RUN_MG(1); break;
       case 16: rc = PBIT_RUN_MG(2); break;

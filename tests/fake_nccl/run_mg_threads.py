@@ -66,13 +66,17 @@ def run_case(G, n, key_bits, keys, links, K, kind, desc, with_prev, seed):
             with torch.cuda.stream(st):
                 comm = p.mg_comm_init(G, uid, r)
                 prev = torch.empty(hi - lo, dtype=torch.int32, device="cuda") if with_prev else None
+                # the sorted records of this rank's positions (N3)
+                order = torch.empty(hi - lo, dtype=torch.int32, device="cuda")
+                skeys = torch.empty_like(li.keys[lo:hi])
                 # node_lo = r * S even for a rank whose slice is empty (pbit.h)
                 h, out = p.sort_list_mg(li.keys[lo:hi], li.next[lo:hi], li.head, n, r * S, comm, key_bits=key_bits,
                                         digit_bits=K, key_kind=kind, descending=desc, stream=st,
-                                        out_prev_local=prev)
+                                        out_prev_local=prev, out_order_local=order, out_keys_local=skeys)
                 st.synchronize()
                 res[r] = (h, out.cpu().numpy().view(np.uint32).copy(),
-                          prev.cpu().numpy().view(np.uint32).copy() if with_prev else None, p.mg_transport(comm))
+                          prev.cpu().numpy().view(np.uint32).copy() if with_prev else None, p.mg_transport(comm),
+                          order.cpu().numpy().view(np.uint32).copy(), skeys.cpu().numpy().copy())
                 p.mg_comm_destroy(comm)
         except Exception as e:  # noqa: BLE001  (reported by the main thread)
             errs[r] = e
@@ -107,6 +111,15 @@ def run_case(G, n, key_bits, keys, links, K, kind, desc, with_prev, seed):
         gp = np.concatenate([r_[2] for r_ in res])
         if not np.array_equal(gp, oracle.repair_back(on, oh)):
             return False, "out_prev differs from the oracle's repair walk", False
+    if n:
+        want_order = oracle.list_order(on, oh)
+        got_order = np.concatenate([r_[4] for r_ in res])
+        if not np.array_equal(got_order, want_order):
+            return False, "out_order differs from the oracle's sorted list", False
+        kn_ = workloads.keys_numpy(li)
+        got_keys = np.concatenate([r_[5] for r_ in res]).view(kn_.dtype)
+        if not np.array_equal(got_keys, kn_[want_order]):
+            return False, "out_keys differ from the keys along the oracle's sorted list", False
     return True, f"ok ({want_t})", False
 
 

@@ -108,3 +108,19 @@ def test_mg_out_prev(mg, n, key_bits, keys):
     oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, key_bits, 4)
     assert h == oh and np.array_equal(out.cpu().numpy().view(np.uint32), on)
     assert np.array_equal(prev.cpu().numpy().view(np.uint32), oracle.repair_back(on, oh))
+
+
+def test_mg_sorted_records(mg):
+    """N3 records through the multi-GPU call: out_order / out_keys of the rank's sorted
+    positions (one rank: all of them) = the oracle's sorted list and its keys."""
+    p, comm = mg
+    li = workloads.make_list(200003, 32, seed=41, keys="zipf", device="cuda")
+    order = torch.empty(li.n, dtype=torch.int32, device="cuda")
+    skeys = torch.empty_like(li.keys)
+    h, out = p.sort_list_mg(li.keys, li.next, li.head, li.n, 0, comm, out_order_local=order, out_keys_local=skeys)
+    torch.cuda.synchronize()
+    oh, on = oracle.pbit_sort(workloads.keys_numpy(li), workloads.next_numpy(li), li.head, 32, 4)
+    want = oracle.list_order(on, oh)
+    assert h == oh and np.array_equal(out.cpu().numpy().view(np.uint32), on)
+    assert np.array_equal(order.cpu().numpy().view(np.uint32), want)
+    assert np.array_equal(skeys.cpu().numpy().view(np.uint32), workloads.keys_numpy(li)[want])
