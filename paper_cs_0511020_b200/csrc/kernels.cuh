@@ -78,6 +78,11 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_VEC_STORE
 #define PBIT_VEC_STORE 0
 #endif
+// pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
+// (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
+#ifndef PBIT_SWEEP_PREFETCH
+#define PBIT_SWEEP_PREFETCH 74
+#endif
 // per-warp digit counters of the pass ranking: u32 (one word per digit: no two digits
 // share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
 using WCnt = std::conditional_t<PBIT_WCNT32 != 0, uint32_t, uint16_t>;
@@ -981,6 +986,20 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     asm volatile("mbarrier.arrive.expect_tx.shared.b64 _, [%0], %1;" ::"r"(m), "r"(kb + ib) : "memory");
     bulk_g2s(sm.k, kin + tile_base, kb, &sm.mbar);
     if (SRC != SRC_IOTA) bulk_g2s(sm.iin, iin + tile_base, ib, &sm.mbar);
+#if PBIT_SWEEP_PREFETCH
+    // warm L2 with the tile a CTA launched about one resident wave later will take (tickets
+    // are handed out in launch order), so its TMA load hits L2 instead of waiting on HBM
+    const uint32_t pt = tile + (uint32_t)PBIT_SWEEP_PREFETCH;
+    if ((size_t)pt * TILE < n) {
+      const uint32_t pc = min((uint32_t)TILE, n - pt * (uint32_t)TILE);
+      const uint32_t pkb = (pc * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(kin + (size_t)pt * TILE), "r"(pkb) : "memory");
+      if (SRC != SRC_IOTA) {
+        const uint32_t pib = (pc * 4u + 15u) & ~15u;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(iin + (size_t)pt * TILE), "r"(pib) : "memory");
+      }
+    }
+#endif
   }
   if (SRC == SRC_IOTA)
     for (uint32_t j = t; j < tile_count; j += SWEEP_THREADS) sm.iin[j] = tile_base + j;
