@@ -50,7 +50,10 @@ constexpr int WALK_THREADS = 256;
 // 256 B 4.22 ms on C4)
 constexpr int WALK_FLUSH_BYTES = PBIT_WALK_FLUSH;
 constexpr int WALK_FLUSH_BYTES64 = PBIT_WALK_FLUSH64;
-constexpr int SWEEP_THREADS = 512;  // 16 warps x 16 items: 8192-item tiles halve the lookback traffic
+#ifndef PBIT_SWEEP_THREADS
+#define PBIT_SWEEP_THREADS 512
+#endif
+constexpr int SWEEP_THREADS = PBIT_SWEEP_THREADS;  // 16 warps x 16 items: 8192-item tiles halve the lookback traffic
 constexpr int SWEEP_WARPS = SWEEP_THREADS / 32;
 #ifndef PBIT_SWEEP_IPT
 #define PBIT_SWEEP_IPT 16
@@ -930,7 +933,7 @@ __device__ __forceinline__ uint32_t split_dest(const SplitTable& sp, uint32_t g)
 }
 
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK, int SRC = SRC_TMA>
-__global__ void __launch_bounds__(SWEEP_THREADS, 2)
+__global__ void __launch_bounds__(SWEEP_THREADS, 1024 / SWEEP_THREADS)
 k_onesweep(const __grid_constant__ SweepArgs a) {
   pdl_enter();
   using S = SweepSmem<KeyT, RADIX_BITS, IPT>;
