@@ -86,6 +86,11 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_SWEEP_PREFETCH
 #define PBIT_SWEEP_PREFETCH 74
 #endif
+// first pass (gather from the walk's slots): prefetch the segment table entries of the tile
+// PBIT_SWEEP_PREFETCH ahead into L2 (1) or not (0)
+#ifndef PBIT_GATHER_META_PREFETCH
+#define PBIT_GATHER_META_PREFETCH 1
+#endif
 // per-warp digit counters of the pass ranking: u32 (one word per digit: no two digits
 // share a word, so ATOMS lanes collide only on equal digits) or u16 pairs (half the smem)
 using WCnt = std::conditional_t<PBIT_WCNT32 != 0, uint32_t, uint16_t>;
@@ -981,6 +986,19 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
   // ---- TMA bulk loads of the tile (sizes rounded up to 16 B; buffers padded to 256 B);
   // the first key pass gathers the tile from the segment slots instead
   constexpr bool GATHER = SRC == SRC_GATHER;
+#if PBIT_GATHER_META_PREFETCH
+  // first pass: warm L2 with the segment table entries (list positions and slots, both in
+  // list-ordinal order) of the tile PBIT_SWEEP_PREFETCH tickets ahead
+  if (GATHER && t == 0) {
+    const uint32_t pt = tile + (uint32_t)PBIT_SWEEP_PREFETCH;
+    if ((size_t)(pt + 1) * TILE < n) {
+      const uint32_t k0 = a.tile_first[pt] & ~3u, k1 = (a.tile_first[pt + 1] + 4u) & ~3u;
+      const uint32_t bytes = min(k1 - k0, 4096u) * 4u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.seg_pos + k0), "r"(bytes) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.seg_ord + k0), "r"(bytes) : "memory");
+    }
+  }
+#endif
   if (GATHER) gather_tile<KeyT, TILE>(a, tile, tile_base, tile_count, sm.k, sm.iin, w, lane, &sm.mbar);
   if (!GATHER && t == 0) {
     const uint32_t kb = (tile_count * (uint32_t)sizeof(KeyT) + 15u) & ~15u;
