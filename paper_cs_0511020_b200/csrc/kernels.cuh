@@ -841,7 +841,13 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
     uint32_t pos = E, r = 0, len = 0;
     if (k < nseg) {
       pos = a.seg_pos[k];
-      if (pos < E) { r = a.seg_ord[k]; len = a.seg[r].x; }
+      // segments in ordinal order tile the list: the k-th one ends where the next starts,
+      // so its length comes from the (sequential, cached) position table instead of a
+      // random load of its segment-table entry (one dependent round trip less)
+      if (pos < E) {
+        r = a.seg_ord[k];
+        len = (k + 1 < nseg ? a.seg_pos[k + 1] : a.n) - pos;
+      }
     }
     uint32_t todo = __ballot_sync(0xffffffffu, pos < E);
     if (!todo) break;
