@@ -583,6 +583,39 @@ def test_concurrent_host_threads_on_own_streams(pbit):
         _assert_same(got[i], want[i], f"thread {i}")
 
 
+def test_concurrent_host_buffer_calls(pbit):
+    """The pipelined e2e of bench.py: host (pinned) buffers sorted from 3 host threads at
+    once, each with its own stream -- every thread's chunked copies run on its own copy
+    stream while another thread's sort runs; each result equals the oracle's."""
+    import threading
+    lists = [workloads.make_list(n, 32, seed=70 + i, keys=k)
+             for i, (n, k) in enumerate((((1 << 20) + 3, "zipf"), (300007, "uniform"), ((1 << 21) - 5, "runs4096")))]
+    want = [_oracle(li) for li in lists]
+    got = [None] * len(lists)
+    errors = []
+
+    def work(i):
+        try:
+            li = lists[i]
+            kh, nh = li.keys.pin_memory(), li.next.pin_memory()
+            oh = torch.empty_like(nh).pin_memory()
+            s = torch.cuda.Stream()
+            for _ in range(3):
+                h, _ = pbit.sort_list(kh, nh, li.head, out_next=oh, stream=s)
+            got[i] = (h, oh.numpy().view(np.uint32).copy())
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(len(lists))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for i in range(len(lists)):
+        _assert_same(got[i], want[i], f"host-buffer thread {i}")
+
+
 # ---------------------------------------------------------------- N3: sorted records (out_order, out_keys)
 @pytest.mark.parametrize("n,key_bits,keys,links,kind,desc", [
     (1, 32, "uniform", "random", "unsigned", False), (1000, 8, "uniform", "random", "unsigned", False),
