@@ -81,6 +81,11 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_VEC_STORE
 #define PBIT_VEC_STORE 0
 #endif
+// in-warp ranking: the "all lanes share one digit" test by match.all (1) or by a shuffle of
+// lane 0's digit and a vote (0)
+#ifndef PBIT_RANK_MATCHALL
+#define PBIT_RANK_MATCHALL 1
+#endif
 // pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
 // (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
 #ifndef PBIT_SWEEP_PREFETCH
@@ -751,8 +756,15 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
       // measured, not documented: checked at load time by k_selftest_atomic_order
       // (pbit.cu), which falls back to RANK_BALLOT if it ever fails.  A warp whose items
       // share one digit (equal-key runs) lets lane 0 add 32 instead of serialising.
+#if PBIT_RANK_MATCHALL
+      // one match.all instead of shfl + compare + vote (an invalid lane never matches)
+      int all_eq = 0;
+      __match_all_sync(0xffffffffu, valid ? d : 0x10000u + lane, &all_eq);
+      const bool uni = all_eq != 0;
+#else
       const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
       const bool uni = __all_sync(0xffffffffu, d == d0 && valid);
+#endif
       uint32_t r = 0;
 #if PBIT_RANK_UNIBRANCH
       // `uni` is warp-uniform: branch on it, so that a full tile's common case (every lane
