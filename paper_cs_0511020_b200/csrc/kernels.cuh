@@ -86,6 +86,11 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_RANK_MATCHALL
 #define PBIT_RANK_MATCHALL 1
 #endif
+// in-warp ranking without a branch around the atomic: lanes with nothing to add hit their
+// own scratch word (1)
+#ifndef PBIT_RANK_PRED
+#define PBIT_RANK_PRED 1
+#endif
 // pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
 // (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
 #ifndef PBIT_SWEEP_PREFETCH
@@ -630,6 +635,7 @@ struct SweepSmem {
   uint32_t goff[RADIX];
   uint32_t gpre[RADIX + 1];  // 128-bit write-out: exclusive scan of each digit run's 16 B groups
   uint32_t scan[SWEEP_WARPS];
+  uint32_t scratch[32];    // the ranking's per-lane words for atomics that add nothing
   uint32_t tile;
   int bad;
   unsigned long long mbar;
@@ -716,7 +722,7 @@ enum : int { RANK_BALLOT = 0, RANK_MATCH = 1, RANK_ATOMIC = 2 };
 template <typename KeyT, int RADIX_BITS, int IPT, int RANK, bool FULL>
 __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd)[IPT], int shift,
                                            WCnt* __restrict__ wrow, uint32_t wofs, uint32_t lane,
-                                           uint32_t tile_count, bool combine = false) {
+                                           uint32_t tile_count, bool combine, uint32_t scratch) {
   constexpr int RADIX = 1 << RADIX_BITS;
   if (RANK == RANK_ATOMIC && combine) {
     // Skewed digits after the first pass: the input is sorted by the lower digits, so a
@@ -724,6 +730,36 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
     // sharing lane 0's digit (eq) take ONE atomic, issued by lane 0 (the lowest lane, so
     // the lane order of the remaining conflicting atomics is unchanged); the other lanes
     // add 1 each as usual.
+#if PBIT_RANK_PRED
+    if constexpr (sizeof(WCnt) == 2) {
+      // branch-free: a lane with nothing to add (in lane 0's group but not lane 0, or past
+      // the tile's end) adds 0 to its own scratch word instead of skipping the atomic, so
+      // every lane issues one ATOMS with no divergent branch around it; the lane mask is
+      // hoisted and in_eq comes from the compare itself
+      const uint32_t lt = lanemask_lt();
+      const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(wrow);
+      const uint32_t mine = scratch + lane * 4u;
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const bool valid = FULL || (wofs + i * 32 + lane < tile_count);
+        const uint32_t d = (uint32_t)(key[i] >> shift) & (RADIX - 1);
+        const uint32_t d0 = __shfl_sync(0xffffffffu, d, 0);
+        const bool in_eq = valid && d == d0;
+        const uint32_t eq = __ballot_sync(0xffffffffu, in_eq);  // valid lanes: a prefix
+        const uint32_t add = lane == 0 ? (uint32_t)__popc(eq) : (valid && !in_eq ? 1u : 0u);
+        const uint32_t sh = (d & 1u) << 4;
+        const uint32_t addr = add ? wbase + ((d >> 1) << 2) : mine;
+        uint32_t old;
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(add << sh) : "memory");
+        uint32_t r = (old >> sh) & 0xFFFFu;
+        const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0);
+        r = in_eq ? r0 + (uint32_t)__popc(eq & lt) : r;
+        rd[i] = r | (d << 16);
+      }
+      return;
+    } else
+#endif
+    {
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const bool valid = FULL || (wofs + i * 32 + lane < tile_count);
@@ -745,6 +781,7 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
       rd[i] = r | (d << 16);
     }
     return;
+    }
   }
 #pragma unroll
   for (int i = 0; i < IPT; ++i) {
@@ -766,6 +803,22 @@ __device__ __forceinline__ void rank_items(const KeyT (&key)[IPT], uint32_t (&rd
       const bool uni = __all_sync(0xffffffffu, d == d0 && valid);
 #endif
       uint32_t r = 0;
+#if PBIT_RANK_PRED
+      if constexpr (sizeof(WCnt) == 2) {
+        // branch-free (see the combining path): lanes 1-31 of an all-equal warp and lanes
+        // past the tile's end add 0 to their own scratch word
+        const uint32_t sh = (d & 1u) << 4;
+        const uint32_t add = uni ? (lane == 0 ? 32u : 0u) : (valid ? 1u : 0u);
+        const uint32_t addr = add ? (uint32_t)__cvta_generic_to_shared(wrow) + ((d >> 1) << 2) : scratch + lane * 4u;
+        uint32_t old;
+        asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(addr), "r"(add << sh) : "memory");
+        r = (old >> sh) & 0xFFFFu;
+        const uint32_t r0 = __shfl_sync(0xffffffffu, r, 0);
+        r = uni ? r0 + lane : r;
+        rd[i] = r | (d << 16);
+        continue;
+      }
+#endif
 #if PBIT_RANK_UNIBRANCH
       // `uni` is warp-uniform: branch on it, so that a full tile's common case (every lane
       // adds 1) issues its atomic without a per-lane predicate or reconvergence barrier
@@ -1068,11 +1121,15 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     uint32_t dg[IPT];
 #pragma unroll
     for (int i = 0; i < IPT; ++i) dg[i] = split_bucket(sp, (unsigned long long)key[i]);
-    if (full_tile) rank_items<uint32_t, RADIX_BITS, IPT, RANK, true>(dg, rd, 0, sm.wcnt[w], wofs, lane, tile_count, combine);
-    else rank_items<uint32_t, RADIX_BITS, IPT, RANK, false>(dg, rd, 0, sm.wcnt[w], wofs, lane, tile_count, combine);
+    if (full_tile) rank_items<uint32_t, RADIX_BITS, IPT, RANK, true>(dg, rd, 0, sm.wcnt[w], wofs, lane, tile_count, combine,
+                                                         (uint32_t)__cvta_generic_to_shared(sm.scratch));
+    else rank_items<uint32_t, RADIX_BITS, IPT, RANK, false>(dg, rd, 0, sm.wcnt[w], wofs, lane, tile_count, combine,
+                                                         (uint32_t)__cvta_generic_to_shared(sm.scratch));
   } else {
-    if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
-    else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine);
+    if (full_tile) rank_items<KeyT, RADIX_BITS, IPT, RANK, true>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine,
+                                                     (uint32_t)__cvta_generic_to_shared(sm.scratch));
+    else rank_items<KeyT, RADIX_BITS, IPT, RANK, false>(key, rd, shift, sm.wcnt[w], wofs, lane, tile_count, combine,
+                                                     (uint32_t)__cvta_generic_to_shared(sm.scratch));
   }
   __syncthreads();
 

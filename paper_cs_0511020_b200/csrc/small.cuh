@@ -61,6 +61,7 @@ k_small_sort(const __grid_constant__ SmallArgs a) {
   __shared__ WCnt wcnt[SMALL_WARPS][RADIX];
   __shared__ uint32_t s_base[RADIX], s_scan[SMALL_WARPS];
   __shared__ int s_trivial;
+  __shared__ uint32_t s_scratch[32];  // rank_items' per-lane words for atomics that add nothing
   __shared__ int s_err;  // this CTA's error bits; combined over the cluster via DSMEM
   __shared__ int s_bad;
 
@@ -149,7 +150,8 @@ k_small_sort(const __grid_constant__ SmallArgs a) {
       const uint32_t j = wofs + i * 32 + lane;
       key[i] = j < cnt ? kin[lo + j] : (KeyT)0;
     }
-    rank_items<KeyT, RADIX_BITS, SMALL_IPT, RANK_ATOMIC, false>(key, rd, dg * RADIX_BITS, wcnt[w], wofs, lane, cnt);
+    rank_items<KeyT, RADIX_BITS, SMALL_IPT, RANK_ATOMIC, false>(key, rd, dg * RADIX_BITS, wcnt[w], wofs, lane, cnt,
+                                                                false, (uint32_t)__cvta_generic_to_shared(s_scratch));
     __syncthreads();
     if (t < RADIX) {  // exclusive prefix over the warps (in place); the CTA's digit counts
       uint32_t tot = 0;
