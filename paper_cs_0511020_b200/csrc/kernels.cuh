@@ -627,9 +627,10 @@ template <typename KeyT, int RADIX_BITS, int IPT>
 struct SweepSmem {
   static constexpr int RADIX = 1 << RADIX_BITS;
   static constexpr int TILE = SWEEP_THREADS * IPT;
-  KeyT k[TILE];            // input keys, later the staged output keys
+  KeyT k[TILE + 32];       // input keys, later the staged output keys (+ a word per lane
+                           // for the staging stores of items past the last tile's end)
   uint32_t iin[TILE];      // input ids
-  uint32_t iout[TILE];     // staged output ids
+  uint32_t iout[TILE + 32];  // staged output ids (+ the same scratch words)
   WCnt wcnt[SWEEP_WARPS][RADIX];
   uint32_t dstart[RADIX];
   uint32_t goff[RADIX];
@@ -1167,6 +1168,9 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 
   // ---- stage in (digit, input order) order: keys from registers into sm.k (every warp
   // read its keys before the barriers above), values from sm.iin into sm.iout
+  // (non-AOS passes: an item past the last tile's end is staged into its lane's scratch
+  // slot, index TILE + lane, instead of being skipped -- no branch per item; the AOS first
+  // pass keeps the branch, measured faster there)
   if constexpr (AOS) {
     // ids first (they live in the records the keys will overwrite), then the keys
 #pragma unroll
@@ -1189,15 +1193,12 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 #pragma unroll
     for (int i = 0; i < IPT; ++i) {
       const uint32_t j = wofs + i * 32 + lane;
-      if (full_tile || j < tile_count) {
-        const uint32_t d = rd[i] >> 16;
-        const uint32_t lp = sm.wcnt[w][d] + (rd[i] & 0xFFFFu);
-        sm.iout[lp] = sm.iin[j];
-        sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass needs only digits
-      }
+      const uint32_t d = rd[i] >> 16;
+      const uint32_t lp = (full_tile || j < tile_count) ? sm.wcnt[w][d] + (rd[i] & 0xFFFFu) : (uint32_t)TILE + lane;
+      sm.iout[lp] = sm.iin[j];
+      sm.k[lp] = last ? (KeyT)d : key[i];  // the last key pass needs only digits
     }
   }
-
   // ---- decoupled lookback, one thread per digit value, LB_WIN predecessors per step
   uint32_t ngrp = 0;  // 16 B-aligned groups of 4 output slots the digit's run touches
   if (t < RADIX) {
