@@ -26,7 +26,9 @@ def phase_of(name: str, onesweep_idx: int, key_passes: int) -> str:
     if "k_gather" in name or "k_plan" in name:
         return "gather"
     if "k_onesweep" in name:
-        return f"pass{onesweep_idx}" if onesweep_idx < key_passes else "relink"
+        # every k_onesweep launch of a list sort is a key pass (u64 keys: up to 8); the
+        # relink has kernels of its own
+        return f"pass{onesweep_idx}"
     if "k_relink" in name:
         return "relink"
     if "k_selftest" in name:
