@@ -91,6 +91,16 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_RANK_PRED
 #define PBIT_RANK_PRED 1
 #endif
+// pass kernel: the per-digit scan keeps the warps' exclusive prefixes in registers (1)
+// instead of writing them to the warp counters and re-reading them (0)
+#ifndef PBIT_SCAN_REG
+#define PBIT_SCAN_REG 0
+#endif
+// pass 0 gather: lanes copy their own even-aligned segments by TMA in parallel (1) instead
+// of the whole warp taking every segment in turn (0)
+#ifndef PBIT_GATHER_LANEBULK
+#define PBIT_GATHER_LANEBULK 0
+#endif
 // pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
 // (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
 #ifndef PBIT_SWEEP_PREFETCH
@@ -917,6 +927,28 @@ __device__ __forceinline__ void gather_tile(const SweepArgs& a, uint32_t tile, u
     }
     uint32_t todo = __ballot_sync(0xffffffffu, pos < E);
     if (!todo) break;
+#if PBIT_GATHER_LANEBULK
+    if constexpr (!WIDE && PBIT_GATHER_BULK) {
+      // every lane whose segment starts at an even list position copies it itself: one
+      // TMA bulk copy of the aligned middle plus <= 2 edge records, no warp-serial step;
+      // the warp-cooperative loop below takes only the odd-aligned (and short) segments
+      const uint32_t lo = max(P, pos), hi = min(E, pos + len);
+      const bool mine = pos < E && (pos & 1u) == 0u && hi >= lo + 4u;
+      if (mine) {
+        const uint32_t a0 = (lo + 1u) & ~1u, a1 = hi & ~1u;
+        PBIT_ASSERT(hi - P <= (uint32_t)TILE && len <= cap);
+        const uint2* src = reinterpret_cast<const uint2*>(slots) + (size_t)r * cap;
+        uint2* dst = reinterpret_cast<uint2*>(sk);
+        const uint32_t bytes = (a1 - a0) * 8u;
+        const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+        bulk_g2s(dst + (a0 - P), src + (a0 - pos), bytes, mbar);
+        if (lo < a0) cp_async8(dst + (lo - P), src + (lo - pos));
+        if (a1 < hi) cp_async8(dst + (a1 - P), src + (a1 - pos));
+      }
+      todo &= ~__ballot_sync(0xffffffffu, mine);
+    }
+#endif
     while (todo) {
       const int q = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -1136,6 +1168,23 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
 
   // ---- per digit (thread t = digit t): exclusive over warps, tile total, aggregate
   uint32_t total = 0;
+#if PBIT_SCAN_REG
+  // the warps' exclusive prefixes stay in registers (two u16 per word) until the tile's
+  // digit start is known: one read and one write of each warp counter instead of two each
+  constexpr int NPW = (SWEEP_WARPS + 1) / 2;
+  uint32_t wpre[NPW];
+#pragma unroll
+  for (int q = 0; q < NPW; ++q) wpre[q] = 0;
+  if (t < RADIX) {
+#pragma unroll
+    for (int ww = 0; ww < SWEEP_WARPS; ++ww) {
+      const uint32_t c = sm.wcnt[ww][t];
+      wpre[ww >> 1] |= total << ((ww & 1) * 16);
+      total += c;
+    }
+    if (tile > 0) st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (1ull << 32) | total);
+  }
+#else
   if (t < RADIX) {
 #pragma unroll
     for (int ww = 0; ww < SWEEP_WARPS; ++ww) {
@@ -1145,6 +1194,7 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     }
     if (tile > 0) st_relaxed_u64(status + (size_t)tile * RADIX + t, (epoch << 34) | (1ull << 32) | total);
   }
+#endif
   {
     uint32_t x = total;
 #pragma unroll
@@ -1160,8 +1210,13 @@ k_onesweep(const __grid_constant__ SweepArgs a) {
     if (t < RADIX) {
       const uint32_t ds = x - total + add;
       sm.dstart[t] = ds;
+#if PBIT_SCAN_REG
+#pragma unroll
+      for (int ww = 0; ww < SWEEP_WARPS; ++ww) sm.wcnt[ww][t] = (WCnt)(((wpre[ww >> 1] >> ((ww & 1) * 16)) & 0xFFFFu) + ds);
+#else
 #pragma unroll
       for (int ww = 0; ww < SWEEP_WARPS; ++ww) sm.wcnt[ww][t] = (WCnt)(sm.wcnt[ww][t] + ds);
+#endif
     }
   }
   __syncthreads();
