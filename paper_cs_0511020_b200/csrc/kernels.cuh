@@ -94,12 +94,12 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 // pass kernel: the per-digit scan keeps the warps' exclusive prefixes in registers (1)
 // instead of writing them to the warp counters and re-reading them (0)
 #ifndef PBIT_SCAN_REG
-#define PBIT_SCAN_REG 0
+#define PBIT_SCAN_REG 1
 #endif
 // pass 0 gather: lanes copy their own even-aligned segments by TMA in parallel (1) instead
 // of the whole warp taking every segment in turn (0)
 #ifndef PBIT_GATHER_LANEBULK
-#define PBIT_GATHER_LANEBULK 0
+#define PBIT_GATHER_LANEBULK 1
 #endif
 // pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
 // (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
