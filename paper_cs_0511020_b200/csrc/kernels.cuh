@@ -101,6 +101,10 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_GATHER_LANEBULK
 #define PBIT_GATHER_LANEBULK 1
 #endif
+// relink partition: the next tile's bin claims issued before the current tile's write-out (1)
+#ifndef PBIT_PART_PIPE
+#define PBIT_PART_PIPE 0
+#endif
 // pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
 // (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
 #ifndef PBIT_SWEEP_PREFETCH
@@ -1527,6 +1531,9 @@ struct PartSmem {
   R in[2][TILE];  // double-buffered tile loads (FROM_IDS: u32 ids + 4 look-behind + 4 look-ahead)
   R stage[TILE];  // the tile in bin order
   uint32_t cnt[256], start[256], gofs[256], warp[PART_THREADS / 32];
+#if PBIT_PART_PIPE
+  uint32_t cnt2[2][256], start2[2][256];  // per-slot counts / starts of the pipelined loop
+#endif
   unsigned long long mbar[2];
 };
 
@@ -1571,8 +1578,127 @@ k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* 
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+#if PBIT_PART_PIPE
+    if (blockIdx.x + gridDim.x < ntiles) issue(blockIdx.x + gridDim.x, 1);
+#endif
   }
   __syncthreads();
+#if PBIT_PART_PIPE
+  // Software-pipelined: the global bin claims of the CTA's next tile are issued before the
+  // current tile is written out and consumed one tile later, so their L2 round trip is off
+  // the tile's critical path.  Every bin's records stay one dense run per tile (the record
+  // order inside a bin is free: the apply scatters by v).
+  {
+    R x[IPT];
+    uint32_t r[IPT];
+    auto wait_tile = [&](uint32_t q) {
+      const uint32_t m = (uint32_t)__cvta_generic_to_shared(&sm.mbar[q & 1u]);
+      const uint32_t par = (q >> 1) & 1u;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(m), "r"(par) : "memory");
+    };
+    // items of the CTA's q-th tile into registers, ranked on the slot's bin counters
+    auto load_rank = [&](uint32_t q, uint32_t tile) {
+      const uint32_t base = lo + tile * (uint32_t)TILE;
+      const uint32_t cnt = min((uint32_t)TILE, n - base);
+      const uint32_t* in_ids = reinterpret_cast<const uint32_t*>(&sm.in[q & 1u][0]);
+      const uint32_t off = (FROM_IDS && W == 3 && base >= 4u) ? 4u : 0u;
+      uint32_t* c = sm.cnt2[q & 1u];
+#pragma unroll
+      for (int i = 0; i < IPT; ++i) {
+        const uint32_t j = i * PART_THREADS + t;
+        if (j < cnt) {
+          if constexpr (FROM_IDS) {
+            x[i].x = in_ids[off + j];
+            x[i].y = base + j + 1 < n ? in_ids[off + j + 1] : PBIT_NULL32;
+            if constexpr (W == 3) x[i].z = base + j > 0 ? in_ids[off + j - 1] : PBIT_NULL32;
+          } else {
+            x[i] = sm.in[q & 1u][j];
+            x[i].x -= v_off;
+          }
+          r[i] = atomicAdd(&c[(x[i].x >> shift) & mask], 1u);
+        }
+      }
+    };
+    // exclusive scan of a tile's bin counts (start2[slot]) and its claims (returned, t < nb)
+    auto scan_claim = [&](uint32_t q, uint32_t tile, uint32_t& claim, uint32_t& my_start) {
+      const uint32_t base = lo + tile * (uint32_t)TILE;
+      const uint32_t parent = FROM_IDS ? 0u : base >> (shift + bits);
+      const uint32_t c = t < nb ? sm.cnt2[q & 1u][t] : 0u;
+      uint32_t y = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= (uint32_t)o) y += z;
+      }
+      if (lane == 31) sm.warp[w] = y;
+      __syncthreads();
+      uint32_t add = 0;
+      for (uint32_t qq = 0; qq < w; ++qq) add += sm.warp[qq];
+      claim = 0;
+      my_start = 0;
+      if (t < nb) {
+        my_start = y - c + add;
+        sm.start2[q & 1u][t] = my_start;
+        if (c) claim = atomicAdd(cursor + ((parent << bits) | t), c);
+      }
+    };
+    uint32_t tile = blockIdx.x;
+    if (tile < ntiles) {
+      if (t < 256) { sm.cnt2[0][t] = 0; sm.cnt2[1][t] = 0; }
+      wait_tile(0);
+      __syncthreads();
+      load_rank(0, tile);
+      __syncthreads();
+      if (t == 0 && tile + 2u * gridDim.x < ntiles) issue(tile + 2u * gridDim.x, 0);  // buffer 0 is consumed
+      uint32_t claim_cur, start_cur;
+      scan_claim(0, tile, claim_cur, start_cur);
+      __syncthreads();
+      for (uint32_t q = 0;; ++q) {
+        const uint32_t s = q & 1u;
+        const uint32_t base = lo + tile * (uint32_t)TILE;
+        const uint32_t cnt = min((uint32_t)TILE, n - base);
+        const uint32_t parent = FROM_IDS ? 0u : base >> (shift + bits);
+        // stage tile q in bin order
+#pragma unroll
+        for (int i = 0; i < IPT; ++i) {
+          const uint32_t j = i * PART_THREADS + t;
+          if (j < cnt) sm.stage[sm.start2[s][(x[i].x >> shift) & mask] + r[i]] = x[i];
+        }
+        if (t < 256) sm.cnt2[s][t] = 0;  // tile q's counts were read by its scan (barriers since)
+        if (t < nb) sm.gofs[t] = (((parent << bits) | t) << shift) + claim_cur - start_cur;
+        const uint32_t next = tile + gridDim.x;
+        const bool has_next = next < ntiles;  // CTA-uniform
+        __syncthreads();  // stage and gofs of tile q visible; slot s counters zeroed
+        uint32_t claim_nx = 0, start_nx = 0;
+        if (has_next) {
+          wait_tile(q + 1);
+          load_rank(q + 1, next);
+          __syncthreads();
+          if (t == 0 && next + 2u * gridDim.x < ntiles) issue(next + 2u * gridDim.x, (q + 1) & 1u);
+          scan_claim(q + 1, next, claim_nx, start_nx);  // the claims are consumed one tile later
+        }
+        // coalesced write-out of tile q
+#pragma unroll 4
+        for (uint32_t j = t; j < cnt; j += PART_THREADS) {
+          const R p = sm.stage[j];
+          const uint32_t b = (p.x >> shift) & mask;
+          PBIT_ASSERT(sm.gofs[b] + j < n);
+          if constexpr (W == 2) __stcs(pout + (sm.gofs[b] + j), p);
+          else pout[sm.gofs[b] + j] = p;
+        }
+        __syncthreads();  // stage and gofs are rewritten for tile q + 1
+        if (!has_next) break;
+        claim_cur = claim_nx;
+        start_cur = start_nx;
+        tile = next;
+      }
+    }
+    return;
+  }
+#endif
   uint32_t it = 0;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int buf = it & 1;
