@@ -105,6 +105,9 @@ constexpr int SWEEP_IPT64 = PBIT_SWEEP_IPT64;  // 64-bit keys
 #ifndef PBIT_PART_PIPE
 #define PBIT_PART_PIPE 0
 #endif
+#ifndef PBIT_PP_DBG
+#define PBIT_PP_DBG 0  // bisection knobs of the pipelined loop: 1 proxy fence, 2 claims after the write-out, 4 serial
+#endif
 // pass kernel: tiles ahead of its own whose keys and ids a CTA prefetches into L2
 // (cp.async.bulk.prefetch.L2), about one resident wave (0 = none)
 #ifndef PBIT_SWEEP_PREFETCH
@@ -1673,13 +1676,27 @@ k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* 
         const bool has_next = next < ntiles;  // CTA-uniform
         __syncthreads();  // stage and gofs of tile q visible; slot s counters zeroed
         uint32_t claim_nx = 0, start_nx = 0;
-        if (has_next) {
-          wait_tile(q + 1);
-          load_rank(q + 1, next);
-          __syncthreads();
-          if (t == 0 && next + 2u * gridDim.x < ntiles) issue(next + 2u * gridDim.x, (q + 1) & 1u);
-          scan_claim(q + 1, next, claim_nx, start_nx);  // the claims are consumed one tile later
-        }
+        auto prep_next = [&](int part) {  // part 1: load + rank + refill, part 2: scan + claims
+          if (!has_next) return;
+          if (part & 1) {
+            wait_tile(q + 1);
+            load_rank(q + 1, next);
+            __syncthreads();
+#if PBIT_PP_DBG & 1
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+#endif
+            if (t == 0 && next + 2u * gridDim.x < ntiles) issue(next + 2u * gridDim.x, (q + 1) & 1u);
+          }
+          if (part & 2) scan_claim(q + 1, next, claim_nx, start_nx);  // consumed one tile later
+        };
+#if PBIT_PP_DBG & 4
+        (void)0;
+#elif PBIT_PP_DBG & 2
+        prep_next(1);
+#else
+        prep_next(3);
+#endif
         // coalesced write-out of tile q
 #pragma unroll 4
         for (uint32_t j = t; j < cnt; j += PART_THREADS) {
@@ -1689,6 +1706,13 @@ k_relink_part(const uint32_t* __restrict__ ids, const typename RelinkRec<W>::T* 
           if constexpr (W == 2) __stcs(pout + (sm.gofs[b] + j), p);
           else pout[sm.gofs[b] + j] = p;
         }
+#if PBIT_PP_DBG & 4
+        __syncthreads();
+        prep_next(3);
+#elif PBIT_PP_DBG & 2
+        __syncthreads();
+        prep_next(2);
+#endif
         __syncthreads();  // stage and gofs are rewritten for tile q + 1
         if (!has_next) break;
         claim_cur = claim_nx;
